@@ -1,0 +1,271 @@
+"""Trace event model, text formats, and the struct-of-arrays ingest form.
+
+Mirrors the reference trace module (pkg/src/memplan/trace.py:1-192): the
+same ``EventKind``/``TraceEvent``/``Trace`` types, the JSONL/CSV formats
+with identical error lines, and ``validate_trace``.  What is new is
+``TraceArrays``: the columnar layout every device kernel consumes
+(``kind u8 | var i32 | size i64 | t_us i64``, 21 B/event), built once per
+trace and cached on the ``Trace`` object.
+
+Variable ids are interned in *lexicographic order of the name strings*, so
+an id comparison is a name comparison (Python ``str`` order is code-point
+order, equal to UTF-8 byte order).  The UTF-8 name bytes travel with the
+arrays so the device can order the rare ``base#alloc`` renames exactly.
+"""
+from __future__ import annotations
+
+import csv
+import io
+import json
+from dataclasses import dataclass, field
+from enum import Enum
+from typing import Iterable, Iterator, Sequence
+
+import numpy as np
+
+from .errors import InvariantViolation, MalformedRecord
+
+JSONL_KEYS = ("index", "t_us", "kind", "var", "size")
+CSV_HEADER = "index,t_us,kind,var,size"
+
+# kind codes shared with include/memplan_b200.h (MP_MALLOC ...)
+KIND_CODE = {"malloc": 0, "free": 1, "read": 2, "write": 3}
+
+
+class EventKind(str, Enum):
+    MALLOC = "malloc"
+    FREE = "free"
+    READ = "read"
+    WRITE = "write"
+
+
+KIND_BY_CODE = (EventKind.MALLOC, EventKind.FREE, EventKind.READ, EventKind.WRITE)
+_CODE_OF_KIND = {k: i for i, k in enumerate(KIND_BY_CODE)}
+
+
+@dataclass(frozen=True)
+class TraceEvent:
+    index: int
+    t_us: int
+    kind: EventKind
+    var: str
+    size: int = 0
+
+
+@dataclass
+class Trace:
+    events: list[TraceEvent]
+    meta: dict = field(default_factory=dict)
+
+    def __len__(self) -> int:
+        return len(self.events)
+
+    def __iter__(self) -> Iterator[TraceEvent]:
+        return iter(self.events)
+
+    def __getitem__(self, i):
+        return self.events[i]
+
+
+# ---------------------------------------------------------------------------
+# columnar form
+
+
+class TraceArrays:
+    """Struct-of-arrays view of one trace (host numpy, C-contiguous).
+
+    ``names[i]`` is the string of var id ``i``; ids are sorted by name.
+    ``index`` is kept only when it differs from the position (unvalidated
+    input), so the validator can report the reference's first error.
+    """
+
+    __slots__ = ("kind", "var", "size", "t_us", "index", "names",
+                 "name_blob", "name_off", "_meta")
+
+    def __init__(self, kind, var, size, t_us, names: Sequence[str],
+                 index=None):
+        self.kind = np.ascontiguousarray(kind, dtype=np.uint8)
+        self.var = np.ascontiguousarray(var, dtype=np.int32)
+        self.size = np.ascontiguousarray(size, dtype=np.int64)
+        self.t_us = np.ascontiguousarray(t_us, dtype=np.int64)
+        self.index = None if index is None else np.ascontiguousarray(index, dtype=np.int64)
+        self.names = list(names)
+        blobs = [s.encode("utf-8") for s in self.names]
+        off = np.zeros(len(blobs) + 1, dtype=np.int64)
+        if blobs:
+            off[1:] = np.cumsum([len(b) for b in blobs])
+        self.name_off = off
+        self.name_blob = np.frombuffer(b"".join(blobs) or b"\0", dtype=np.uint8).copy()
+        self._meta = None
+
+    def __len__(self) -> int:
+        return int(self.kind.shape[0])
+
+    @property
+    def nvars(self) -> int:
+        return len(self.names)
+
+    @classmethod
+    def from_columns(cls, kind, var_names, size, t_us, index=None) -> "TraceArrays":
+        """Intern an array of var-name strings in lexicographic id order."""
+        arr = np.asarray(var_names, dtype=object)
+        if arr.size == 0:
+            return cls(np.zeros(0, np.uint8), np.zeros(0, np.int32),
+                       np.zeros(0, np.int64), np.zeros(0, np.int64), [], index)
+        uniq, inv = np.unique(arr.astype(str), return_inverse=True)
+        return cls(kind, inv.astype(np.int32), size, t_us, [str(u) for u in uniq], index)
+
+    def to_trace(self) -> Trace:
+        names = self.names
+        ev = [TraceEvent(index=i, t_us=int(t), kind=KIND_BY_CODE[int(k)],
+                         var=names[int(v)], size=int(s))
+              for i, (k, v, s, t) in enumerate(zip(self.kind.tolist(), self.var.tolist(),
+                                                   self.size.tolist(), self.t_us.tolist()))]
+        return Trace(events=ev)
+
+
+def _events_to_arrays(events: Sequence[TraceEvent]) -> TraceArrays:
+    n = len(events)
+    kind = np.empty(n, dtype=np.uint8)
+    size = np.empty(n, dtype=np.int64)
+    t_us = np.empty(n, dtype=np.int64)
+    index = np.empty(n, dtype=np.int64)
+    names = [None] * n
+    code = _CODE_OF_KIND
+    for i, ev in enumerate(events):
+        kind[i] = code[EventKind(ev.kind)]
+        size[i] = ev.size
+        t_us[i] = ev.t_us
+        index[i] = ev.index
+        names[i] = ev.var
+    contiguous = n == 0 or bool(np.array_equal(index, np.arange(n, dtype=np.int64)))
+    return TraceArrays.from_columns(kind, names, size, t_us,
+                                    None if contiguous else index)
+
+
+def as_arrays(trace) -> TraceArrays:
+    """Columnar view of a Trace (cached on the object) or TraceArrays."""
+    if isinstance(trace, TraceArrays):
+        return trace
+    events = trace.events if isinstance(trace, Trace) else list(trace)
+    key = (id(events), len(events))
+    if isinstance(trace, Trace):
+        cached = trace.__dict__.get("_mp_arrays")
+        if cached is not None and cached[0] == key:
+            return cached[1]
+    arrays = _events_to_arrays(events)
+    if isinstance(trace, Trace):
+        trace.__dict__["_mp_arrays"] = (key, arrays)
+    return arrays
+
+
+def validate_trace(events: Iterable[TraceEvent]) -> None:
+    """Check the stream invariants on the device (trace.py:55-84).
+
+    Raises InvariantViolation at the first failing event with the
+    reference's reason text.
+    """
+    from . import _native
+    arrays = as_arrays(events if isinstance(events, (Trace, TraceArrays)) else list(events))
+    _native.validate(arrays)
+
+
+# ---------------------------------------------------------------------------
+# text formats (host-side plumbing; trace.py:87-192)
+
+
+def _record(line_no: int, index, t_us, kind, var, size) -> TraceEvent:
+    try:
+        index, t_us, size = int(index), int(t_us), int(size)
+    except (TypeError, ValueError):
+        raise MalformedRecord(line_no, "index/t_us/size must be integers")
+    try:
+        kind = EventKind(kind)
+    except ValueError:
+        raise MalformedRecord(line_no, f"unknown kind {kind!r}")
+    if not isinstance(var, str) or not var:
+        raise MalformedRecord(line_no, "var must be a non-empty string")
+    return TraceEvent(index=index, t_us=t_us, kind=kind, var=var, size=size)
+
+
+def _read_jsonl(text: str) -> list[TraceEvent]:
+    out = []
+    want = set(JSONL_KEYS)
+    for line_no, line in enumerate(text.splitlines(), start=1):
+        if not line.strip():
+            continue
+        try:
+            rec = json.loads(line)
+        except json.JSONDecodeError as exc:
+            raise MalformedRecord(line_no, f"bad JSON: {exc.msg}")
+        if not isinstance(rec, dict) or set(rec) != want:
+            raise MalformedRecord(line_no, f"keys must be exactly {want}")
+        out.append(_record(line_no, *(rec[k] for k in JSONL_KEYS)))
+    return out
+
+
+def _read_csv(text: str) -> list[TraceEvent]:
+    rows = csv.reader(io.StringIO(text))
+    header = next(rows, None)
+    if header is None:
+        raise MalformedRecord(1, "empty file, header required")
+    if header != CSV_HEADER.split(","):
+        raise MalformedRecord(1, f"header must be {CSV_HEADER!r}")
+    out = []
+    for line_no, row in enumerate(rows, start=2):
+        if not row:
+            continue
+        if len(row) != 5:
+            raise MalformedRecord(line_no, f"expected 5 fields, got {len(row)}")
+        out.append(_record(line_no, *row))
+    return out
+
+
+def parse_trace(data: bytes | str, format: str = "jsonl") -> Trace:
+    """Decode JSONL/CSV text and validate it (trace.py:140-151)."""
+    if isinstance(data, bytes):
+        data = data.decode("utf-8")
+    if format == "jsonl":
+        events = _read_jsonl(data)
+    elif format == "csv":
+        events = _read_csv(data)
+    else:
+        raise ValueError(f"unknown format {format!r}")
+    trace = Trace(events=events)
+    validate_trace(trace)
+    return trace
+
+
+def serialize_trace(trace: Trace, format: str = "jsonl") -> str:
+    """Canonical text form; parse(serialize(t)) round-trips byte-exactly."""
+    if format == "jsonl":
+        lines = [json.dumps({"index": e.index, "t_us": e.t_us, "kind": e.kind.value,
+                             "var": e.var, "size": e.size}, separators=(",", ":"))
+                 for e in trace.events]
+        return "\n".join(lines) + ("\n" if lines else "")
+    if format == "csv":
+        buf = io.StringIO()
+        w = csv.writer(buf, lineterminator="\n")
+        w.writerow(CSV_HEADER.split(","))
+        for e in trace.events:
+            w.writerow([e.index, e.t_us, e.kind.value, e.var, e.size])
+        return buf.getvalue()
+    raise ValueError(f"unknown format {format!r}")
+
+
+def _fmt_of(path: str, format: str | None) -> str:
+    if format is not None:
+        return format
+    return "csv" if path.endswith(".csv") else "jsonl"
+
+
+def load_trace(path, format: str | None = None) -> Trace:
+    path = str(path)
+    with open(path, "rb") as fh:
+        return parse_trace(fh.read(), format=_fmt_of(path, format))
+
+
+def save_trace(trace: Trace, path, format: str | None = None) -> None:
+    path = str(path)
+    with open(path, "w", encoding="utf-8") as fh:
+        fh.write(serialize_trace(trace, format=_fmt_of(path, format)))
