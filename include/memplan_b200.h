@@ -1,0 +1,189 @@
+/*
+ * memplan_b200.h — C ABI of the B200-native memplan hot path.
+ *
+ * The drop-in boundary: the reference exposes this path as Python
+ * functions of the `memplan` package (pkg/src/memplan/__init__.py:92-166).
+ * Each entry point below replaces one of them; the Python package
+ * `paper_1903_06631_b200` binds these symbols with ctypes and re-exposes
+ * the reference's names, dataclasses and exceptions.
+ *
+ * Conventions
+ *   - every call returns an int32 status: 0 = MP_OK, otherwise an MP_E_*
+ *     code; details land in the caller's mp_err (may be NULL).
+ *   - inputs are caller-owned, C-contiguous host arrays borrowed for the
+ *     call; results go to caller-allocated host arrays sized from the
+ *     *_dims queries, or stay device-resident behind an opaque handle.
+ *   - variable ids are dense int32 ranks of the variable-name strings in
+ *     lexicographic order; the UTF-8 names (blob + offsets) travel with the
+ *     trace so renamed instances ("base#alloc", iteration.py:236-241) can be
+ *     ordered exactly on the device.
+ *   - all floating point is IEEE binary64 with no contraction (-fmad=false)
+ *     and the reference's left-fold order, so results are bit-identical.
+ *   - kind codes: 0 malloc, 1 free, 2 read, 3 write (trace.py:24-28).
+ */
+#ifndef MEMPLAN_B200_H
+#define MEMPLAN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MP_MALLOC 0
+#define MP_FREE 1
+#define MP_READ 2
+#define MP_WRITE 3
+
+/* status codes; mapping to the reference exceptions in errors.py */
+enum {
+  MP_OK = 0,
+  MP_E_INVARIANT = 1,        /* InvariantViolation(index, reason)   errors.py:20 */
+  MP_E_PERIOD_NOT_FOUND = 2, /* PeriodNotFound                      errors.py:36 */
+  MP_E_LIMIT_UNREACHABLE = 3,/* LimitUnreachable(limit, achievable) errors.py:48 */
+  MP_E_SWAP_DEADLOCK = 4,    /* SwapDeadlock(index, reason)         errors.py:62 */
+  MP_E_SIM_INDEXERROR = 5,   /* reference defect swapsim.py:266-276 raises IndexError */
+  MP_E_VALUE = 6,            /* ValueError (bad window / policy / score)          */
+  MP_E_CUDA = 7,             /* CUDA runtime failure (no silent fallback)         */
+  MP_E_NOMEM = 8,
+  MP_E_UNSUPPORTED = 9
+};
+
+/* InvariantViolation reason codes (mp_err.aux0); reason text is formatted
+ * by the host with the variable name in aux1 (a var id). */
+enum {
+  MP_V_INDEX = 1,        /* "index {index} not contiguous"   trace.py:64-65 (aux1 = bad index) */
+  MP_V_NEG_T = 2,        /* "negative timestamp"              trace.py:66-67 */
+  MP_V_T_DEC = 3,        /* "timestamp decreases"             trace.py:68-69 */
+  MP_V_MALLOC_SIZE = 4,  /* "malloc size must be > 0"         trace.py:72-73 */
+  MP_V_MALLOC_LIVE = 5,  /* "malloc of live id {var!r}"       trace.py:74-75 */
+  MP_V_SIZE_NONZERO = 6, /* "{kind} size must be 0"           trace.py:78-79 (aux1 = kind) */
+  MP_V_FREE_DEAD = 7,    /* "free of dead id {var!r}"         trace.py:80-82 */
+  MP_V_USE_DEAD = 8,     /* "use of dead id {var!r}"          trace.py:80-82 */
+  MP_V_W_MALLOC_LIVE = 9,/* "malloc of live id {base!r} in window" iteration.py:161-162 */
+  MP_V_W_FREE_DEAD = 10, /* "free of dead id {base!r} in window"   iteration.py:177-178 */
+  MP_V_W_USE_DEAD = 11   /* "use of dead id {base!r} in window"    iteration.py:184-185 */
+};
+
+typedef struct mp_err {
+  int32_t code;
+  int32_t trace; /* batch member the error belongs to */
+  int64_t index;
+  int64_t aux0;
+  int64_t aux1;
+  char msg[192];
+} mp_err;
+
+/* One trace in struct-of-arrays form (host memory). */
+typedef struct mp_trace_in {
+  int64_t n;
+  const uint8_t *kind;
+  const int32_t *var;
+  const int64_t *size;
+  const int64_t *t_us;
+  const int64_t *index;     /* NULL when index == position */
+  int32_t nvars;
+  const uint8_t *name_blob; /* names of var ids, concatenated UTF-8 */
+  const int64_t *name_off;  /* nvars + 1 offsets into name_blob */
+} mp_trace_in;
+
+/* Iteration profile (iteration.py:63-90) in flat form.  Variables are in
+ * the reference order (alloc or -1, name) (iteration.py:257-260): the
+ * `ncarry` carry-ins first, then window instances by alloc index. */
+typedef struct mp_profile_dims {
+  int64_t period, nvars, ncarry, naccess;
+  int64_t peak_bytes, peak_index;
+  double duration_us;
+} mp_profile_dims;
+
+#define MP_F_PERSISTENT 1
+#define MP_F_WRAPS 2
+#define MP_F_RENAMED 4 /* name is "base#alloc" */
+
+typedef struct mp_profile_out {
+  /* per variable [nvars] */
+  int32_t *base;    /* var id of base_var */
+  int64_t *size;
+  int32_t *alloc;   /* -1 = None */
+  int32_t *free_;   /* -1 = None */
+  int32_t *nseg;    /* 1 or 2 */
+  int32_t *seg;     /* [nvars][4] = lo0, hi0, lo1, hi1 */
+  uint8_t *flags;   /* MP_F_* */
+  int64_t *acc_off; /* [nvars + 1] */
+  /* per access [naccess] */
+  int32_t *acc_index;
+  uint8_t *acc_kind;
+  uint8_t *acc_next;
+  /* per op [period] */
+  double *op_times;
+  int64_t *loads;
+  int32_t *op_owner; /* variable index that op r resolved to */
+} mp_profile_out;
+
+/* ---------------------------------------------------------------------- */
+/* device context                                                           */
+
+typedef struct mp_ctx mp_ctx;
+typedef struct mp_dtrace mp_dtrace;     /* device-resident trace  */
+typedef struct mp_dprofile mp_dprofile; /* device-resident profile */
+typedef struct mp_dgraph mp_dgraph;     /* device-resident CSR conflict graph */
+
+int mp_version(void);
+int mp_ctx_create(int device, mp_ctx **out, mp_err *err);
+int mp_ctx_destroy(mp_ctx *ctx);
+/* launches of this library's kernels since creation (bench evidence) */
+int64_t mp_ctx_launches(mp_ctx *ctx);
+int mp_ctx_sync(mp_ctx *ctx, mp_err *err);
+/* stream the context launches on (cudaStream_t as void*) */
+void *mp_ctx_stream(mp_ctx *ctx);
+
+/* validate_trace (trace.py:55-84) + upload.  Replaces
+ * memplan.trace.validate_trace; the first violation is reported exactly as
+ * the sequential reference would. */
+int mp_trace_upload(mp_ctx *ctx, const mp_trace_in *in, mp_dtrace **out, mp_err *err);
+int mp_trace_free(mp_dtrace *t);
+int mp_validate(mp_ctx *ctx, mp_dtrace *t, mp_err *err);
+
+/* detect_iteration (iteration.py:93-105): smallest p with the last 2p
+ * (kind, size) fingerprints equal pairwise; window = (n - p, n). */
+int mp_detect(mp_ctx *ctx, mp_dtrace *t, int64_t *period, mp_err *err);
+
+/* extract_lifetimes (iteration.py:275-301) incl. build_profile and
+ * compute_load_profile (iteration.py:135-272, 304-320). */
+int mp_extract(mp_ctx *ctx, mp_dtrace *t, int64_t start, int64_t end,
+               mp_dprofile **out, mp_err *err);
+int mp_profile_get_dims(mp_dprofile *p, mp_profile_dims *dims);
+int mp_profile_download(mp_ctx *ctx, mp_dprofile *p, mp_profile_out *out, mp_err *err);
+int mp_profile_free(mp_dprofile *p);
+/* upload a host-built profile (e.g. IterationProfile objects built in
+ * Python); names must be interned so var ids are ranks, flags carry no
+ * MP_F_RENAMED. */
+int mp_profile_upload(mp_ctx *ctx, const mp_profile_dims *dims, const mp_profile_out *in,
+                      const uint8_t *name_blob, const int64_t *name_off, int32_t nnames,
+                      mp_dprofile **out, mp_err *err);
+
+/* build_conflict_graph / conflict_graph_from_arcs (smartpool.py:51-88).
+ * Edge iff two segments overlap as half-open intervals; the device CSR may
+ * hold an edge more than once when a variable has two segments (sets on the
+ * Python side deduplicate; planning is insensitive to repeats). */
+int mp_conflict_from_profile(mp_ctx *ctx, mp_dprofile *p, mp_dgraph **out, mp_err *err);
+int mp_conflict_from_arcs(mp_ctx *ctx, int32_t nvars, const int64_t *size,
+                          const int64_t *tiekey, const int64_t *seg_off,
+                          const int32_t *seg_lo, const int32_t *seg_hi,
+                          mp_dgraph **out, mp_err *err);
+int mp_graph_dims(mp_dgraph *g, int64_t *nvars, int64_t *nnz);
+int mp_graph_download(mp_ctx *ctx, mp_dgraph *g, int64_t *row_off, int32_t *col, mp_err *err);
+int mp_graph_free(mp_dgraph *g);
+
+/* plan_pool (smartpool.py:91-144).  policy 0 = first_fit, 1 = best_fit.
+ * Placement order (-size, alloc, name) — the tie part comes from the
+ * graph's tiekey (profile order for profiles). */
+int mp_plan_pool(mp_ctx *ctx, mp_dgraph *g, int32_t policy, int64_t *offsets,
+                 int64_t *footprint, int64_t *levels, mp_err *err);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MEMPLAN_B200_H */
