@@ -1,0 +1,159 @@
+// capi.cu — context and handle management of the C ABI (include/memplan_b200.h).
+#include "handles.cuh"
+
+int profile_loads(mp_ctx *ctx, mp_dprofile *P, mp_err *err);
+int profile_alloc(mp_ctx *ctx, mp_dprofile *P, mp_err *err);
+
+extern "C" int mp_version(void) { return 1; }
+
+extern "C" int mp_ctx_create(int device, mp_ctx **out, mp_err *err) {
+  mp_ctx *c = new mp_ctx();
+  c->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) {
+    mp_set_err(err, MP_E_CUDA, 0, e, 0, cudaGetErrorString(e));
+    delete c;
+    return MP_E_CUDA;
+  }
+  CUDA_TRY(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+  CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  CUDA_TRY(cudaMallocHost((void **)&c->h_small, 64 * sizeof(int64_t)));
+  CUDA_TRY(cudaMalloc((void **)&c->d_small, 64 * sizeof(int64_t)));
+  // keep freed scratch in the pool instead of returning it to the driver
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  *out = c;
+  return MP_OK;
+}
+
+extern "C" int mp_ctx_destroy(mp_ctx *c) {
+  if (!c) return MP_OK;
+  cudaStreamSynchronize(c->stream);
+  cudaFreeHost(c->h_small);
+  cudaFree(c->d_small);
+  cudaStreamDestroy(c->stream);
+  delete c;
+  return MP_OK;
+}
+
+extern "C" int64_t mp_ctx_launches(mp_ctx *c) { return c->launches; }
+
+extern "C" int mp_ctx_sync(mp_ctx *c, mp_err *err) {
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return MP_OK;
+}
+
+extern "C" void *mp_ctx_stream(mp_ctx *c) { return (void *)c->stream; }
+
+extern "C" int mp_trace_upload(mp_ctx *ctx, const mp_trace_in *in, mp_dtrace **out, mp_err *err) {
+  cudaStream_t st = ctx->stream;
+  mp_dtrace *t = new mp_dtrace();
+  t->ctx = ctx;
+  t->n = in->n;
+  t->nvars = in->nvars;
+  t->name_bytes = in->name_off ? in->name_off[in->nvars] : 0;
+  int64_t n = in->n;
+  CUDA_TRY(t->kind.alloc(n, st));
+  CUDA_TRY(t->var.alloc(n, st));
+  CUDA_TRY(t->size.alloc(n, st));
+  CUDA_TRY(t->t_us.alloc(n, st));
+  if (n) {
+    CUDA_TRY(cudaMemcpyAsync(t->kind.p, in->kind, n, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(t->var.p, in->var, n * 4, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(t->size.p, in->size, n * 8, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(t->t_us.p, in->t_us, n * 8, cudaMemcpyHostToDevice, st));
+  }
+  if (in->index) {
+    CUDA_TRY(t->index.alloc(n, st));
+    CUDA_TRY(cudaMemcpyAsync(t->index.p, in->index, n * 8, cudaMemcpyHostToDevice, st));
+  }
+  CUDA_TRY(t->blob.alloc(t->name_bytes, st));
+  CUDA_TRY(t->name_off.alloc((int64_t)in->nvars + 1, st));
+  if (t->name_bytes) CUDA_TRY(cudaMemcpyAsync(t->blob.p, in->name_blob, t->name_bytes, cudaMemcpyHostToDevice, st));
+  if (in->name_off)
+    CUDA_TRY(cudaMemcpyAsync(t->name_off.p, in->name_off, ((int64_t)in->nvars + 1) * 8, cudaMemcpyHostToDevice, st));
+  // inputs are borrowed for the duration of the call only
+  CUDA_TRY(cudaStreamSynchronize(st));
+  *out = t;
+  return MP_OK;
+}
+
+extern "C" int mp_trace_free(mp_dtrace *t) {
+  delete t;
+  return MP_OK;
+}
+
+extern "C" int mp_profile_get_dims(mp_dprofile *p, mp_profile_dims *dims) {
+  *dims = p->d;
+  return MP_OK;
+}
+
+extern "C" int mp_profile_download(mp_ctx *ctx, mp_dprofile *P, mp_profile_out *o, mp_err *err) {
+  cudaStream_t st = ctx->stream;
+  int64_t V = P->d.nvars, A = P->d.naccess, p = P->d.period;
+#define DL(dst, src, bytes) \
+  if ((bytes) > 0 && (dst)) CUDA_TRY(cudaMemcpyAsync((dst), (src), (bytes), cudaMemcpyDeviceToHost, st))
+  DL(o->base, P->base.p, V * 4);
+  DL(o->size, P->size.p, V * 8);
+  DL(o->alloc, P->alloc.p, V * 4);
+  DL(o->free_, P->free_.p, V * 4);
+  DL(o->nseg, P->nseg.p, V * 4);
+  DL(o->seg, P->seg.p, V * 16);
+  DL(o->flags, P->flags.p, V);
+  DL(o->acc_off, P->acc_off.p, (V + 1) * 8);
+  DL(o->acc_index, P->acc_index.p, A * 4);
+  DL(o->acc_kind, P->acc_kind.p, A);
+  DL(o->acc_next, P->acc_next.p, A);
+  DL(o->op_times, P->op_times.p, p * 8);
+  DL(o->loads, P->loads.p, p * 8);
+  DL(o->op_owner, P->op_owner.p, p * 4);
+#undef DL
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return MP_OK;
+}
+
+extern "C" int mp_profile_free(mp_dprofile *p) {
+  delete p;
+  return MP_OK;
+}
+
+extern "C" int mp_profile_upload(mp_ctx *ctx, const mp_profile_dims *dims, const mp_profile_out *in,
+                                 const uint8_t *name_blob, const int64_t *name_off, int32_t nnames,
+                                 mp_dprofile **out, mp_err *err) {
+  cudaStream_t st = ctx->stream;
+  mp_dprofile *P = new mp_dprofile();
+  P->ctx = ctx;
+  P->d = *dims;
+  int rc = profile_alloc(ctx, P, err);
+  if (rc) { delete P; return rc; }
+  int64_t V = P->d.nvars, A = P->d.naccess, p = P->d.period;
+#define UL(dst, src, bytes) \
+  if ((bytes) > 0 && (src)) CUDA_TRY(cudaMemcpyAsync((dst), (src), (bytes), cudaMemcpyHostToDevice, st))
+  UL(P->base.p, in->base, V * 4);
+  UL(P->size.p, in->size, V * 8);
+  UL(P->alloc.p, in->alloc, V * 4);
+  UL(P->free_.p, in->free_, V * 4);
+  UL(P->nseg.p, in->nseg, V * 4);
+  UL(P->seg.p, in->seg, V * 16);
+  UL(P->flags.p, in->flags, V);
+  UL(P->acc_off.p, in->acc_off, (V + 1) * 8);
+  UL(P->acc_index.p, in->acc_index, A * 4);
+  UL(P->acc_kind.p, in->acc_kind, A);
+  UL(P->acc_next.p, in->acc_next, A);
+  UL(P->op_times.p, in->op_times, p * 8);
+  UL(P->loads.p, in->loads, p * 8);
+  UL(P->op_owner.p, in->op_owner, p * 4);
+  int64_t nb = name_off ? name_off[nnames] : 0;
+  P->nnames = nnames;
+  CUDA_TRY(P->blob.alloc(nb, st));
+  CUDA_TRY(P->name_off.alloc((int64_t)nnames + 1, st));
+  UL(P->blob.p, name_blob, nb);
+  UL(P->name_off.p, name_off, ((int64_t)nnames + 1) * 8);
+#undef UL
+  CUDA_TRY(cudaStreamSynchronize(st));
+  *out = P;
+  return MP_OK;
+}

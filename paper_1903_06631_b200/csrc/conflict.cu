@@ -1,0 +1,244 @@
+// conflict.cu — weighted interval-conflict graph as CSR (smartpool.py:51-88).
+//
+// The reference sweeps sorted endpoints and unions an active set into
+// adjacency sets.  Here the same relation is built sort-and-sweep style:
+//   1. per variable, segments are normalized into the disjoint "effective"
+//      intervals the reference's add/discard toggling produces (identity
+//      for profile lifetimes; matters only for self-overlapping arcs);
+//   2. intervals are radix-sorted by start (and, separately, by end);
+//   3. interval k overlaps exactly the sorted run (k, ub(end_k)) after it
+//      ("forward") plus the earlier intervals still open at start_k
+//      ("backward", counted with one binary search over sorted ends);
+//   4. row k's forward run is copied contiguously, and each forward pair is
+//      mirrored into the partner's backward slots with an atomic cursor.
+// The CSR may repeat an edge when a variable owns two intervals; plan_pool
+// only looks at the union of neighbour ranges, and the Python adjacency
+// sets deduplicate.
+#include "handles.cuh"
+
+constexpr int MAXSEG = 64;
+
+// effective intervals of each variable: [lo_k, min{hi_m > lo_k}) merged
+__global__ void k_norm_count(int64_t nv, const int64_t *seg_off, const int32_t *lo, const int32_t *hi,
+                             int64_t *ecnt, int32_t *ea, int32_t *eb, int *overflow, int write,
+                             const int64_t *eoff, int32_t *ivar) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
+    int32_t L[MAXSEG], H[MAXSEG];
+    int m = 0;
+    for (int64_t s = seg_off[v]; s < seg_off[v + 1]; s++) {
+      if (hi[s] <= lo[s]) continue;  // empty segments never enter the sweep
+      if (m == MAXSEG) { *overflow = 1; break; }
+      // insertion sort by lo
+      int j = m++;
+      while (j > 0 && L[j - 1] > lo[s]) { L[j] = L[j - 1]; H[j] = H[j - 1]; j--; }
+      L[j] = lo[s];
+      H[j] = hi[s];
+    }
+    int64_t out = write ? eoff[v] : 0, c = 0;
+    int32_t cur_end = INT32_MIN;
+    for (int k = 0; k < m; k++) {
+      if (L[k] < cur_end) continue;  // inside the current effective interval
+      int32_t ne = INT32_MAX;
+      for (int q = 0; q < m; q++)
+        if (H[q] > L[k] && H[q] < ne) ne = H[q];
+      if (write) {
+        ea[out + c] = L[k];
+        eb[out + c] = ne;
+        ivar[out + c] = (int32_t)v;
+      }
+      c++;
+      cur_end = ne;
+    }
+    if (!write) ecnt[v] = c;
+  }
+}
+
+__global__ void k_iv_keys(int64_t n, const int32_t *a, uint32_t *keys, uint32_t *vals) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    keys[i] = (uint32_t)a[i] ^ 0x80000000u;  // order-preserving for signed bounds
+    vals[i] = (uint32_t)i;
+  }
+}
+
+// fwd/bwd counts per interval (indexed by interval id)
+__global__ void k_iv_counts(int64_t n, const uint32_t *sstart, const uint32_t *perm, const uint32_t *send,
+                            const int32_t *eb, int64_t *cnt, int32_t *fwd) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t iid = perm[k];
+    uint32_t a = sstart[k], b = (uint32_t)eb[iid] ^ 0x80000000u;
+    int64_t lo = k + 1, hi = n;  // first sorted start >= b
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (sstart[mid] < b) lo = mid + 1; else hi = mid;
+    }
+    int64_t f = lo - k - 1;
+    lo = 0; hi = n;  // number of ends <= a
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (send[mid] <= a) lo = mid + 1; else hi = mid;
+    }
+    int64_t bw = k - lo;
+    fwd[iid] = (int32_t)f;
+    cnt[iid] = f + bw;
+  }
+}
+
+__global__ void k_row_off(int64_t nv, const int64_t *eoff, const int64_t *sub_off, int64_t *row_off) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v <= nv; v += (int64_t)gridDim.x * blockDim.x)
+    row_off[v] = sub_off[eoff[v]];
+}
+
+// warp per sorted interval: forward run + mirrored backward entries
+__global__ void k_iv_fill(int64_t n, const uint32_t *perm, const int32_t *ivar, const int32_t *fwd,
+                          const int64_t *sub_off, int32_t *bcur, int32_t *col) {
+  const int lane = threadIdx.x & 31;
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t k = warp; k < n; k += nwarps) {
+    uint32_t iid = perm[k];
+    int32_t u = ivar[iid];
+    int32_t f = fwd[iid];
+    int64_t so = sub_off[iid];
+    for (int32_t j = lane; j < f; j += 32) {
+      uint32_t jid = perm[k + 1 + j];
+      col[so + j] = ivar[jid];
+      int32_t slot = atomicAdd(&bcur[jid], 1);
+      col[sub_off[jid] + fwd[jid] + slot] = u;
+    }
+  }
+}
+
+static int build_csr(mp_ctx *ctx, int64_t nv, const int64_t *seg_off_d, const int32_t *lo_d,
+                     const int32_t *hi_d, mp_dgraph *g, mp_err *err) {
+  cudaStream_t st = ctx->stream;
+  DBuf<int64_t> ecnt, eoff;
+  CUDA_TRY(ecnt.alloc(nv + 1, st));
+  CUDA_TRY(eoff.alloc(nv + 1, st));
+  int *d_over = (int *)ctx->d_small;
+  CUDA_TRY(cudaMemsetAsync(d_over, 0, 4, st));
+  LAUNCH(ctx, k_norm_count, grid_for(nv, 128), 128, 0, nv, seg_off_d, lo_d, hi_d, ecnt.p, (int32_t *)nullptr,
+         (int32_t *)nullptr, d_over, 0, (const int64_t *)nullptr, (int32_t *)nullptr);
+  int64_t *d_tot = ctx->d_small + 1;
+  int rc = dev_exclusive_scan<int64_t>(ctx, ecnt.p, eoff.p, nv, d_tot, err);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(eoff.p + nv, d_tot, 8, cudaMemcpyDeviceToDevice, st));
+  int64_t h[2];
+  rc = dev_read_n(ctx, ctx->d_small, h, 16, err);
+  if (rc) return rc;
+  if ((int)h[0]) {
+    mp_set_err(err, MP_E_UNSUPPORTED, 0, MAXSEG, 0, "more than 64 segments on one variable");
+    return MP_E_UNSUPPORTED;
+  }
+  int64_t ni = h[1];
+  DBuf<int32_t> ea, eb, ivar, fwd, bcur;
+  CUDA_TRY(ea.alloc(ni, st)); CUDA_TRY(eb.alloc(ni, st)); CUDA_TRY(ivar.alloc(ni, st));
+  CUDA_TRY(fwd.alloc(ni, st)); CUDA_TRY(bcur.alloc(ni, st));
+  LAUNCH(ctx, k_norm_count, grid_for(nv, 128), 128, 0, nv, seg_off_d, lo_d, hi_d, ecnt.p, ea.p, eb.p,
+         d_over, 1, eoff.p, ivar.p);
+  // sort starts (with interval ids) and ends
+  DBuf<uint32_t> skey, perm, ekey, edummy;
+  CUDA_TRY(skey.alloc(ni, st)); CUDA_TRY(perm.alloc(ni, st));
+  CUDA_TRY(ekey.alloc(ni, st)); CUDA_TRY(edummy.alloc(ni, st));
+  LAUNCH(ctx, k_iv_keys, grid_for(ni, 256), 256, 0, ni, ea.p, skey.p, perm.p);
+  LAUNCH(ctx, k_iv_keys, grid_for(ni, 256), 256, 0, ni, eb.p, ekey.p, edummy.p);
+  int kb = 32;
+  rc = dev_radix_sort_u32(ctx, skey.p, perm.p, ni, kb, err);
+  if (rc) return rc;
+  rc = dev_radix_sort_u32(ctx, ekey.p, edummy.p, ni, kb, err);
+  if (rc) return rc;
+  DBuf<int64_t> cnt, sub_off;
+  CUDA_TRY(cnt.alloc(ni + 1, st));
+  CUDA_TRY(sub_off.alloc(ni + 1, st));
+  LAUNCH(ctx, k_iv_counts, grid_for(ni, 256), 256, 0, ni, skey.p, perm.p, ekey.p, eb.p, cnt.p, fwd.p);
+  rc = dev_exclusive_scan<int64_t>(ctx, cnt.p, sub_off.p, ni, d_tot, err);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(sub_off.p + ni, d_tot, 8, cudaMemcpyDeviceToDevice, st));
+  int64_t nnz;
+  rc = dev_read_i64(ctx, d_tot, &nnz, err);
+  if (rc) return rc;
+  g->nvars = nv;
+  g->nnz = nnz;
+  CUDA_TRY(g->row_off.alloc(nv + 1, st));
+  CUDA_TRY(g->col.alloc(nnz, st));
+  LAUNCH(ctx, k_row_off, grid_for(nv + 1, 256), 256, 0, nv, eoff.p, sub_off.p, g->row_off.p);
+  CUDA_TRY(cudaMemsetAsync(bcur.p, 0, ni * 4, st));
+  LAUNCH(ctx, k_iv_fill, grid_for(ni * 32, 256, 148 * 64), 256, 0, ni, perm.p, ivar.p, fwd.p, sub_off.p,
+         bcur.p, g->col.p);
+  return MP_OK;
+}
+
+__global__ void k_prof_segs(int64_t nv, const int32_t *nseg, const int32_t *seg, int64_t *seg_off,
+                            int32_t *lo, int32_t *hi) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
+    seg_off[v] = 2 * v;
+    int ns = nseg[v];
+    lo[2 * v] = seg[4 * v]; hi[2 * v] = seg[4 * v + 1];
+    lo[2 * v + 1] = ns > 1 ? seg[4 * v + 2] : 0;
+    hi[2 * v + 1] = ns > 1 ? seg[4 * v + 3] : 0;  // empty when absent
+    if (v == nv - 1) seg_off[nv] = 2 * nv;
+  }
+}
+
+extern "C" int mp_conflict_from_profile(mp_ctx *ctx, mp_dprofile *P, mp_dgraph **out, mp_err *err) {
+  cudaStream_t st = ctx->stream;
+  int64_t nv = P->d.nvars;
+  DBuf<int64_t> so;
+  DBuf<int32_t> lo, hi;
+  CUDA_TRY(so.alloc(nv + 1, st)); CUDA_TRY(lo.alloc(2 * nv, st)); CUDA_TRY(hi.alloc(2 * nv, st));
+  if (nv == 0) CUDA_TRY(cudaMemsetAsync(so.p, 0, 8, st));
+  else LAUNCH(ctx, k_prof_segs, grid_for(nv, 256), 256, 0, nv, P->nseg.p, P->seg.p, so.p, lo.p, hi.p);
+  mp_dgraph *g = new mp_dgraph();
+  g->ctx = ctx;
+  int rc = build_csr(ctx, nv, so.p, lo.p, hi.p, g, err);
+  if (rc) { delete g; return rc; }
+  CUDA_TRY(g->size.alloc(nv, st));
+  if (nv) CUDA_TRY(cudaMemcpyAsync(g->size.p, P->size.p, nv * 8, cudaMemcpyDeviceToDevice, st));
+  *out = g;
+  return MP_OK;
+}
+
+extern "C" int mp_conflict_from_arcs(mp_ctx *ctx, int32_t nvars, const int64_t *size, const int64_t *tiekey,
+                                     const int64_t *seg_off, const int32_t *seg_lo, const int32_t *seg_hi,
+                                     mp_dgraph **out, mp_err *err) {
+  cudaStream_t st = ctx->stream;
+  int64_t nv = nvars, ns = seg_off[nvars];
+  DBuf<int64_t> so;
+  DBuf<int32_t> lo, hi;
+  CUDA_TRY(so.alloc(nv + 1, st)); CUDA_TRY(lo.alloc(ns, st)); CUDA_TRY(hi.alloc(ns, st));
+  CUDA_TRY(cudaMemcpyAsync(so.p, seg_off, (nv + 1) * 8, cudaMemcpyHostToDevice, st));
+  if (ns) {
+    CUDA_TRY(cudaMemcpyAsync(lo.p, seg_lo, ns * 4, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(hi.p, seg_hi, ns * 4, cudaMemcpyHostToDevice, st));
+  }
+  mp_dgraph *g = new mp_dgraph();
+  g->ctx = ctx;
+  int rc = build_csr(ctx, nv, so.p, lo.p, hi.p, g, err);
+  if (rc) { delete g; return rc; }
+  CUDA_TRY(g->size.alloc(nv, st));
+  CUDA_TRY(g->tiekey.alloc(nv, st));
+  if (nv) {
+    CUDA_TRY(cudaMemcpyAsync(g->size.p, size, nv * 8, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(g->tiekey.p, tiekey, nv * 8, cudaMemcpyHostToDevice, st));
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));  // host arrays are only borrowed for the call
+  *out = g;
+  return MP_OK;
+}
+
+extern "C" int mp_graph_dims(mp_dgraph *g, int64_t *nvars, int64_t *nnz) {
+  *nvars = g->nvars;
+  *nnz = g->nnz;
+  return MP_OK;
+}
+
+extern "C" int mp_graph_download(mp_ctx *ctx, mp_dgraph *g, int64_t *row_off, int32_t *col, mp_err *err) {
+  CUDA_TRY(cudaMemcpyAsync(row_off, g->row_off.p, (g->nvars + 1) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  if (g->nnz) CUDA_TRY(cudaMemcpyAsync(col, g->col.p, g->nnz * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return MP_OK;
+}
+
+extern "C" int mp_graph_free(mp_dgraph *g) {
+  delete g;
+  return MP_OK;
+}

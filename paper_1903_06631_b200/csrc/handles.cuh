@@ -1,0 +1,49 @@
+// handles.cuh — device-resident objects behind the opaque C-ABI handles.
+#pragma once
+
+#include "common.cuh"
+
+struct mp_dtrace {
+  mp_ctx *ctx = nullptr;
+  int64_t n = 0;
+  int32_t nvars = 0;
+  int64_t name_bytes = 0;
+  DBuf<uint8_t> kind;
+  DBuf<int32_t> var;
+  DBuf<int64_t> size;
+  DBuf<int64_t> t_us;
+  DBuf<int64_t> index;  // empty when index == position
+  DBuf<uint8_t> blob;
+  DBuf<int64_t> name_off;
+  // events grouped by variable: perm = event indices sorted by (var, index),
+  // gstart[v] .. gstart[v+1] = var v's run (built once, reused by validate,
+  // live-at and extraction)
+  bool grouped = false;
+  DBuf<uint32_t> perm;
+  DBuf<int64_t> gstart;
+};
+
+struct mp_dprofile {
+  mp_ctx *ctx = nullptr;
+  mp_profile_dims d{};
+  int64_t window0 = 0;
+  DBuf<int32_t> base, alloc, free_, nseg, seg, acc_index, op_owner;
+  DBuf<int64_t> size, acc_off, loads;
+  DBuf<uint8_t> flags, acc_kind, acc_next;
+  DBuf<double> op_times;
+  DBuf<uint8_t> blob;
+  DBuf<int64_t> name_off;
+  int32_t nnames = 0;
+};
+
+struct mp_dgraph {
+  mp_ctx *ctx = nullptr;
+  int64_t nvars = 0;
+  int64_t nnz = 0;
+  DBuf<int64_t> row_off;
+  DBuf<int32_t> col;
+  DBuf<int64_t> size;     // vertex weights
+  DBuf<int64_t> tiekey;   // placement tie-break after -size (empty: vertex order)
+};
+
+int build_groups(mp_ctx *ctx, mp_dtrace *t, mp_err *err);

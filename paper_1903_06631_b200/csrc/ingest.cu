@@ -1,0 +1,727 @@
+// ingest.cu — trace validation, period detection and lifetime extraction.
+//
+//   validate_trace      trace.py:55-84
+//   detect_iteration    iteration.py:93-105
+//   extract_lifetimes   iteration.py:124-301 (incl. build_profile)
+//   compute_load_profile iteration.py:304-320
+//
+// Layout: one stable radix sort groups the trace's events by variable
+// (perm, gstart).  Every per-variable state machine of the reference
+// (live set, open instances, carry-ins) then runs as one thread per
+// variable over its own run — the runs are independent, so the first
+// violation in event order is the minimum over variables of each run's
+// first violation.  Instances are addressed by their malloc position in the
+// window (window instances) or by variable id (carry-ins); prefix sums turn
+// them into the reference's variable order (carry-ins by name, then window
+// instances by alloc index).
+#include "handles.cuh"
+
+// ---------------------------------------------------------------------------
+// grouping
+
+__global__ void k_group_init(const int32_t *var, int64_t n, uint32_t *keys, uint32_t *vals) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    keys[i] = (uint32_t)var[i];
+    vals[i] = (uint32_t)i;
+  }
+}
+
+__global__ void k_group_bounds(const uint32_t *skeys, int64_t n, int32_t nvars, int64_t *gstart) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v <= nvars; v += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = n;  // lower_bound(v)
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (skeys[mid] < (uint32_t)v) lo = mid + 1; else hi = mid;
+    }
+    gstart[v] = lo;
+  }
+}
+
+int build_groups(mp_ctx *ctx, mp_dtrace *t, mp_err *err) {
+  if (t->grouped) return MP_OK;
+  int64_t n = t->n;
+  DBuf<uint32_t> keys;
+  CUDA_TRY(keys.alloc(n, ctx->stream));
+  CUDA_TRY(t->perm.alloc(n, ctx->stream));
+  CUDA_TRY(t->gstart.alloc((int64_t)t->nvars + 1, ctx->stream));
+  LAUNCH(ctx, k_group_init, grid_for(n, 256), 256, 0, t->var.p, n, keys.p, t->perm.p);
+  int rc = dev_radix_sort_u32(ctx, keys.p, t->perm.p, n, bits_for((uint64_t)(t->nvars > 0 ? t->nvars - 1 : 0)), err);
+  if (rc) return rc;
+  LAUNCH(ctx, k_group_bounds, grid_for((int64_t)t->nvars + 1, 256), 256, 0, keys.p, n, t->nvars, t->gstart.p);
+  t->grouped = true;
+  return MP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// validate_trace
+
+__global__ void k_validate_elem(const uint8_t *kind, const int64_t *size, const int64_t *t_us,
+                                const int64_t *index, int64_t n, unsigned long long *first) {
+  for (int64_t pos = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; pos < n; pos += (int64_t)gridDim.x * blockDim.x) {
+    int code = 0;
+    if (index && index[pos] != pos) code = MP_V_INDEX;
+    else if (t_us[pos] < 0) code = MP_V_NEG_T;
+    else if (pos > 0 && t_us[pos] < t_us[pos - 1]) code = MP_V_T_DEC;
+    else if (kind[pos] == MP_MALLOC) { if (size[pos] <= 0) code = MP_V_MALLOC_SIZE; }
+    else if (size[pos] != 0) code = MP_V_SIZE_NONZERO;
+    if (code) atomicMin(first, ((unsigned long long)pos << 4) | (unsigned)code);
+  }
+}
+
+__global__ void k_validate_var(const uint8_t *kind, const uint32_t *perm, const int64_t *gstart,
+                               int32_t nvars, unsigned long long *first) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvars; v += (int64_t)gridDim.x * blockDim.x) {
+    bool live = false;
+    for (int64_t q = gstart[v]; q < gstart[v + 1]; q++) {
+      uint32_t e = perm[q];
+      uint8_t k = kind[e];
+      int code = 0;
+      if (k == MP_MALLOC) {
+        if (live) code = MP_V_MALLOC_LIVE;
+        live = true;
+      } else {
+        if (!live) code = k == MP_FREE ? MP_V_FREE_DEAD : MP_V_USE_DEAD;
+        if (k == MP_FREE) live = false;
+      }
+      if (code) {
+        atomicMin(first, ((unsigned long long)e << 4) | (unsigned)code);
+        break;
+      }
+    }
+  }
+}
+
+extern "C" int mp_validate(mp_ctx *ctx, mp_dtrace *t, mp_err *err) {
+  if (t->n == 0) return MP_OK;
+  int rc = build_groups(ctx, t, err);
+  if (rc) return rc;
+  unsigned long long *d_first = (unsigned long long *)ctx->d_small;
+  CUDA_TRY(cudaMemsetAsync(d_first, 0xff, 8, ctx->stream));
+  LAUNCH(ctx, k_validate_elem, grid_for(t->n, 256, 4096), 256, 0, t->kind.p, t->size.p, t->t_us.p,
+         t->index.p, t->n, d_first);
+  LAUNCH(ctx, k_validate_var, grid_for(t->nvars, 256), 256, 0, t->kind.p, t->perm.p, t->gstart.p,
+         t->nvars, d_first);
+  int64_t first;
+  rc = dev_read_i64(ctx, (const int64_t *)d_first, &first, err);
+  if (rc) return rc;
+  if ((uint64_t)first == ~0ull) return MP_OK;
+  int64_t pos = (int64_t)((uint64_t)first >> 4);
+  int code = (int)(first & 15);
+  int64_t aux1 = 0;
+  if (code == MP_V_INDEX) {
+    rc = dev_read_n(ctx, t->index.p + pos, &aux1, 8, err);
+  } else if (code == MP_V_SIZE_NONZERO) {
+    uint8_t k;
+    rc = dev_read_n(ctx, t->kind.p + pos, &k, 1, err);
+    aux1 = k;
+  } else {
+    int32_t v;
+    rc = dev_read_n(ctx, t->var.p + pos, &v, 4, err);
+    aux1 = v;
+  }
+  if (rc) return rc;
+  mp_set_err(err, MP_E_INVARIANT, pos, code, aux1, "invariant violation");
+  return MP_E_INVARIANT;
+}
+
+// ---------------------------------------------------------------------------
+// detect_iteration: polynomial hashes mod 2^61-1, all candidate periods
+// tested in parallel, smallest hash-equal period verified exactly.
+
+#define MODP 0x1fffffffffffffffull
+#define HBASE 0x00b2d9c2e4f1a37bull
+
+__device__ __forceinline__ uint64_t mulmod61(uint64_t a, uint64_t b) {
+  uint64_t lo = a * b, hi = __umul64hi(a, b);
+  uint64_t r = (lo & MODP) + (lo >> 61) + (hi << 3);
+  r = (r & MODP) + (r >> 61);
+  return r >= MODP ? r - MODP : r;
+}
+__device__ __forceinline__ uint64_t addmod61(uint64_t a, uint64_t b) {
+  uint64_t r = a + b;
+  return r >= MODP ? r - MODP : r;
+}
+__device__ __forceinline__ uint64_t submod61(uint64_t a, uint64_t b) { return a >= b ? a - b : a + MODP - b; }
+__device__ uint64_t powmod61(uint64_t b, uint64_t e) {
+  uint64_t r = 1;
+  while (e) {
+    if (e & 1) r = mulmod61(r, b);
+    b = mulmod61(b, b);
+    e >>= 1;
+  }
+  return r;
+}
+
+__device__ __forceinline__ uint64_t fp_hash(uint8_t kind, int64_t size) {
+  uint64_t x = (uint64_t)size * 4u + kind + 0x9e3779b97f4a7c15ull;
+  x ^= x >> 30; x *= 0xbf58476d1ce4e5b9ull;
+  x ^= x >> 27; x *= 0x94d049bb133111ebull;
+  x ^= x >> 31;
+  return (x & MODP) % MODP;
+}
+
+struct HPair { uint64_t h, pw; };  // hash of a run and B^len
+__device__ __forceinline__ HPair hcombine(HPair a, HPair b) { return {addmod61(mulmod61(a.h, b.pw), b.h), mulmod61(a.pw, b.pw)}; }
+
+constexpr int DT_THREADS = 256;
+constexpr int DT_ITEMS = 16;
+constexpr int DT_TILE = DT_THREADS * DT_ITEMS;
+
+__device__ HPair block_scan_hash(HPair v, HPair *total) {
+  // exclusive scan of a non-commutative monoid, thread order
+  __shared__ HPair s[DT_THREADS];
+  s[threadIdx.x] = v;
+  __syncthreads();
+  for (int o = 1; o < DT_THREADS; o <<= 1) {
+    HPair x = s[threadIdx.x];
+    HPair y = threadIdx.x >= o ? s[threadIdx.x - o] : HPair{0, 1};
+    __syncthreads();
+    s[threadIdx.x] = hcombine(y, x);
+    __syncthreads();
+  }
+  HPair incl = s[threadIdx.x];
+  HPair excl = threadIdx.x ? s[threadIdx.x - 1] : HPair{0, 1};
+  if (total) *total = s[DT_THREADS - 1];
+  __syncthreads();
+  (void)incl;
+  return excl;
+}
+
+__global__ void __launch_bounds__(DT_THREADS) k_hash_tiles(const uint8_t *kind, const int64_t *size, int64_t n, HPair *tile_agg) {
+  int64_t base = (int64_t)blockIdx.x * DT_TILE + (int64_t)threadIdx.x * DT_ITEMS;
+  HPair a{0, 1};
+  for (int i = 0; i < DT_ITEMS; i++) {
+    int64_t j = base + i;
+    if (j < n) a = hcombine(a, HPair{fp_hash(kind[j], size[j]), HBASE});
+  }
+  __shared__ HPair tot;
+  block_scan_hash(a, &tot);
+  if (threadIdx.x == 0) tile_agg[blockIdx.x] = tot;
+}
+
+__global__ void k_hash_tile_prefix(HPair *agg, int64_t ntiles) {
+  // sequential over tiles (ntiles = n / 4096, small)
+  if (threadIdx.x || blockIdx.x) return;
+  HPair run{0, 1};
+  for (int64_t t = 0; t < ntiles; t++) {
+    HPair x = agg[t];
+    agg[t] = run;
+    run = hcombine(run, x);
+  }
+}
+
+// P[i] = hash of events [0, i) for i in [0, n]
+__global__ void __launch_bounds__(DT_THREADS) k_hash_prefix(const uint8_t *kind, const int64_t *size, int64_t n,
+                                                            const HPair *tile_pre, uint64_t *P) {
+  int64_t base = (int64_t)blockIdx.x * DT_TILE + (int64_t)threadIdx.x * DT_ITEMS;
+  HPair a{0, 1};
+  uint64_t f[DT_ITEMS];
+  for (int i = 0; i < DT_ITEMS; i++) {
+    int64_t j = base + i;
+    f[i] = j < n ? fp_hash(kind[j], size[j]) : 0;
+    if (j < n) a = hcombine(a, HPair{f[i], HBASE});
+  }
+  HPair ex = block_scan_hash(a, nullptr);
+  HPair run = hcombine(tile_pre[blockIdx.x], ex);
+  for (int i = 0; i < DT_ITEMS; i++) {
+    int64_t j = base + i;
+    if (j < n) {
+      run = hcombine(run, HPair{f[i], HBASE});
+      P[j + 1] = run.h;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) P[0] = 0;
+}
+
+__global__ void k_period_candidates(const uint64_t *P, int64_t n, int64_t pmin, unsigned long long *best) {
+  for (int64_t p = pmin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p <= n / 2; p += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t bp = powmod61(HBASE, (uint64_t)p);
+    uint64_t h1 = submod61(P[n], mulmod61(P[n - p], bp));
+    uint64_t h2 = submod61(P[n - p], mulmod61(P[n - 2 * p], bp));
+    if (h1 == h2) atomicMin(best, (unsigned long long)p);
+  }
+}
+
+__global__ void k_period_verify(const uint8_t *kind, const int64_t *size, int64_t n, int64_t p, int *bad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < p; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t a = n - p + i, b = n - 2 * p + i;
+    if (kind[a] != kind[b] || size[a] != size[b]) *bad = 1;
+  }
+}
+
+extern "C" int mp_detect(mp_ctx *ctx, mp_dtrace *t, int64_t *period, mp_err *err) {
+  int64_t n = t->n;
+  if (n < 2) {
+    mp_set_err(err, MP_E_PERIOD_NOT_FOUND, n, 0, 0, "no period");
+    return MP_E_PERIOD_NOT_FOUND;
+  }
+  int64_t ntiles = (n + DT_TILE - 1) / DT_TILE;
+  DBuf<HPair> agg;
+  DBuf<uint64_t> P;
+  CUDA_TRY(agg.alloc(ntiles, ctx->stream));
+  CUDA_TRY(P.alloc(n + 1, ctx->stream));
+  LAUNCH(ctx, k_hash_tiles, (unsigned)ntiles, DT_THREADS, 0, t->kind.p, t->size.p, n, agg.p);
+  LAUNCH(ctx, k_hash_tile_prefix, 1, 32, 0, agg.p, ntiles);
+  LAUNCH(ctx, k_hash_prefix, (unsigned)ntiles, DT_THREADS, 0, t->kind.p, t->size.p, n, agg.p, P.p);
+  unsigned long long *d_best = (unsigned long long *)ctx->d_small;
+  int *d_bad = (int *)(ctx->d_small + 1);
+  int64_t pmin = 1;
+  for (;;) {
+    CUDA_TRY(cudaMemsetAsync(d_best, 0xff, 8, ctx->stream));
+    LAUNCH(ctx, k_period_candidates, grid_for(n / 2 - pmin + 1, 256, 8192), 256, 0, P.p, n, pmin, d_best);
+    int64_t best;
+    int rc = dev_read_i64(ctx, (const int64_t *)d_best, &best, err);
+    if (rc) return rc;
+    if ((uint64_t)best == ~0ull) {
+      mp_set_err(err, MP_E_PERIOD_NOT_FOUND, n, 0, 0, "no period");
+      return MP_E_PERIOD_NOT_FOUND;
+    }
+    CUDA_TRY(cudaMemsetAsync(d_bad, 0, 4, ctx->stream));
+    LAUNCH(ctx, k_period_verify, grid_for(best, 256, 4096), 256, 0, t->kind.p, t->size.p, n, best, d_bad);
+    int bad = 0;
+    rc = dev_read_n(ctx, d_bad, &bad, 4, err);
+    if (rc) return rc;
+    if (!bad) {
+      *period = best;
+      return MP_OK;
+    }
+    pmin = best + 1;  // hash collision: keep searching above it
+  }
+}
+
+// ---------------------------------------------------------------------------
+// extract_lifetimes
+
+// window-instance flags
+#define WF_OPEN_END 1
+#define WF_MERGED 2
+#define WF_COEXIST 4
+// carry-in cases
+#define CC_PERSIST 0
+#define CC_MERGED 1
+#define CC_COEXIST 2
+#define CC_CONSERVATIVE 3
+
+struct ExScratch {
+  // per window op r
+  int32_t *owner;   // >= 0: window instance (malloc position); < 0: carry -(v+1)
+  int32_t *w_free;  // free position of a window instance
+  int32_t *w_nacc;
+  uint8_t *w_flags;
+  int32_t *w_mcarry;  // carry var merged into this twin
+  int32_t *is_malloc; // scanned -> window instance ordinal
+  // per variable
+  uint8_t *c_live;
+  int64_t *c_abs;
+  int64_t *c_size;
+  int32_t *c_free;
+  int32_t *c_nacc;
+  uint8_t *c_case;
+  int32_t *c_twin;
+  int32_t *c_surv;    // scanned -> carry ordinal
+  int32_t *nmalloc;
+};
+
+__global__ void k_ex_var(const uint8_t *kind, const int64_t *size, const uint32_t *perm,
+                         const int64_t *gstart, int32_t nvars, int64_t start, int64_t end,
+                         ExScratch s, unsigned long long *first) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvars; v += (int64_t)gridDim.x * blockDim.x) {
+    int64_t q = gstart[v], qe = gstart[v + 1];
+    // _live_at: last malloc/free before the window
+    int64_t live = -1;
+    for (; q < qe; q++) {
+      int64_t e = perm[q];
+      if (e >= start) break;
+      uint8_t k = kind[e];
+      if (k == MP_MALLOC) live = e;
+      else if (k == MP_FREE) live = -1;
+    }
+    s.c_live[v] = live >= 0;
+    s.c_abs[v] = live;
+    s.c_size[v] = live >= 0 ? size[live] : 0;
+    s.c_free[v] = -1;
+    s.c_case[v] = CC_PERSIST;
+    s.c_twin[v] = -1;
+    bool carry_alive = live >= 0;
+    int32_t open = -1, nacc_c = 0, nm = 0;
+    for (; q < qe; q++) {
+      int64_t e = perm[q];
+      if (e >= end) break;
+      int32_t r = (int32_t)(e - start);
+      uint8_t k = kind[e];
+      int code = 0;
+      if (k == MP_MALLOC) {
+        if (open >= 0) code = MP_V_W_MALLOC_LIVE;
+        else {
+          open = r;
+          nm++;
+          s.w_free[r] = -1;
+          s.w_nacc[r] = 0;
+          s.w_flags[r] = 0;
+          s.owner[r] = r;
+        }
+      } else if (k == MP_FREE) {
+        if (open >= 0) { s.w_free[open] = r; s.owner[r] = open; open = -1; }
+        else if (carry_alive) { s.c_free[v] = r; carry_alive = false; s.owner[r] = -(int32_t)(v + 1); }
+        else code = MP_V_W_FREE_DEAD;
+      } else {
+        if (open >= 0) { s.w_nacc[open]++; s.owner[r] = open; }
+        else if (carry_alive) { nacc_c++; s.owner[r] = -(int32_t)(v + 1); }
+        else code = MP_V_W_USE_DEAD;
+      }
+      if (code) {
+        atomicMin(first, ((unsigned long long)r << 4) | (unsigned)code);
+        break;
+      }
+    }
+    if (open >= 0) s.w_flags[open] |= WF_OPEN_END;
+    s.c_nacc[v] = nacc_c;
+    s.nmalloc[v] = nm;
+  }
+}
+
+__global__ void k_ex_marks(const uint8_t *kind, int64_t start, int64_t p, int32_t *is_malloc) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < p; r += (int64_t)gridDim.x * blockDim.x)
+    is_malloc[r] = kind[start + r] == MP_MALLOC;
+}
+
+// twin pairing, iteration.py:193-225
+__global__ void k_ex_twin(const uint8_t *kind, const int64_t *size, int32_t nvars, int64_t start,
+                          int64_t p, ExScratch s) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvars; v += (int64_t)gridDim.x * blockDim.x) {
+    int32_t surv = 0;
+    if (s.c_live[v]) {
+      surv = 1;
+      int32_t r_f = s.c_free[v];
+      if (r_f >= 0) {
+        int64_t abs_idx = s.c_abs[v];
+        int64_t tw = abs_idx >= start - p ? abs_idx - (start - p) : -1;
+        bool ok = tw >= 0 && tw < p && kind[start + tw] == MP_MALLOC &&
+                  (s.w_flags[tw] & WF_OPEN_END) && size[start + tw] == s.c_size[v];
+        if (ok && r_f <= tw) {
+          s.c_case[v] = CC_MERGED;
+          s.c_twin[v] = (int32_t)tw;
+          s.w_flags[tw] |= WF_MERGED;
+          s.w_mcarry[tw] = (int32_t)v;
+          surv = 0;
+        } else if (ok) {
+          s.c_case[v] = CC_COEXIST;
+          s.w_flags[tw] |= WF_COEXIST;
+        } else {
+          s.c_case[v] = CC_CONSERVATIVE;
+        }
+      }
+    }
+    s.c_surv[v] = surv;
+  }
+}
+
+struct ProfOut {
+  int32_t *base, *alloc, *free_, *nseg, *seg, *acc_index, *op_owner;
+  int64_t *size, *acc_off, *loads;
+  uint8_t *flags, *acc_kind, *acc_next;
+  double *op_times;
+};
+
+// final per-variable records (carry-ins)
+__global__ void k_ex_fill_carry(int32_t nvars, int64_t p, ExScratch s, const int32_t *carry_ord, ProfOut o,
+                                int64_t *acc_cnt) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvars; v += (int64_t)gridDim.x * blockDim.x) {
+    if (!s.c_live[v] || s.c_case[v] == CC_MERGED) continue;
+    int64_t i = carry_ord[v];
+    o.base[i] = (int32_t)v;
+    o.size[i] = s.c_size[v];
+    o.alloc[i] = -1;
+    o.free_[i] = s.c_free[v];
+    o.nseg[i] = 1;
+    uint8_t fl = 0;
+    int32_t hi = (int32_t)p;
+    switch (s.c_case[v]) {
+      case CC_PERSIST: fl = MP_F_PERSISTENT; break;
+      case CC_COEXIST: hi = s.c_free[v]; break;
+      default: fl = MP_F_WRAPS; break;
+    }
+    o.seg[4 * i] = 0; o.seg[4 * i + 1] = hi; o.seg[4 * i + 2] = 0; o.seg[4 * i + 3] = 0;
+    o.flags[i] = fl;
+    acc_cnt[i] = s.c_nacc[v];
+  }
+}
+
+// final per-variable records (window instances, alloc order)
+__global__ void k_ex_fill_window(const int32_t *var, const int64_t *size, int64_t start, int64_t p,
+                                 int64_t ncarry, ExScratch s, const int32_t *win_ord,
+                                 const int32_t *carry_survive, ProfOut o, int64_t *acc_cnt) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < p; r += (int64_t)gridDim.x * blockDim.x) {
+    if (!s.is_malloc[r]) continue;
+    int64_t i = ncarry + win_ord[r];
+    int32_t b = var[start + r];
+    o.base[i] = b;
+    o.size[i] = size[start + r];
+    o.alloc[i] = (int32_t)r;
+    uint8_t wf = s.w_flags[r];
+    uint8_t fl = 0;
+    int32_t nseg = 1, l0 = (int32_t)r, h0 = s.w_free[r], l1 = 0, h1 = 0, fr = s.w_free[r];
+    int64_t nacc = s.w_nacc[r];
+    if (wf & WF_MERGED) {
+      int32_t cv = s.w_mcarry[r];
+      fr = s.c_free[cv];
+      fl = MP_F_WRAPS;
+      nseg = 2; h0 = (int32_t)p; l1 = 0; h1 = fr;
+      nacc += s.c_nacc[cv];
+    } else if (wf & WF_COEXIST) {
+      fl = MP_F_WRAPS; fr = -1; h0 = (int32_t)p;
+    } else if (wf & WF_OPEN_END) {
+      fl = MP_F_PERSISTENT | MP_F_WRAPS; fr = -1; l0 = 0; h0 = (int32_t)p;
+    }
+    // renames, iteration.py:236-241: more than one instance of this base
+    if (carry_survive[b] + s.nmalloc[b] > 1) fl |= MP_F_RENAMED;
+    o.free_[i] = fr;
+    o.nseg[i] = nseg;
+    o.seg[4 * i] = l0; o.seg[4 * i + 1] = h0; o.seg[4 * i + 2] = l1; o.seg[4 * i + 3] = h1;
+    o.flags[i] = fl;
+    acc_cnt[i] = nacc;
+  }
+}
+
+// second walk: accesses into the final CSR, owners into op_owner
+__global__ void k_ex_access(const uint8_t *kind, const uint32_t *perm, const int64_t *gstart,
+                            int32_t nvars, int64_t start, int64_t end, int64_t ncarry, ExScratch s,
+                            const int32_t *carry_ord, const int32_t *win_ord, ProfOut o) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvars; v += (int64_t)gridDim.x * blockDim.x) {
+    int64_t q = gstart[v], qe = gstart[v + 1];
+    while (q < qe && perm[q] < start) q++;
+    // destination of carry-in accesses
+    int64_t cdst = -1, cfinal = -1;
+    uint8_t cnext = 0;
+    if (s.c_live[v]) {
+      if (s.c_case[v] == CC_MERGED) {
+        int32_t tw = s.c_twin[v];
+        cfinal = ncarry + win_ord[tw];
+        cdst = o.acc_off[cfinal] + s.w_nacc[tw];
+        cnext = 1;
+      } else {
+        cfinal = carry_ord[v];
+        cdst = o.acc_off[cfinal];
+      }
+    }
+    int64_t wdst = 0, wfinal = -1;
+    for (; q < qe; q++) {
+      int64_t e = perm[q];
+      if (e >= end) break;
+      int32_t r = (int32_t)(e - start);
+      int32_t ow = s.owner[r];
+      uint8_t k = kind[e];
+      int64_t fin;
+      if (ow >= 0) {
+        if (k == MP_MALLOC) { wfinal = ncarry + win_ord[r]; wdst = o.acc_off[wfinal]; }
+        fin = wfinal;
+        if (k == MP_READ || k == MP_WRITE) {
+          o.acc_index[wdst] = r; o.acc_kind[wdst] = k; o.acc_next[wdst] = 0; wdst++;
+        }
+      } else {
+        fin = cfinal;
+        if (k == MP_READ || k == MP_WRITE) {
+          o.acc_index[cdst] = r; o.acc_kind[cdst] = k; o.acc_next[cdst] = cnext; cdst++;
+        }
+      }
+      o.op_owner[r] = (int32_t)fin;
+    }
+  }
+}
+
+__global__ void k_ex_times(const int64_t *t_us, int64_t start, int64_t end, double *op_times, double *dur) {
+  int64_t p = end - start;
+  int64_t t0 = t_us[start];
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < p; r += (int64_t)gridDim.x * blockDim.x)
+    op_times[r] = (double)(t_us[start + r] - t0);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    // period duration, iteration.py:285-291
+    double last = (double)(t_us[end - 1] - t0);
+    double d;
+    if (start >= 1) {
+      d = (double)(t_us[end - 1] - t_us[start - 1]);
+    } else {
+      double tail = p > 1 ? last - (double)(t_us[end - 2] - t0) : 1.0;
+      d = last + pymax(tail, 1.0);
+    }
+    if (d <= last) d = last + 1.0;
+    *dur = d;
+  }
+}
+
+__global__ void k_load_diff(int64_t nv, const int32_t *nseg, const int32_t *seg, const int64_t *size,
+                            unsigned long long *diff) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
+    for (int s = 0; s < nseg[i]; s++) {
+      atomicAdd(&diff[seg[4 * i + 2 * s]], (unsigned long long)size[i]);
+      atomicAdd(&diff[seg[4 * i + 2 * s + 1]], (unsigned long long)(-size[i]));
+    }
+  }
+}
+
+__global__ void k_load_peak(const int64_t *loads, int64_t p, long long *peak) {
+  long long m = LLONG_MIN;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < p; r += (int64_t)gridDim.x * blockDim.x)
+    if (loads[r] > m) m = loads[r];
+  for (int o = 16; o; o >>= 1) {
+    long long u = __shfl_xor_sync(FULL_MASK, m, o);
+    if (u > m) m = u;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(peak, m);
+}
+
+__global__ void k_load_argmax(const int64_t *loads, int64_t p, const long long *peak, unsigned long long *idx) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < p; r += (int64_t)gridDim.x * blockDim.x)
+    if (loads[r] == *peak) atomicMin(idx, (unsigned long long)r);
+}
+
+// loads + peak for any device profile (also used after uploads)
+int profile_loads(mp_ctx *ctx, mp_dprofile *P, mp_err *err) {
+  int64_t p = P->d.period, V = P->d.nvars;
+  DBuf<int64_t> diff;
+  CUDA_TRY(diff.alloc(p + 1, ctx->stream));
+  CUDA_TRY(cudaMemsetAsync(diff.p, 0, (p + 1) * 8, ctx->stream));
+  LAUNCH(ctx, k_load_diff, grid_for(V, 256), 256, 0, V, P->nseg.p, P->seg.p, P->size.p,
+         (unsigned long long *)diff.p);
+  // loads[r] = sum diff[0..r]: exclusive scan of p+1 entries, shifted by one
+  DBuf<int64_t> ex;
+  CUDA_TRY(ex.alloc(p + 1, ctx->stream));
+  int rc = dev_exclusive_scan<int64_t>(ctx, diff.p, ex.p, p + 1, nullptr, err);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(P->loads.p, ex.p + 1, p * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+  long long *d_peak = (long long *)ctx->d_small;
+  unsigned long long *d_idx = (unsigned long long *)(ctx->d_small + 1);
+  const long long lmin = LLONG_MIN;
+  CUDA_TRY(cudaMemcpyAsync(d_peak, &lmin, 8, cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(cudaMemsetAsync(d_idx, 0xff, 8, ctx->stream));
+  LAUNCH(ctx, k_load_peak, grid_for(p, 256, 2048), 256, 0, P->loads.p, p, d_peak);
+  LAUNCH(ctx, k_load_argmax, grid_for(p, 256, 2048), 256, 0, P->loads.p, p, d_peak, d_idx);
+  int64_t h[2];
+  rc = dev_read_n(ctx, ctx->d_small, h, 16, err);
+  if (rc) return rc;
+  P->d.peak_bytes = p ? h[0] : 0;
+  P->d.peak_index = p ? h[1] : 0;
+  return MP_OK;
+}
+
+int profile_alloc(mp_ctx *ctx, mp_dprofile *P, mp_err *err) {
+  int64_t V = P->d.nvars, A = P->d.naccess, p = P->d.period;
+  cudaStream_t s = ctx->stream;
+  CUDA_TRY(P->base.alloc(V, s)); CUDA_TRY(P->alloc.alloc(V, s)); CUDA_TRY(P->free_.alloc(V, s));
+  CUDA_TRY(P->nseg.alloc(V, s)); CUDA_TRY(P->seg.alloc(4 * V, s)); CUDA_TRY(P->size.alloc(V, s));
+  CUDA_TRY(P->flags.alloc(V, s)); CUDA_TRY(P->acc_off.alloc(V + 1, s));
+  CUDA_TRY(P->acc_index.alloc(A, s)); CUDA_TRY(P->acc_kind.alloc(A, s)); CUDA_TRY(P->acc_next.alloc(A, s));
+  CUDA_TRY(P->op_times.alloc(p, s)); CUDA_TRY(P->loads.alloc(p, s)); CUDA_TRY(P->op_owner.alloc(p, s));
+  return MP_OK;
+}
+
+static ProfOut prof_out(mp_dprofile *P) {
+  return ProfOut{P->base.p, P->alloc.p, P->free_.p, P->nseg.p, P->seg.p, P->acc_index.p, P->op_owner.p,
+                 P->size.p, P->acc_off.p, P->loads.p, P->flags.p, P->acc_kind.p, P->acc_next.p, P->op_times.p};
+}
+
+extern "C" int mp_extract(mp_ctx *ctx, mp_dtrace *t, int64_t start, int64_t end, mp_dprofile **out,
+                          mp_err *err) {
+  int64_t n = t->n;
+  if (!(0 <= start && start < end && end <= n)) {
+    mp_set_err(err, MP_E_VALUE, start, end, n, "window out of range");
+    return MP_E_VALUE;
+  }
+  int rc = build_groups(ctx, t, err);
+  if (rc) return rc;
+  cudaStream_t st = ctx->stream;
+  int64_t p = end - start;
+  int32_t nv = t->nvars;
+  DBuf<int32_t> owner, w_free, w_nacc, w_mcarry, is_malloc, win_ord, c_free, c_nacc, c_twin, c_surv,
+      carry_ord, nmalloc;
+  DBuf<uint8_t> w_flags, c_live, c_case;
+  DBuf<int64_t> c_abs, c_size;
+  CUDA_TRY(owner.alloc(p, st)); CUDA_TRY(w_free.alloc(p, st)); CUDA_TRY(w_nacc.alloc(p, st));
+  CUDA_TRY(w_mcarry.alloc(p, st)); CUDA_TRY(is_malloc.alloc(p, st)); CUDA_TRY(win_ord.alloc(p, st));
+  CUDA_TRY(w_flags.alloc(p, st));
+  CUDA_TRY(c_free.alloc(nv, st)); CUDA_TRY(c_nacc.alloc(nv, st)); CUDA_TRY(c_twin.alloc(nv, st));
+  CUDA_TRY(c_surv.alloc(nv, st)); CUDA_TRY(carry_ord.alloc(nv, st)); CUDA_TRY(nmalloc.alloc(nv, st));
+  CUDA_TRY(c_live.alloc(nv, st)); CUDA_TRY(c_case.alloc(nv, st)); CUDA_TRY(c_abs.alloc(nv, st));
+  CUDA_TRY(c_size.alloc(nv, st));
+  ExScratch s{owner.p, w_free.p, w_nacc.p, w_flags.p, w_mcarry.p, is_malloc.p, c_live.p, c_abs.p,
+              c_size.p, c_free.p, c_nacc.p, c_case.p, c_twin.p, c_surv.p, nmalloc.p};
+  unsigned long long *d_first = (unsigned long long *)ctx->d_small;
+  CUDA_TRY(cudaMemsetAsync(d_first, 0xff, 8, st));
+  LAUNCH(ctx, k_ex_var, grid_for(nv, 128), 128, 0, t->kind.p, t->size.p, t->perm.p, t->gstart.p, nv,
+         start, end, s, d_first);
+  LAUNCH(ctx, k_ex_marks, grid_for(p, 256), 256, 0, t->kind.p, start, p, is_malloc.p);
+  int64_t first;
+  rc = dev_read_i64(ctx, (const int64_t *)d_first, &first, err);
+  if (rc) return rc;
+  if ((uint64_t)first != ~0ull) {
+    int64_t r = (int64_t)((uint64_t)first >> 4);
+    int32_t v;
+    rc = dev_read_n(ctx, t->var.p + start + r, &v, 4, err);
+    if (rc) return rc;
+    mp_set_err(err, MP_E_INVARIANT, r, (int64_t)(first & 15), v, "window invariant");
+    return MP_E_INVARIANT;
+  }
+  LAUNCH(ctx, k_ex_twin, grid_for(nv, 256), 256, 0, t->kind.p, t->size.p, nv, start, p, s);
+  // carry ordinals (surviving carry-ins, by name = var id) and window ordinals
+  int32_t *d_tot = (int32_t *)ctx->d_small;
+  rc = dev_exclusive_scan<int32_t>(ctx, c_surv.p, carry_ord.p, nv, d_tot, err);
+  if (rc) return rc;
+  rc = dev_exclusive_scan<int32_t>(ctx, is_malloc.p, win_ord.p, p, d_tot + 2, err);
+  if (rc) return rc;
+  int32_t tots[4];
+  rc = dev_read_n(ctx, d_tot, tots, 16, err);
+  if (rc) return rc;
+  int64_t ncarry = tots[0], nwin = tots[2];
+
+  mp_dprofile *P = new mp_dprofile();
+  P->ctx = ctx;
+  P->window0 = start;
+  P->d.period = p;
+  P->d.nvars = ncarry + nwin;
+  P->d.ncarry = ncarry;
+  int64_t V = P->d.nvars;
+  DBuf<int64_t> acc_cnt;
+  CUDA_TRY(acc_cnt.alloc(V + 1, st));
+  CUDA_TRY(P->acc_off.alloc(V + 1, st));
+  // size everything but the access arrays first
+  {
+    cudaStream_t s2 = st;
+    CUDA_TRY(P->base.alloc(V, s2)); CUDA_TRY(P->alloc.alloc(V, s2)); CUDA_TRY(P->free_.alloc(V, s2));
+    CUDA_TRY(P->nseg.alloc(V, s2)); CUDA_TRY(P->seg.alloc(4 * V, s2)); CUDA_TRY(P->size.alloc(V, s2));
+    CUDA_TRY(P->flags.alloc(V, s2));
+    CUDA_TRY(P->op_times.alloc(p, s2)); CUDA_TRY(P->loads.alloc(p, s2)); CUDA_TRY(P->op_owner.alloc(p, s2));
+  }
+  ProfOut o = prof_out(P);
+  // c_surv still holds the 0/1 flags (scan wrote carry_ord)
+  LAUNCH(ctx, k_ex_fill_carry, grid_for(nv, 256), 256, 0, nv, p, s, carry_ord.p, o, acc_cnt.p);
+  LAUNCH(ctx, k_ex_fill_window, grid_for(p, 256), 256, 0, t->var.p, t->size.p, start, p, ncarry, s,
+         win_ord.p, c_surv.p, o, acc_cnt.p);
+  int64_t *d_atot = ctx->d_small + 2;
+  rc = dev_exclusive_scan<int64_t>(ctx, acc_cnt.p, P->acc_off.p, V, d_atot, err);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(P->acc_off.p + V, d_atot, 8, cudaMemcpyDeviceToDevice, st));
+  int64_t A;
+  rc = dev_read_i64(ctx, d_atot, &A, err);
+  if (rc) { delete P; return rc; }
+  P->d.naccess = A;
+  CUDA_TRY(P->acc_index.alloc(A, st)); CUDA_TRY(P->acc_kind.alloc(A, st)); CUDA_TRY(P->acc_next.alloc(A, st));
+  o = prof_out(P);
+  LAUNCH(ctx, k_ex_access, grid_for(nv, 128), 128, 0, t->kind.p, t->perm.p, t->gstart.p, nv, start, end,
+         ncarry, s, carry_ord.p, win_ord.p, o);
+  double *d_dur = (double *)(ctx->d_small + 3);
+  LAUNCH(ctx, k_ex_times, grid_for(p, 256), 256, 0, t->t_us.p, start, end, P->op_times.p, d_dur);
+  rc = profile_loads(ctx, P, err);
+  if (rc) { delete P; return rc; }
+  double dur;
+  rc = dev_read_n(ctx, d_dur, &dur, 8, err);
+  if (rc) { delete P; return rc; }
+  P->d.duration_us = dur;
+  // the profile keeps its own copy of the name table
+  P->nnames = t->nvars;
+  CUDA_TRY(P->blob.alloc(t->name_bytes, st));
+  CUDA_TRY(P->name_off.alloc((int64_t)t->nvars + 1, st));
+  if (t->name_bytes) CUDA_TRY(cudaMemcpyAsync(P->blob.p, t->blob.p, t->name_bytes, cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(P->name_off.p, t->name_off.p, ((int64_t)t->nvars + 1) * 8, cudaMemcpyDeviceToDevice, st));
+  *out = P;
+  return MP_OK;
+}

@@ -80,7 +80,7 @@ class TraceArrays:
     """
 
     __slots__ = ("kind", "var", "size", "t_us", "index", "names",
-                 "name_blob", "name_off", "_meta")
+                 "name_blob", "name_off", "_meta", "_dev")
 
     def __init__(self, kind, var, size, t_us, names: Sequence[str],
                  index=None):
@@ -97,6 +97,7 @@ class TraceArrays:
         self.name_off = off
         self.name_blob = np.frombuffer(b"".join(blobs) or b"\0", dtype=np.uint8).copy()
         self._meta = None
+        self._dev = None
 
     def __len__(self) -> int:
         return int(self.kind.shape[0])
