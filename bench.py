@@ -1,0 +1,341 @@
+"""Benchmark: SmartPool planning throughput on the 1M-variable interval trace.
+
+Workload (BASELINE.json configs[3]): two
+iterations of 1,000,000 interval lifetimes (4,000,008 events); one step is
+the whole pool-planning hot path on the device —
+validate_trace -> detect_iteration -> extract_lifetimes ->
+build_conflict_graph -> plan_pool(best_fit) — over the full trace.
+Metric: planned variables per second (whole job, all ranks).
+
+  value   inputs resident in HBM; offsets stay in HBM
+  e2e     public API (pipeline.plan_arrays) from pinned host arrays: H2D of
+          the trace, the same pipeline, D2H of the offsets
+  roofline  dominant kernel's algorithmic bytes / its CUDA-event time
+  cpu_baseline  the C oracle (sequential restatement of the reference) on
+          this host, rank 0, same trace, 1 thread
+
+N GPUs: one process per GPU (torchrun), each plans its own replica of the
+trace (the path does not shard: "replicas only"); value is the
+sum of planned variables over ranks / max-over-ranks time.
+
+--impl reference: the reference's CPU algorithm (the C oracle port — the
+Python reference cannot run on this box) on all host cores, one trace
+replica per process, same metric.
+"""
+from __future__ import annotations
+
+import argparse
+import hashlib
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path[:0] = [ROOT]
+
+import numpy as np  # noqa: E402
+
+NVARS = 1_000_000
+METRIC = "planned vars/sec (SmartPool plan, bit-exact vs ref)"
+UNIT = "vars/s"
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_PATH) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# algorithmic bytes per stage
+
+def stage_bytes(n, p, V, nnz, levels):
+    """Minimal HBM bytes each stage must move for one trace."""
+    return {
+        "group_sort": n * 4 + n * 4,                     # read var ids, write grouping permutation
+        "validate": n * (1 + 8 + 8) + n * 4,             # kind/size/t + permutation walk
+        "detect": n * (1 + 8) + (n + 1) * 8,             # fingerprints read, prefix hashes written
+        "extract": n * 4 + p * (1 + 4 + 8 + 8) + V * 44 + p * 12,
+        "loads": V * 24 + p * 16,
+        "conflict_prep": V * 24 + V * 24,
+        "conflict_fill": nnz * 4 + V * 16,               # CSR column writes + row metadata
+        "place_order": V * 8 + V * 4,
+        "place_split": nnz * (4 + 4 + 4),                # read col + rank gather + write partitioned col
+        "place": nnz // 2 * (4 + 8 + 8) + nnz // 2 * (4 + 4) + V * 24,
+        "footprint": V * 16,
+    }
+
+
+# ---------------------------------------------------------------------------
+
+
+def build_workload(accesses: bool):
+    from paper_1903_06631_b200 import workloads
+    arrays, window = workloads.interval_trace(NVARS, seed=0, accesses=accesses)
+    return arrays, window
+
+
+def pinned_like(a: np.ndarray):
+    import torch
+    t = torch.empty(a.nbytes, dtype=torch.uint8, pin_memory=True)
+    view = t.numpy().view(a.dtype)[: a.size].reshape(a.shape)
+    view[...] = a
+    return t, view
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    torch.cuda.set_device(local_rank)
+    os.environ["MEMPLAN_DEVICE"] = str(local_rank)
+    from paper_1903_06631_b200 import _native as N
+    from paper_1903_06631_b200.pipeline import plan_arrays
+    from paper_1903_06631_b200.trace import TraceArrays
+
+    arrays, window = build_workload(args.accesses)
+    n = len(arrays)
+    # pinned host copies for the e2e leg (a user hands us host buffers)
+    keep = []
+    cols = {}
+    for name in ("kind", "var", "size", "t_us"):
+        t, v = pinned_like(getattr(arrays, name))
+        keep.append(t)
+        cols[name] = v
+    host = TraceArrays(cols["kind"], cols["var"], cols["size"], cols["t_us"], arrays.names)
+    out_t, out_offs = pinned_like(np.zeros(NVARS + 1, np.int64))
+    keep.append(out_t)
+
+    stream = torch.cuda.ExternalStream(N.stream_ptr())
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def l2_flush():
+        with torch.cuda.stream(stream):
+            flush.zero_()
+
+    # ---- value: resident inputs ----
+    dev_arrays = arrays  # uploaded once below; the trace handle stays in HBM
+    plan = None
+    for _ in range(args.warmup):
+        plan = plan_arrays(dev_arrays, keep_on_device=True)
+    N.sync()
+    first = N.launches()
+    N.set_timing(True)
+    times = []
+    with ClockSampler(local_rank) as clk:
+        for _ in range(args.steps):
+            l2_flush()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(stream)
+            plan = plan_arrays(dev_arrays, keep_on_device=True)
+            e.record(stream)
+            e.synchronize()
+            times.append(s.elapsed_time(e))
+    stages = N.timings()
+    N.set_timing(False)
+    launches = N.launches() - first
+    step_ms = float(np.mean(times))
+    # ---- e2e: pinned host -> device -> pinned host, public API ----
+    e2e_times = []
+    for i in range(args.warmup + args.steps):
+        host._dev = None  # every step uploads the trace afresh
+        l2_flush()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        p2 = plan_arrays(host, offsets_out=out_offs)
+        e.record(stream)
+        e.synchronize()
+        if i >= args.warmup:
+            e2e_times.append(s.elapsed_time(e))
+    e2e_ms = float(np.mean(e2e_times))
+    sha = hashlib.sha256(out_offs[:p2.nvars].tobytes()).hexdigest()
+    h2d = sum(getattr(host, c).nbytes for c in ("kind", "var", "size", "t_us")) + \
+        host.name_blob.nbytes + host.name_off.nbytes
+    d2h = p2.nvars * 8
+
+    # max over ranks
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([step_ms, e2e_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        step_ms, e2e_ms = float(tt[0]), float(tt[1])
+    vars_total = plan.nvars * world
+    res = {
+        "plan": plan, "step_ms": step_ms, "e2e_ms": e2e_ms, "stages": stages, "launches": launches,
+        "clocks": clk.summary(), "sha": sha, "h2d": h2d, "d2h": d2h, "n": n, "vars_total": vars_total,
+        "footprint_e2e": p2.footprint_bytes,
+    }
+    return arrays, res
+
+
+def cpu_baseline(arrays):
+    """C oracle on this host: detect + extract + conflict + best_fit plan, 1 thread."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as orc
+    t0 = time.perf_counter()
+    rc, p = orc.detect(arrays)
+    rc, fp = orc.extract(arrays, len(arrays) - p, len(arrays))
+    off, lo, hi = orc.profile_segments(fp)
+    h, row, col = orc.conflict(off, lo, hi)
+    rc, offs, foot = orc.plan(h, fp.size, fp.alloc.astype(np.int64), fp.base, fp.name_ralloc(),
+                              fp.name_blob, fp.name_off, 1)
+    dt = time.perf_counter() - t0
+    orc.graph_free(h)
+    return {"value": fp.nvars / dt, "seconds": dt, "footprint": foot, "peak": fp.peak_bytes,
+            "sha": hashlib.sha256(offs.tobytes()).hexdigest(), "nvars": fp.nvars}
+
+
+def _ref_worker(args):
+    accesses, = args
+    sys.path[:0] = [ROOT, os.path.join(ROOT, "oracle")]
+    arrays, _ = build_workload(accesses)
+    return cpu_baseline(arrays)
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    import multiprocessing as mp
+    procs = os.cpu_count() or 1
+    ctx = mp.get_context("fork")
+    step_s = []
+    with ctx.Pool(procs) as pool:
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            outs = pool.map(_ref_worker, [(args.accesses,)] * procs)
+            dt = time.perf_counter() - t0
+            if i >= args.warmup:
+                step_s.append(max(o["seconds"] for o in outs))
+    step = float(np.mean(step_s))
+    value = procs * outs[0]["nvars"] / step
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic", "config": {"workload": "interval_trace_1M (BASELINE configs[3])",
+                                            "nvars": NVARS, "policy": "best_fit"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port",
+                             "sample": f"{procs} replicas of the full 1M-var trace, one per process "
+                                       "(C oracle; the Python reference is not on this box)"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--accesses", action="store_true", help="config-4 variant with write/read per var")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dist.barrier()
+    arrays, r = run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    if rank != 0:
+        return 0
+    plan = r["plan"]
+    peak, peak_src = hbm_peak()
+    stages = r["stages"]
+    steps = args.steps
+    sb = stage_bytes(r["n"], plan.period, plan.nvars, plan.nnz, plan.levels)
+    per_stage = {k: ms / steps for k, (ms, _c) in stages.items()}
+    dom = max(per_stage, key=per_stage.get)
+    achieved = sb.get(dom, 0) / (per_stage[dom] * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": r["vars_total"] / (r["step_ms"] * 1e-3), "unit": UNIT,
+        "n_gpus": world, "steps": steps, "warmup": args.warmup, "ms_per_step": r["step_ms"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic",
+        "config": {"workload": "interval_trace_1M (BASELINE configs[3])", "nvars": NVARS,
+                   "events": r["n"], "period": plan.period, "policy": "best_fit",
+                   "accesses": bool(args.accesses), "l2": "flushed (256 MiB write) between steps",
+                   "parallelism": f"replicas x{world}"},
+        "result": {"peak_bytes": plan.peak_bytes, "footprint_bytes": plan.footprint_bytes,
+                   "alpha": plan.competitive_ratio, "levels": plan.levels, "csr_entries": plan.nnz,
+                   "offsets_sha256": r["sha"][:16]},
+        "e2e": {"value": r["vars_total"] / (r["e2e_ms"] * 1e-3), "unit": UNIT,
+                "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"], "ms_per_step": r["e2e_ms"]},
+        "gpu_launches": r["launches"],
+        "stage_ms": {k: round(v, 4) for k, v in per_stage.items()},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                     "algorithmic_bytes": sb.get(dom, 0)},
+        "clocks": r["clocks"],
+    }
+    if not args.no_cpu_baseline:
+        cb = cpu_baseline(arrays)
+        line["cpu_baseline"] = {"value": cb["value"], "unit": UNIT, "cores": 1, "kind": "port",
+                                "sample": f"full 1M-var trace, {cb['seconds']:.2f} s, C oracle 1 thread"}
+        line["parity"] = {"footprint_equal": cb["footprint"] == plan.footprint_bytes,
+                          "peak_equal": cb["peak"] == plan.peak_bytes,
+                          "offsets_equal": cb["sha"] == r["sha"]}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -138,11 +138,34 @@ int mp_ctx_sync(mp_ctx *ctx, mp_err *err);
 /* stream the context launches on (cudaStream_t as void*) */
 void *mp_ctx_stream(mp_ctx *ctx);
 
+/* per-stage device time, measured with CUDA events recorded on the
+ * context stream around each stage while timing is on */
+enum {
+  MP_ST_GROUP_SORT = 0, /* radix sort of events by variable */
+  MP_ST_VALIDATE,       /* validate_trace kernels */
+  MP_ST_DETECT,         /* period hashes + candidates + verify */
+  MP_ST_EXTRACT,        /* per-variable state machines, twins, records */
+  MP_ST_LOADS,          /* diff scatter + scan + peak */
+  MP_ST_CONFLICT_PREP,  /* interval normalization, sorts, counts */
+  MP_ST_CONFLICT_FILL,  /* CSR fill */
+  MP_ST_PLACE_ORDER,    /* placement-order sort */
+  MP_ST_PLACE_SPLIT,    /* row partition into preds / succs */
+  MP_ST_PLACE,          /* wavefront placement kernel */
+  MP_ST_FOOTPRINT,
+  MP_ST_SWAP,           /* swap planning kernels */
+  MP_NSTAGES = 16
+};
+int mp_ctx_set_timing(mp_ctx *ctx, int on);
+/* accumulated ms and event-pair counts per stage since the last call */
+int mp_ctx_timings(mp_ctx *ctx, double *ms, int64_t *count, mp_err *err);
+
 /* validate_trace (trace.py:55-84) + upload.  Replaces
  * memplan.trace.validate_trace; the first violation is reported exactly as
  * the sequential reference would. */
 int mp_trace_upload(mp_ctx *ctx, const mp_trace_in *in, mp_dtrace **out, mp_err *err);
 int mp_trace_free(mp_dtrace *t);
+/* drop cached derived state (event grouping) so the next stage recomputes it */
+int mp_trace_reset(mp_dtrace *t);
 int mp_validate(mp_ctx *ctx, mp_dtrace *t, mp_err *err);
 
 /* detect_iteration (iteration.py:93-105): smallest p with the last 2p
@@ -175,10 +198,13 @@ int mp_conflict_from_arcs(mp_ctx *ctx, int32_t nvars, const int64_t *size,
 int mp_graph_dims(mp_dgraph *g, int64_t *nvars, int64_t *nnz);
 int mp_graph_download(mp_ctx *ctx, mp_dgraph *g, int64_t *row_off, int32_t *col, mp_err *err);
 int mp_graph_free(mp_dgraph *g);
+/* device pointer of the last plan's offsets (int64[nvars]) */
+const int64_t *mp_graph_offsets_device(mp_dgraph *g);
 
 /* plan_pool (smartpool.py:91-144).  policy 0 = first_fit, 1 = best_fit.
  * Placement order (-size, alloc, name) — the tie part comes from the
- * graph's tiekey (profile order for profiles). */
+ * graph's tiekey (profile order for profiles).  offsets may be NULL: the
+ * result then stays on the device (mp_graph_offsets_device). */
 int mp_plan_pool(mp_ctx *ctx, mp_dgraph *g, int32_t policy, int64_t *offsets,
                  int64_t *footprint, int64_t *levels, mp_err *err);
 

@@ -215,14 +215,42 @@ def graph_dims(g: DGraph):
     return int(nv.value), int(nnz.value)
 
 
-def plan_pool(g: DGraph, policy: int, nvars: int):
-    offs = np.zeros(max(nvars, 1), np.int64)
+def plan_pool(g: DGraph, policy: int, nvars: int, out: np.ndarray | None = None):
+    offs = np.zeros(max(nvars, 1), np.int64) if out is None else out
     fp = C.c_int64(0)
     lv = C.c_int64(0)
     err = MpErr()
     rc = lib().mp_plan_pool(ctx(), g.h, C.c_int32(policy), ptr(offs), C.byref(fp), C.byref(lv), C.byref(err))
     raise_for(rc, err, what=f"unknown policy {policy!r}")
     return offs[:nvars], int(fp.value), int(lv.value)
+
+
+def plan_pool_device(g: DGraph, policy: int):
+    """Plan and leave the offsets in HBM (mp_graph_offsets_device)."""
+    fp = C.c_int64(0)
+    lv = C.c_int64(0)
+    err = MpErr()
+    rc = lib().mp_plan_pool(ctx(), g.h, C.c_int32(policy), None, C.byref(fp), C.byref(lv), C.byref(err))
+    raise_for(rc, err, what=f"unknown policy {policy!r}")
+    return int(fp.value), int(lv.value)
+
+
+STAGES = ("group_sort", "validate", "detect", "extract", "loads", "conflict_prep", "conflict_fill",
+          "place_order", "place_split", "place", "footprint", "swap")
+
+
+def set_timing(on: bool) -> None:
+    lib().mp_ctx_set_timing(ctx(), C.c_int(1 if on else 0))
+
+
+def timings() -> dict:
+    """Accumulated per-stage device ms (CUDA events on the library stream)."""
+    ms = (C.c_double * 16)()
+    cnt = (C.c_int64 * 16)()
+    err = MpErr()
+    rc = lib().mp_ctx_timings(ctx(), ms, cnt, C.byref(err))
+    raise_for(rc, err)
+    return {name: (float(ms[i]), int(cnt[i])) for i, name in enumerate(STAGES) if cnt[i]}
 
 
 _ = (MpProfileOut,)

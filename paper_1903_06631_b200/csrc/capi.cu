@@ -48,6 +48,32 @@ extern "C" int mp_ctx_sync(mp_ctx *c, mp_err *err) {
 
 extern "C" void *mp_ctx_stream(mp_ctx *c) { return (void *)c->stream; }
 
+extern "C" int mp_ctx_set_timing(mp_ctx *c, int on) {
+  c->timing = on != 0;
+  return MP_OK;
+}
+
+extern "C" int mp_ctx_timings(mp_ctx *c, double *ms, int64_t *count, mp_err *err) {
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  for (int i = 0; i < MP_NSTAGES; i++) { ms[i] = 0.0; count[i] = 0; }
+  for (auto &r : c->pending) {
+    float t = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&t, r.a, r.b));
+    if (r.id >= 0 && r.id < MP_NSTAGES) { ms[r.id] += t; count[r.id]++; }
+    c->spare.push_back(r.a);
+    c->spare.push_back(r.b);
+  }
+  c->pending.clear();
+  return MP_OK;
+}
+
+extern "C" int mp_trace_reset(mp_dtrace *t) {
+  t->grouped = false;
+  t->perm.release();
+  t->gstart.release();
+  return MP_OK;
+}
+
 extern "C" int mp_trace_upload(mp_ctx *ctx, const mp_trace_in *in, mp_dtrace **out, mp_err *err) {
   cudaStream_t st = ctx->stream;
   mp_dtrace *t = new mp_dtrace();

@@ -18,6 +18,11 @@
 #define MP_WARP 32
 #define FULL_MASK 0xffffffffu
 
+struct mp_stage_rec {
+  int id;
+  cudaEvent_t a, b;
+};
+
 struct mp_ctx {
   int device = 0;
   int num_sms = 148;
@@ -26,6 +31,36 @@ struct mp_ctx {
   // pinned host staging for small scalar readbacks
   int64_t *h_small = nullptr;
   int64_t *d_small = nullptr;
+  // stage timing (CUDA events on `stream`)
+  bool timing = false;
+  std::vector<mp_stage_rec> pending;
+  std::vector<cudaEvent_t> spare;
+  cudaEvent_t event() {
+    cudaEvent_t e;
+    if (!spare.empty()) { e = spare.back(); spare.pop_back(); }
+    else cudaEventCreate(&e);
+    return e;
+  }
+};
+
+// RAII: brackets a stage with events on the context stream when timing is on
+struct StageTimer {
+  mp_ctx *c;
+  int id;
+  cudaEvent_t a = nullptr;
+  StageTimer(mp_ctx *c_, int id_) : c(c_), id(id_) {
+    if (c->timing) {
+      a = c->event();
+      cudaEventRecord(a, c->stream);
+    }
+  }
+  ~StageTimer() {
+    if (a) {
+      cudaEvent_t b = c->event();
+      cudaEventRecord(b, c->stream);
+      c->pending.push_back({id, a, b});
+    }
+  }
 };
 
 // ----------------------------------------------------------------------------

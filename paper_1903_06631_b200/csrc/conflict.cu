@@ -88,22 +88,44 @@ __global__ void k_row_off(int64_t nv, const int64_t *eoff, const int64_t *sub_of
     row_off[v] = sub_off[eoff[v]];
 }
 
-// warp per sorted interval: forward run + mirrored backward entries
+// warp per sorted interval: the forward run and its mirror, written straight
+// into placement-partitioned rows (predecessors grow from the row start,
+// successors from the row end) so plan_pool needs no separate split pass
 __global__ void k_iv_fill(int64_t n, const uint32_t *perm, const int32_t *ivar, const int32_t *fwd,
-                          const int64_t *sub_off, int32_t *bcur, int32_t *col) {
+                          const int64_t *row_off, const int32_t *rank, int32_t *pc, int32_t *sc, int32_t *col) {
   const int lane = threadIdx.x & 31;
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const unsigned lt = lanemask_lt();
   for (int64_t k = warp; k < n; k += nwarps) {
     uint32_t iid = perm[k];
     int32_t u = ivar[iid];
     int32_t f = fwd[iid];
-    int64_t so = sub_off[iid];
-    for (int32_t j = lane; j < f; j += 32) {
-      uint32_t jid = perm[k + 1 + j];
-      col[so + j] = ivar[jid];
-      int32_t slot = atomicAdd(&bcur[jid], 1);
-      col[sub_off[jid] + fwd[jid] + slot] = u;
+    int32_t ru = rank[u];
+    int64_t rbu = row_off[u], reu = row_off[u + 1];
+    for (int32_t base = 0; base < f; base += 32) {
+      int32_t jx = base + lane;
+      bool valid = jx < f;
+      int32_t j = valid ? ivar[perm[k + 1 + jx]] : 0;
+      bool isp = valid && rank[j] < ru;  // j precedes u in placement order
+      unsigned bp = __ballot_sync(FULL_MASK, isp);
+      unsigned bs = __ballot_sync(FULL_MASK, valid && !isp);
+      int32_t p0 = 0, s0 = 0;
+      if (lane == 0) {
+        if (bp) p0 = atomicAdd(&pc[u], __popc(bp));
+        if (bs) s0 = atomicAdd(&sc[u], __popc(bs));
+      }
+      p0 = __shfl_sync(FULL_MASK, p0, 0);
+      s0 = __shfl_sync(FULL_MASK, s0, 0);
+      if (isp) {
+        col[rbu + p0 + __popc(bp & lt)] = j;
+        int32_t q = atomicAdd(&sc[j], 1);  // u succeeds j
+        col[row_off[j + 1] - 1 - q] = u;
+      } else if (valid) {
+        col[reu - 1 - (s0 + __popc(bs & lt))] = j;
+        int32_t q = atomicAdd(&pc[j], 1);  // u precedes j
+        col[row_off[j] + q] = u;
+      }
     }
   }
 }
@@ -111,6 +133,14 @@ __global__ void k_iv_fill(int64_t n, const uint32_t *perm, const int32_t *ivar, 
 static int build_csr(mp_ctx *ctx, int64_t nv, const int64_t *seg_off_d, const int32_t *lo_d,
                      const int32_t *hi_d, mp_dgraph *g, mp_err *err) {
   cudaStream_t st = ctx->stream;
+  // placement order first: the fill writes rows already split by it
+  CUDA_TRY(g->rank.alloc(nv, st));
+  CUDA_TRY(g->pcnt.alloc(nv, st));
+  if (nv) {
+    int rc0 = placement_rank(ctx, nv, g->size.p, g->tiekey.p, g->rank.p, err);
+    if (rc0) return rc0;
+  }
+  StageTimer *tm = new StageTimer(ctx, MP_ST_CONFLICT_PREP);
   DBuf<int64_t> ecnt, eoff;
   CUDA_TRY(ecnt.alloc(nv + 1, st));
   CUDA_TRY(eoff.alloc(nv + 1, st));
@@ -130,9 +160,9 @@ static int build_csr(mp_ctx *ctx, int64_t nv, const int64_t *seg_off_d, const in
     return MP_E_UNSUPPORTED;
   }
   int64_t ni = h[1];
-  DBuf<int32_t> ea, eb, ivar, fwd, bcur;
+  DBuf<int32_t> ea, eb, ivar, fwd, scur;
   CUDA_TRY(ea.alloc(ni, st)); CUDA_TRY(eb.alloc(ni, st)); CUDA_TRY(ivar.alloc(ni, st));
-  CUDA_TRY(fwd.alloc(ni, st)); CUDA_TRY(bcur.alloc(ni, st));
+  CUDA_TRY(fwd.alloc(ni, st)); CUDA_TRY(scur.alloc(nv, st));
   LAUNCH(ctx, k_norm_count, grid_for(nv, 128), 128, 0, nv, seg_off_d, lo_d, hi_d, ecnt.p, ea.p, eb.p,
          d_over, 1, eoff.p, ivar.p);
   // sort starts (with interval ids) and ends
@@ -161,9 +191,12 @@ static int build_csr(mp_ctx *ctx, int64_t nv, const int64_t *seg_off_d, const in
   CUDA_TRY(g->row_off.alloc(nv + 1, st));
   CUDA_TRY(g->col.alloc(nnz, st));
   LAUNCH(ctx, k_row_off, grid_for(nv + 1, 256), 256, 0, nv, eoff.p, sub_off.p, g->row_off.p);
-  CUDA_TRY(cudaMemsetAsync(bcur.p, 0, ni * 4, st));
-  LAUNCH(ctx, k_iv_fill, grid_for(ni * 32, 256, 148 * 64), 256, 0, ni, perm.p, ivar.p, fwd.p, sub_off.p,
-         bcur.p, g->col.p);
+  CUDA_TRY(cudaMemsetAsync(scur.p, 0, nv * 4, st));
+  CUDA_TRY(cudaMemsetAsync(g->pcnt.p, 0, nv * 4, st));
+  delete tm;
+  StageTimer fill(ctx, MP_ST_CONFLICT_FILL);
+  LAUNCH(ctx, k_iv_fill, grid_for(ni * 32, 256, 148 * 64), 256, 0, ni, perm.p, ivar.p, fwd.p, g->row_off.p,
+         g->rank.p, g->pcnt.p, scur.p, g->col.p);
   return MP_OK;
 }
 
@@ -189,10 +222,12 @@ extern "C" int mp_conflict_from_profile(mp_ctx *ctx, mp_dprofile *P, mp_dgraph *
   else LAUNCH(ctx, k_prof_segs, grid_for(nv, 256), 256, 0, nv, P->nseg.p, P->seg.p, so.p, lo.p, hi.p);
   mp_dgraph *g = new mp_dgraph();
   g->ctx = ctx;
-  int rc = build_csr(ctx, nv, so.p, lo.p, hi.p, g, err);
-  if (rc) { delete g; return rc; }
   CUDA_TRY(g->size.alloc(nv, st));
   if (nv) CUDA_TRY(cudaMemcpyAsync(g->size.p, P->size.p, nv * 8, cudaMemcpyDeviceToDevice, st));
+  // profile variables are already in (alloc or -1, name) order: the
+  // placement tie-break is the vertex index
+  int rc = build_csr(ctx, nv, so.p, lo.p, hi.p, g, err);
+  if (rc) { delete g; return rc; }
   *out = g;
   return MP_OK;
 }
@@ -212,14 +247,14 @@ extern "C" int mp_conflict_from_arcs(mp_ctx *ctx, int32_t nvars, const int64_t *
   }
   mp_dgraph *g = new mp_dgraph();
   g->ctx = ctx;
-  int rc = build_csr(ctx, nv, so.p, lo.p, hi.p, g, err);
-  if (rc) { delete g; return rc; }
   CUDA_TRY(g->size.alloc(nv, st));
   CUDA_TRY(g->tiekey.alloc(nv, st));
   if (nv) {
     CUDA_TRY(cudaMemcpyAsync(g->size.p, size, nv * 8, cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaMemcpyAsync(g->tiekey.p, tiekey, nv * 8, cudaMemcpyHostToDevice, st));
   }
+  int rc = build_csr(ctx, nv, so.p, lo.p, hi.p, g, err);
+  if (rc) { delete g; return rc; }
   CUDA_TRY(cudaStreamSynchronize(st));  // host arrays are only borrowed for the call
   *out = g;
   return MP_OK;

@@ -44,6 +44,11 @@ struct mp_dgraph {
   DBuf<int32_t> col;
   DBuf<int64_t> size;     // vertex weights
   DBuf<int64_t> tiekey;   // placement tie-break after -size (empty: vertex order)
+  DBuf<int64_t> offsets;  // last plan
+  DBuf<int32_t> rank;     // position in the placement order (-size, tie)
+  DBuf<int32_t> pcnt;     // row prefix holding the placement predecessors
 };
 
 int build_groups(mp_ctx *ctx, mp_dtrace *t, mp_err *err);
+int placement_rank(mp_ctx *ctx, int64_t V, const int64_t *size, const int64_t *tiekey, int32_t *rank,
+                   mp_err *err);

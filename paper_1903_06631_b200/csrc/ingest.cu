@@ -14,6 +14,8 @@
 // window (window instances) or by variable id (carry-ins); prefix sums turn
 // them into the reference's variable order (carry-ins by name, then window
 // instances by alloc index).
+#include <climits>
+
 #include "handles.cuh"
 
 // ---------------------------------------------------------------------------
@@ -39,6 +41,7 @@ __global__ void k_group_bounds(const uint32_t *skeys, int64_t n, int32_t nvars, 
 
 int build_groups(mp_ctx *ctx, mp_dtrace *t, mp_err *err) {
   if (t->grouped) return MP_OK;
+  StageTimer tm(ctx, MP_ST_GROUP_SORT);
   int64_t n = t->n;
   DBuf<uint32_t> keys;
   CUDA_TRY(keys.alloc(n, ctx->stream));
@@ -95,6 +98,7 @@ extern "C" int mp_validate(mp_ctx *ctx, mp_dtrace *t, mp_err *err) {
   if (t->n == 0) return MP_OK;
   int rc = build_groups(ctx, t, err);
   if (rc) return rc;
+  StageTimer tm(ctx, MP_ST_VALIDATE);
   unsigned long long *d_first = (unsigned long long *)ctx->d_small;
   CUDA_TRY(cudaMemsetAsync(d_first, 0xff, 8, ctx->stream));
   LAUNCH(ctx, k_validate_elem, grid_for(t->n, 256, 4096), 256, 0, t->kind.p, t->size.p, t->t_us.p,
@@ -255,6 +259,7 @@ extern "C" int mp_detect(mp_ctx *ctx, mp_dtrace *t, int64_t *period, mp_err *err
     mp_set_err(err, MP_E_PERIOD_NOT_FOUND, n, 0, 0, "no period");
     return MP_E_PERIOD_NOT_FOUND;
   }
+  StageTimer tm(ctx, MP_ST_DETECT);
   int64_t ntiles = (n + DT_TILE - 1) / DT_TILE;
   DBuf<HPair> agg;
   DBuf<uint64_t> P;
@@ -577,6 +582,7 @@ __global__ void k_load_argmax(const int64_t *loads, int64_t p, const long long *
 
 // loads + peak for any device profile (also used after uploads)
 int profile_loads(mp_ctx *ctx, mp_dprofile *P, mp_err *err) {
+  StageTimer tm(ctx, MP_ST_LOADS);
   int64_t p = P->d.period, V = P->d.nvars;
   DBuf<int64_t> diff;
   CUDA_TRY(diff.alloc(p + 1, ctx->stream));
@@ -631,6 +637,7 @@ extern "C" int mp_extract(mp_ctx *ctx, mp_dtrace *t, int64_t start, int64_t end,
   if (rc) return rc;
   cudaStream_t st = ctx->stream;
   int64_t p = end - start;
+  StageTimer *tm = new StageTimer(ctx, MP_ST_EXTRACT);
   int32_t nv = t->nvars;
   DBuf<int32_t> owner, w_free, w_nacc, w_mcarry, is_malloc, win_ord, c_free, c_nacc, c_twin, c_surv,
       carry_ord, nmalloc;
@@ -710,6 +717,7 @@ extern "C" int mp_extract(mp_ctx *ctx, mp_dtrace *t, int64_t start, int64_t end,
          ncarry, s, carry_ord.p, win_ord.p, o);
   double *d_dur = (double *)(ctx->d_small + 3);
   LAUNCH(ctx, k_ex_times, grid_for(p, 256), 256, 0, t->t_us.p, start, end, P->op_times.p, d_dur);
+  delete tm;
   rc = profile_loads(ctx, P, err);
   if (rc) { delete P; return rc; }
   double dur;

@@ -15,13 +15,14 @@
 // first_fit takes the lowest qualifying hole (ballot + ffs), best_fit the
 // (length, offset) minimum (warp reduction), otherwise the running top.
 //
-// One persistent cooperative kernel runs all levels with a grid barrier
-// between them; tiny graphs use a single CTA and __syncthreads.
-#include <cooperative_groups.h>
+// Scheduling is asynchronous dataflow: a ready queue (claimed in order,
+// published by the last predecessor to finish) feeds persistent warps, so
+// a variable starts as soon as its own predecessors are placed instead of
+// waiting for a whole wavefront.  The CSR rows arrive partitioned into
+// predecessors and successors by the conflict build (conflict.cu).
+#include <climits>
 
 #include "handles.cuh"
-
-namespace cg = cooperative_groups;
 
 struct IV {
   int64_t s, e;
@@ -30,42 +31,66 @@ struct IV {
 struct PlaceArgs {
   int64_t V;
   const int64_t *row_off;
-  const int32_t *col2;  // row partitioned: preds first, then succs
+  const int32_t *col;   // rows partitioned: preds (earlier in placement order) first
   const int32_t *pcnt;
   const int64_t *size;
   int64_t *off;
-  int32_t *remaining;
-  int32_t *F0, *F1;
-  int32_t *counts;  // 3 rotating frontier counters
-  int policy;       // 0 first_fit, 1 best_fit
-  int cap;          // shared-memory ranges per warp
-  IV *gscratch;
-  int64_t gcap;
-  int32_t *levels;
+  int32_t *level;       // DAG depth of each placed variable
+  int32_t *remaining;   // unplaced preds
+  int32_t *queue;       // ready variables, v + 1 (0 = slot not yet published)
+  int32_t *head, *tail;
+  int policy;           // 0 first_fit, 1 best_fit
+  IV *wscratch;         // 128 ranges per warp (packed-key fallback)
+  IV *arena;            // long rows (> 128 preds) bump-allocate here
+  unsigned long long *arena_top;
+  long long *footprint;
+  int32_t *depth;
 };
 
 __device__ __forceinline__ bool iv_less(int64_t as, int64_t ae, int64_t bs, int64_t be) {
   return as < bs || (as == bs && ae < be);
 }
 
-__device__ __forceinline__ void warp_bitonic32(int64_t &s, int64_t &e) {
+// bitonic sort of 32*K (start, end) pairs held as element i = r*32 + lane
+template <int K>
+__device__ __forceinline__ void warp_bitonic_reg(int64_t (&s)[K], int64_t (&e)[K]) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
-  for (int k = 2; k <= 32; k <<= 1) {
+  for (int k = 2; k <= 32 * K; k <<= 1) {
 #pragma unroll
     for (int j = k >> 1; j > 0; j >>= 1) {
-      int64_t os = __shfl_xor_sync(FULL_MASK, s, j);
-      int64_t oe = __shfl_xor_sync(FULL_MASK, e, j);
-      bool up = (lane & k) == 0;
-      bool lower = (lane & j) == 0;
-      bool other_less = iv_less(os, oe, s, e);
-      bool take_other = (lower == up) ? other_less : iv_less(s, e, os, oe);
-      if (take_other) { s = os; e = oe; }
+      if (j >= 32) {
+        const int jr = j >> 5;
+#pragma unroll
+        for (int r = 0; r < K; r++) {
+          if ((r & jr) == 0) {
+            const int r2 = r | jr;
+            const bool up = ((r * 32) & k) == 0;
+            bool gt = iv_less(s[r2], e[r2], s[r], e[r]);
+            if (up == gt) {
+              int64_t ts = s[r], te = e[r];
+              s[r] = s[r2]; e[r] = e[r2]; s[r2] = ts; e[r2] = te;
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < K; r++) {
+          int64_t os = __shfl_xor_sync(FULL_MASK, s[r], j);
+          int64_t oe = __shfl_xor_sync(FULL_MASK, e[r], j);
+          const bool up = ((r * 32 + lane) & k) == 0;
+          const bool lower = (lane & j) == 0;
+          bool take = (lower == up) ? iv_less(os, oe, s[r], e[r]) : iv_less(s[r], e[r], os, oe);
+          if (take) { s[r] = os; e[r] = oe; }
+        }
+      }
     }
   }
 }
 
-__device__ void warp_bitonic_mem(IV *buf, int n2) {
+// bitonic sort of n2 pairs in memory (shared or global), one warp
+template <typename P>
+__device__ void warp_bitonic_mem(P buf, int n2) {
   const int lane = threadIdx.x & 31;
   for (int k = 2; k <= n2; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
@@ -98,14 +123,12 @@ __device__ __forceinline__ bool hole_chunk(HoleState &h, int64_t s, int64_t e, b
   int64_t excl = __shfl_up_sync(FULL_MASK, incl, 1);
   if (lane == 0) excl = INT64_MIN;
   int64_t tb = excl > h.top ? excl : h.top;
-  bool hole = valid && s > tb;
+  bool ok = valid && s > tb && s - tb >= need;
   int64_t len = s - tb;
-  bool ok = hole && len >= need;
   unsigned bal = __ballot_sync(FULL_MASK, ok);
   if (policy == 0) {
     if (bal) {
-      int first = __ffs(bal) - 1;
-      h.best_off = __shfl_sync(FULL_MASK, tb, first);
+      h.best_off = __shfl_sync(FULL_MASK, tb, __ffs(bal) - 1);
       h.found = true;
       return true;
     }
@@ -127,88 +150,193 @@ __device__ __forceinline__ bool hole_chunk(HoleState &h, int64_t s, int64_t e, b
   return false;
 }
 
-__device__ int64_t place_one(const PlaceArgs &a, int64_t v, IV *wbuf, IV *gbuf) {
+__device__ __forceinline__ int warp_max_i32(int v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(FULL_MASK, v, o));
+  return v;
+}
+
+// bitonic sort of 32*K unsigned keys held as element i = r*32 + lane
+template <int K>
+__device__ __forceinline__ void warp_bitonic_keys(uint64_t (&x)[K]) {
   const int lane = threadIdx.x & 31;
-  int64_t rb = a.row_off[v];
-  int m = a.pcnt[v];
-  int64_t need = a.size[v];
-  if (m == 0) return 0;
-  HoleState h{0, 0, 0, false};
-  if (m <= 32) {
-    int64_t s = INT64_MAX, e = INT64_MAX;
-    if (lane < m) {
-      int32_t j = a.col2[rb + lane];
-      s = __ldcg(&a.off[j]);
-      e = s + a.size[j];
-    }
-    warp_bitonic32(s, e);
-    hole_chunk(h, s, e, lane < m, need, a.policy);
-  } else {
-    IV *buf = m <= a.cap ? wbuf : gbuf;
-    int n2 = 64;
-    while (n2 < m) n2 <<= 1;
-    for (int i = lane; i < n2; i += 32) {
-      IV x{INT64_MAX, INT64_MAX};
-      if (i < m) {
-        int32_t j = a.col2[rb + i];
-        x.s = __ldcg(&a.off[j]);
-        x.e = x.s + a.size[j];
+#pragma unroll
+  for (int k = 2; k <= 32 * K; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+        const int jr = j >> 5;
+#pragma unroll
+        for (int r = 0; r < K; r++) {
+          if ((r & jr) == 0) {
+            const int r2 = r | jr;
+            const bool up = ((r * 32) & k) == 0;
+            uint64_t lo = min(x[r], x[r2]), hi = max(x[r], x[r2]);
+            x[r] = up ? lo : hi;
+            x[r2] = up ? hi : lo;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < K; r++) {
+          uint64_t o = __shfl_xor_sync(FULL_MASK, x[r], j);
+          const bool up = ((r * 32 + lane) & k) == 0;
+          const bool lower = (lane & j) == 0;
+          x[r] = (lower == up) ? min(x[r], o) : max(x[r], o);
+        }
       }
-      buf[i] = x;
     }
-    __syncwarp();
-    warp_bitonic_mem(buf, n2);
-    for (int base = 0; base < m; base += 32) {
-      int i = base + lane;
-      IV x = i < m ? buf[i] : IV{0, 0};
-      if (hole_chunk(h, x.s, x.e, i < m, need, a.policy)) break;
+  }
+}
+
+// Gather the predecessors' ranges, sort them by start and replay
+// _pick_offset.  Ranges are sorted as one 64-bit key (start << IB | slot):
+// equal starts may come in any order (the hole scan only sees the running
+// max of ends), so the slot just makes keys unique and carries the end.
+template <int K>
+__device__ __forceinline__ int64_t place_reg(const PlaceArgs &a, int64_t rb, int m, int64_t need, int &lvl,
+                                             bool &ok) {
+  const int lane = threadIdx.x & 31;
+  constexpr int IB = K == 1 ? 5 : K == 2 ? 6 : K == 4 ? 7 : 8;
+  uint64_t x[K];
+  int64_t e[K];
+  int lv = 0;
+  bool big = false;
+#pragma unroll
+  for (int r = 0; r < K; r++) {
+    int i = r * 32 + lane;
+    x[r] = ~0ull;
+    e[r] = INT64_MIN;
+    if (i < m) {
+      int32_t j = a.col[rb + i];
+      int64_t s = __ldcg(&a.off[j]);
+      e[r] = s + a.size[j];
+      lv = max(lv, __ldcg(&a.level[j]));
+      big |= (uint64_t)s >> (63 - IB) != 0;
+      x[r] = ((uint64_t)s << IB) | (uint64_t)i;
     }
-    __syncwarp();
+  }
+  ok = !__any_sync(FULL_MASK, big);
+  if (!ok) return 0;
+  lvl = warp_max_i32(lv) + 1;
+  warp_bitonic_keys<K>(x);
+  HoleState h{0, 0, 0, false};
+#pragma unroll
+  for (int r = 0; r < K; r++) {
+    if (r * 32 >= m) break;
+    // end of the range now at sorted position r*32 + lane
+    int src = (int)(x[r] & ((1u << IB) - 1));
+    int64_t es = INT64_MIN;
+#pragma unroll
+    for (int q = 0; q < K; q++) {
+      int64_t t = __shfl_sync(FULL_MASK, e[q], src & 31);
+      if ((src >> 5) == q) es = t;
+    }
+    bool valid = r * 32 + lane < m;
+    int64_t ss = (int64_t)(x[r] >> IB);
+    if (hole_chunk(h, ss, es, valid, need, a.policy)) break;
   }
   return h.found ? h.best_off : h.top;
 }
 
-template <bool GRID>
-__global__ void __launch_bounds__(256) k_place(PlaceArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  IV *sbuf = (IV *)smem_raw;
+template <typename P>
+__device__ int64_t place_mem(const PlaceArgs &a, P buf, int64_t rb, int m, int64_t need, int &lvl) {
   const int lane = threadIdx.x & 31;
-  IV *wbuf = sbuf + (threadIdx.x >> 5) * a.cap;
+  int n2 = 64;
+  while (n2 < m) n2 <<= 1;
+  int lv = 0;
+  for (int i = lane; i < n2; i += 32) {
+    IV x{INT64_MAX, INT64_MAX};
+    if (i < m) {
+      int32_t j = a.col[rb + i];
+      x.s = __ldcg(&a.off[j]);
+      x.e = x.s + a.size[j];
+      lv = max(lv, __ldcg(&a.level[j]));
+    }
+    buf[i] = x;
+  }
+  lvl = warp_max_i32(lv) + 1;
+  __syncwarp();
+  warp_bitonic_mem(buf, n2);
+  HoleState h{0, 0, 0, false};
+  for (int base = 0; base < m; base += 32) {
+    int i = base + lane;
+    IV x = i < m ? buf[i] : IV{0, 0};
+    if (hole_chunk(h, x.s, x.e, i < m, need, a.policy)) break;
+  }
+  __syncwarp();
+  return h.found ? h.best_off : h.top;
+}
+
+constexpr int PLACE_THREADS = 256;
+
+// Asynchronous dataflow placement: warps claim ready variables from a
+// queue in order; placing a variable decrements its successors' counters
+// and the last predecessor to finish publishes the successor.  No grid-wide
+// barrier: a variable starts the moment its last predecessor is placed.
+__global__ void __launch_bounds__(PLACE_THREADS) k_place_async(PlaceArgs a) {
+  const int lane = threadIdx.x & 31;
   int64_t gwarp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  IV *gbuf = a.gscratch ? a.gscratch + gwarp * a.gcap : nullptr;
-  bool leader = blockIdx.x == 0 && threadIdx.x == 0;
-  int r = 0;
+  long long fp = LLONG_MIN;
+  int dmax = 0;
   for (;;) {
-    int n = __ldcg(&a.counts[r % 3]);
-    if (n == 0) break;
-    const int32_t *cur = (r & 1) ? a.F1 : a.F0;
-    int32_t *nxt = (r & 1) ? a.F0 : a.F1;
-    if (leader) a.counts[(r + 2) % 3] = 0;
-    for (int64_t q = gwarp; q < n; q += nwarps) {
-      int32_t v = __ldcg(&cur[q]);
-      int64_t o = place_one(a, v, wbuf, gbuf);
-      if (lane == 0) a.off[v] = o;
-      __threadfence();
-      int64_t rb = a.row_off[v], deg = a.row_off[v + 1] - rb;
-      for (int64_t i = a.pcnt[v] + lane; i < deg; i += 32) {
-        int32_t j = a.col2[rb + i];
-        if (atomicSub(&a.remaining[j], 1) == 1) {
-          int slot = atomicAdd(&a.counts[(r + 1) % 3], 1);
-          nxt[slot] = j;
-        }
+    int i = 0;
+    if (lane == 0) i = atomicAdd(a.head, 1);
+    i = __shfl_sync(FULL_MASK, i, 0);
+    if (i >= a.V) break;
+    int v1 = 0;
+    if (lane == 0) {
+      volatile int32_t *q = a.queue + i;
+      while ((v1 = *q) == 0) __nanosleep(32);
+    }
+    int32_t v = __shfl_sync(FULL_MASK, v1, 0) - 1;
+    __threadfence();
+    int64_t rb = a.row_off[v];
+    int m = a.pcnt[v];
+    int64_t need = a.size[v];
+    int lvl = 1;
+    int64_t o = 0;
+    bool ok = true;
+    if (m == 0) o = 0;
+    else if (m <= 32) o = place_reg<1>(a, rb, m, need, lvl, ok);
+    else if (m <= 64) o = place_reg<2>(a, rb, m, need, lvl, ok);
+    else if (m <= 128) o = place_reg<4>(a, rb, m, need, lvl, ok);
+    else ok = false;
+    // long rows, or offsets too large to pack: sort (start, end) pairs in the
+    // warp's global scratch
+    if (!ok) {
+      IV *buf = a.wscratch + gwarp * 128;
+      if (m > 128) {
+        unsigned long long n2 = 64;
+        while (n2 < (unsigned long long)m) n2 <<= 1;
+        unsigned long long at = 0;
+        if (lane == 0) at = atomicAdd(a.arena_top, n2);
+        buf = a.arena + __shfl_sync(FULL_MASK, at, 0);
+      }
+      o = place_mem(a, buf, rb, m, need, lvl);
+    }
+    if (lane == 0) {
+      a.off[v] = o;
+      a.level[v] = lvl;
+      if (o + need > fp) fp = o + need;
+      if (lvl > dmax) dmax = lvl;
+    }
+    __threadfence();
+    __syncwarp();
+    int64_t deg = a.row_off[v + 1] - rb;
+    for (int64_t k = m + lane; k < deg; k += 32) {
+      int32_t j = a.col[rb + k];
+      if (atomicSub(&a.remaining[j], 1) == 1) {
+        __threadfence();
+        int slot = atomicAdd(a.tail, 1);
+        *(volatile int32_t *)(a.queue + slot) = j + 1;
       }
     }
-    if (GRID) {
-      __threadfence();
-      cg::this_grid().sync();
-    } else {
-      __threadfence_block();
-      __syncthreads();
-    }
-    r++;
   }
-  if (leader) *a.levels = r;
+  if (lane == 0) {
+    atomicMax(a.footprint, fp);
+    atomicMax(a.depth, dmax);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -233,8 +361,16 @@ __global__ void k_size_keys(int64_t V, const int64_t *size, const uint32_t *vals
     lmn = k < lmn ? k : lmn;
     lmx = k > lmx ? k : lmx;
   }
-  atomicMin(mn, lmn);
-  atomicMax(mx, lmx);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    unsigned long long a = __shfl_xor_sync(FULL_MASK, lmn, o), b = __shfl_xor_sync(FULL_MASK, lmx, o);
+    lmn = a < lmn ? a : lmn;
+    lmx = b > lmx ? b : lmx;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(mn, lmn);
+    atomicMax(mx, lmx);
+  }
 }
 
 __global__ void k_sub_keys(int64_t V, uint64_t *keys, const unsigned long long *mn) {
@@ -253,48 +389,51 @@ __global__ void k_rank(int64_t V, const uint32_t *order, int32_t *rank) {
     rank[order[q]] = (int32_t)q;
 }
 
-__global__ void k_partition(int64_t V, const int64_t *row_off, const int32_t *col, const int32_t *rank,
-                            int32_t *col2, int32_t *pcnt, int32_t *remaining, int32_t *F0, int32_t *count0,
-                            int32_t *maxpred) {
-  const int lane = threadIdx.x & 31;
-  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t v = warp; v < V; v += nwarps) {
-    int64_t rb = row_off[v], deg = row_off[v + 1] - rb;
-    int32_t rv = rank[v];
-    int32_t pc = 0, sc = 0;
-    for (int64_t base = 0; base < deg; base += 32) {
-      int64_t idx = base + lane;
-      bool valid = idx < deg;
-      int32_t j = valid ? col[rb + idx] : 0;
-      bool isp = valid && rank[j] < rv;
-      unsigned bp = __ballot_sync(FULL_MASK, isp);
-      unsigned bs = __ballot_sync(FULL_MASK, valid && !isp);
-      if (isp) col2[rb + pc + __popc(bp & lanemask_lt())] = j;
-      else if (valid) col2[rb + deg - 1 - (sc + __popc(bs & lanemask_lt()))] = j;
-      pc += __popc(bp);
-      sc += __popc(bs);
+__global__ void k_ready_init(int64_t V, const int32_t *pcnt, int32_t *remaining, int32_t *queue, int32_t *tail,
+                             unsigned long long *arena_need) {
+  unsigned long long need = 0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
+    int c = pcnt[v];
+    remaining[v] = c;
+    if (c > 128) {
+      unsigned long long n2 = 64;
+      while (n2 < (unsigned long long)c) n2 <<= 1;
+      need += n2;
     }
-    if (lane == 0) {
-      pcnt[v] = pc;
-      remaining[v] = pc;
-      atomicMax(maxpred, pc);
-      if (pc == 0) F0[atomicAdd(count0, 1)] = (int32_t)v;
-    }
+    if (c == 0) queue[atomicAdd(tail, 1)] = (int32_t)(v + 1);
   }
+  need = warp_sum(need);
+  if ((threadIdx.x & 31) == 0 && need) atomicAdd(arena_need, need);
 }
 
-__global__ void k_footprint(int64_t V, const int64_t *off, const int64_t *size, long long *fp) {
-  long long m = LLONG_MIN;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V; i += (int64_t)gridDim.x * blockDim.x) {
-    long long e = off[i] + size[i];
-    if (e > m) m = e;
+// placement rank of every vertex: (-size, tiekey or vertex index)
+int placement_rank(mp_ctx *ctx, int64_t V, const int64_t *size, const int64_t *tiekey, int32_t *rank, mp_err *err) {
+  StageTimer tm(ctx, MP_ST_PLACE_ORDER);
+  cudaStream_t st = ctx->stream;
+  DBuf<uint64_t> keys;
+  DBuf<uint32_t> order;
+  CUDA_TRY(keys.alloc(V, st));
+  CUDA_TRY(order.alloc(V, st));
+  int rc;
+  if (tiekey) {
+    LAUNCH(ctx, k_tie_keys, grid_for(V, 256), 256, 0, V, tiekey, keys.p, order.p);
+    rc = dev_radix_sort_u64(ctx, keys.p, order.p, V, 64, err);
+    if (rc) return rc;
+  } else {
+    LAUNCH(ctx, k_iota, grid_for(V, 256), 256, 0, V, order.p);
   }
-  for (int o = 16; o; o >>= 1) {
-    long long u = __shfl_xor_sync(FULL_MASK, m, o);
-    if (u > m) m = u;
-  }
-  if ((threadIdx.x & 31) == 0) atomicMax(fp, m);
+  unsigned long long *d_mn = (unsigned long long *)ctx->d_small, *d_mx = d_mn + 1;
+  CUDA_TRY(cudaMemsetAsync(d_mn, 0xff, 8, st));
+  CUDA_TRY(cudaMemsetAsync(d_mx, 0, 8, st));
+  LAUNCH(ctx, k_size_keys, grid_for(V, 256, 1024), 256, 0, V, size, order.p, keys.p, d_mn, d_mx);
+  uint64_t mm[2];
+  rc = dev_read_n(ctx, d_mn, mm, 16, err);
+  if (rc) return rc;
+  LAUNCH(ctx, k_sub_keys, grid_for(V, 256), 256, 0, V, keys.p, d_mn);
+  rc = dev_radix_sort_u64(ctx, keys.p, order.p, V, bits_for(mm[1] - mm[0]), err);
+  if (rc) return rc;
+  LAUNCH(ctx, k_rank, grid_for(V, 256), 256, 0, V, order.p, rank);
+  return MP_OK;
 }
 
 extern "C" int mp_plan_pool(mp_ctx *ctx, mp_dgraph *g, int32_t policy, int64_t *offsets, int64_t *footprint,
@@ -310,91 +449,52 @@ extern "C" int mp_plan_pool(mp_ctx *ctx, mp_dgraph *g, int32_t policy, int64_t *
     if (levels) *levels = 0;
     return MP_OK;
   }
-  // placement order: sort by tie key (when given), then stable by -size
-  DBuf<uint64_t> keys;
-  DBuf<uint32_t> order;
-  CUDA_TRY(keys.alloc(V, st));
-  CUDA_TRY(order.alloc(V, st));
-  int rc;
-  if (g->tiekey.p) {
-    LAUNCH(ctx, k_tie_keys, grid_for(V, 256), 256, 0, V, g->tiekey.p, keys.p, order.p);
-    rc = dev_radix_sort_u64(ctx, keys.p, order.p, V, 64, err);
-    if (rc) return rc;
-  } else {
-    LAUNCH(ctx, k_iota, grid_for(V, 256), 256, 0, V, order.p);
-  }
-  unsigned long long *d_mn = (unsigned long long *)ctx->d_small, *d_mx = d_mn + 1;
-  CUDA_TRY(cudaMemsetAsync(d_mn, 0xff, 8, st));
-  CUDA_TRY(cudaMemsetAsync(d_mx, 0, 8, st));
-  LAUNCH(ctx, k_size_keys, grid_for(V, 256, 1024), 256, 0, V, g->size.p, order.p, keys.p, d_mn, d_mx);
-  uint64_t mm[2];
-  rc = dev_read_n(ctx, d_mn, mm, 16, err);
-  if (rc) return rc;
-  LAUNCH(ctx, k_sub_keys, grid_for(V, 256), 256, 0, V, keys.p, d_mn);
-  rc = dev_radix_sort_u64(ctx, keys.p, order.p, V, bits_for(mm[1] - mm[0]), err);
-  if (rc) return rc;
-  DBuf<int32_t> rank, col2, pcnt, remaining, F0, F1, counts;
-  CUDA_TRY(rank.alloc(V, st)); CUDA_TRY(col2.alloc(g->nnz, st)); CUDA_TRY(pcnt.alloc(V, st));
-  CUDA_TRY(remaining.alloc(V, st)); CUDA_TRY(F0.alloc(V, st)); CUDA_TRY(F1.alloc(V, st));
-  CUDA_TRY(counts.alloc(8, st));
-  CUDA_TRY(cudaMemsetAsync(counts.p, 0, 32, st));
-  LAUNCH(ctx, k_rank, grid_for(V, 256), 256, 0, V, order.p, rank.p);
-  int32_t *d_maxpred = counts.p + 4;
-  LAUNCH(ctx, k_partition, grid_for(V * 32, 256, 148 * 64), 256, 0, V, g->row_off.p, g->col.p, rank.p, col2.p,
-         pcnt.p, remaining.p, F0.p, counts.p, d_maxpred);
-  int32_t maxpred;
-  rc = dev_read_n(ctx, d_maxpred, &maxpred, 4, err);
-  if (rc) return rc;
-  DBuf<int64_t> off;
-  CUDA_TRY(off.alloc(V, st));
-  const int cap = 256;
-  const int threads = 256;
-  size_t smem = (size_t)(threads / 32) * cap * sizeof(IV);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_place<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_place<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
-  bool grid_mode = V > 4096;
-  int nblocks = 1;
-  if (grid_mode) {
-    int per_sm = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_place<true>, threads, smem));
-    if (per_sm < 1) per_sm = 1;
-    nblocks = per_sm * ctx->num_sms;
-  }
-  DBuf<IV> gscratch;
-  int64_t gcap = 0;
-  if (maxpred > cap) {
-    gcap = 64;
-    while (gcap < maxpred) gcap <<= 1;
-    CUDA_TRY(gscratch.alloc(gcap * (int64_t)nblocks * (threads / 32), st));
-  }
-  PlaceArgs a{V, g->row_off.p, col2.p, pcnt.p, g->size.p, off.p, remaining.p, F0.p, F1.p, counts.p, policy,
-              cap, gscratch.p, gcap, counts.p + 5};
-  ctx->launches++;
-  if (grid_mode) {
-    void *args[] = {&a};
-    CUDA_TRY(cudaLaunchCooperativeKernel((void *)k_place<true>, dim3(nblocks), dim3(threads), args, smem, st));
-  } else {
-    k_place<false><<<1, threads, smem, st>>>(a);
-    CUDA_TRY(cudaGetLastError());
-  }
-  long long *d_fp = (long long *)ctx->d_small;
+  DBuf<int32_t> remaining, queue, level, ctr;
+  StageTimer *tm = new StageTimer(ctx, MP_ST_PLACE_SPLIT);
+  CUDA_TRY(remaining.alloc(V, st)); CUDA_TRY(queue.alloc(V, st)); CUDA_TRY(level.alloc(V, st));
+  CUDA_TRY(ctr.alloc(16, st));
+  CUDA_TRY(cudaMemsetAsync(queue.p, 0, V * 4, st));
+  CUDA_TRY(cudaMemsetAsync(ctr.p, 0, 64, st));
+  // ctr: [0] head [1] tail [2] - [3] depth [4..5] footprint [6..7] arena need [8..9] arena top
+  long long *d_fp = (long long *)(ctr.p + 4);
+  unsigned long long *d_need = (unsigned long long *)(ctr.p + 6);
   const long long lmin = LLONG_MIN;
   CUDA_TRY(cudaMemcpyAsync(d_fp, &lmin, 8, cudaMemcpyHostToDevice, st));
-  LAUNCH(ctx, k_footprint, grid_for(V, 256, 1024), 256, 0, V, off.p, g->size.p, d_fp);
-  CUDA_TRY(cudaMemcpyAsync(offsets, off.p, V * 8, cudaMemcpyDeviceToHost, st));
-  int64_t fp;
-  rc = dev_read_i64(ctx, (const int64_t *)d_fp, &fp, err);
+  LAUNCH(ctx, k_ready_init, grid_for(V, 256, 2048), 256, 0, V, g->pcnt.p, remaining.p, queue.p, ctr.p + 1,
+         d_need);
+  uint64_t arena_need;
+  int rc = dev_read_n(ctx, d_need, &arena_need, 8, err);
   if (rc) return rc;
-  *footprint = fp;
-  if (levels) {
-    int32_t lv;
-    rc = dev_read_n(ctx, counts.p + 5, &lv, 4, err);
-    if (rc) return rc;
-    *levels = lv;
+  delete tm;
+  DBuf<int64_t> &off = g->offsets;
+  CUDA_TRY(off.alloc(V, st));
+  size_t smem = 0;
+  int per_sm = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_place_async, PLACE_THREADS, smem));
+  if (per_sm < 1) per_sm = 1;
+  // all warps resident: spinning consumers must never starve producers
+  int64_t warps_needed = V;
+  int64_t nblocks = (int64_t)per_sm * ctx->num_sms;
+  int64_t need_blocks = (warps_needed * 32 + PLACE_THREADS - 1) / PLACE_THREADS;
+  if (need_blocks < nblocks) nblocks = need_blocks;
+  // scratch for rows the register sorts do not take: 128 ranges per warp,
+  // plus a bump arena sized for every row longer than 128
+  DBuf<IV> wscratch, arena;
+  CUDA_TRY(wscratch.alloc(128 * nblocks * (PLACE_THREADS / 32), st));
+  CUDA_TRY(arena.alloc((int64_t)arena_need, st));
+  PlaceArgs a{V, g->row_off.p, g->col.p, g->pcnt.p, g->size.p, off.p, level.p, remaining.p, queue.p,
+              ctr.p, ctr.p + 1, policy, wscratch.p, arena.p, (unsigned long long *)(ctr.p + 8), d_fp, ctr.p + 3};
+  {
+    StageTimer ptm(ctx, MP_ST_PLACE);
+    LAUNCH(ctx, k_place_async, (unsigned)nblocks, PLACE_THREADS, smem, a);
   }
+  if (offsets) CUDA_TRY(cudaMemcpyAsync(offsets, off.p, V * 8, cudaMemcpyDeviceToHost, st));
+  int32_t tail4[6];
+  rc = dev_read_n(ctx, ctr.p, tail4, 24, err);
+  if (rc) return rc;
+  *footprint = *(int64_t *)(tail4 + 4);
+  if (levels) *levels = tail4[3];
   return MP_OK;
 }
+
+extern "C" const int64_t *mp_graph_offsets_device(mp_dgraph *g) { return g->offsets.p; }
