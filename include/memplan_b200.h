@@ -208,6 +208,83 @@ const int64_t *mp_graph_offsets_device(mp_dgraph *g);
 int mp_plan_pool(mp_ctx *ctx, mp_dgraph *g, int32_t policy, int64_t *offsets,
                  int64_t *footprint, int64_t *levels, mp_err *err);
 
+/* upload a host CSR (e.g. a ConflictGraph built in Python); rows are
+ * partitioned on the device by the placement order (-size, tiekey) */
+int mp_graph_from_csr(mp_ctx *ctx, int32_t nvars, const int64_t *row_off, const int32_t *col,
+                      const int64_t *size, const int64_t *tiekey, mp_dgraph **out, mp_err *err);
+/* compute_load_profile (iteration.py:304-320) for an uploaded profile */
+int mp_profile_compute_loads(mp_ctx *ctx, mp_dprofile *p, int64_t *loads, int64_t *peak, int64_t *peak_index,
+                             mp_err *err);
+
+/* ---------------------------------------------------------------------- */
+/* AutoSwap planning (autoswap.py, swapsim.py)                              */
+
+/* Swap candidates in columnar form (SwapCandidate, autoswap.py:34-50).
+ * name_rank orders the candidates' var names (ties in every sort). */
+typedef struct mp_cands_io {
+  int64_t k;
+  int32_t *var; /* profile variable index (output of mp_swap_candidates) */
+  int64_t *size;
+  int32_t *out_index;
+  double *out_t;
+  double *out_ready;
+  int32_t *in_index;
+  double *in_t;
+  double *dout;
+  double *din;
+  uint8_t *spans;
+  int32_t *name_rank;
+} mp_cands_io;
+
+/* filter_candidates (autoswap.py:80-116); arrays sized nvars */
+int mp_swap_candidates(mp_ctx *ctx, mp_dprofile *p, int64_t threshold, double bw, double lat,
+                       mp_cands_io *out, mp_err *err);
+/* score_doa / score_aoa / score_wdoa and the unbudgeted SWDOA greedy
+ * (autoswap.py:132-215): order[k], swdoa[k], and peaks[k+1] = max of the
+ * planned load after j picks (a budgeted run is the prefix up to the first
+ * peak <= limit). */
+int mp_swap_scores(mp_ctx *ctx, mp_dprofile *p, const mp_cands_io *c, double *doa, double *aoa, double *wdoa,
+                   double *swdoa, int32_t *order, double *peaks, mp_err *err);
+/* gap_area (autoswap.py:164-174) of every candidate over `loads` (p
+ * doubles; NULL = the profile's loads) */
+int mp_swap_gap_area(mp_ctx *ctx, mp_dprofile *p, const mp_cands_io *c, const double *loads, double *area,
+                     mp_err *err);
+/* static-score selection (autoswap.py:305-317): order by (-ranked, -size,
+ * name) and insert until the planned peak fits; MP_E_LIMIT_UNREACHABLE
+ * with aux0 = limit, aux1 = int(peak) otherwise */
+int mp_swap_select_static(mp_ctx *ctx, mp_dprofile *p, const mp_cands_io *c, const double *ranked,
+                          int64_t limit, int32_t *sel, int64_t *nsel, mp_err *err);
+/* max of the load with the given candidates absent (compute_load_min /
+ * planned_peak, swapsim.py:398-405, autoswap.py:320-326); subset NULL = all */
+int mp_swap_planned_peak(mp_ctx *ctx, mp_dprofile *p, const mp_cands_io *c, const int32_t *subset,
+                         int64_t nsub, double *peak, mp_err *err);
+/* _make_schedule (swapsim.py:62-108) for the selection `sel` */
+int mp_swap_schedule(mp_ctx *ctx, const mp_cands_io *c, const int32_t *sel, int64_t n, const double *ready,
+                     const double *deadline, double *t_so, double *t_eo, double *t_si, double *t_ei,
+                     int32_t *event_order, mp_err *err);
+
+typedef struct mp_sim_io {
+  /* in: initial schedule (selection order); out: final schedule */
+  double *t_so, *t_eo, *t_si, *t_ei;
+  int32_t *event_order;
+  /* out: LOAD' and LOAD'' curves (capacity 1 + period + 2n each) */
+  double *lp_t; int64_t *lp_v; int64_t n_lp; int64_t lp_peak; double lp_peak_t;
+  double *ldp_t; int64_t *ldp_v; int64_t n_ldp; int64_t ldp_peak; double ldp_peak_t;
+  /* out: delayed ops (capacity period) */
+  int64_t *delayed_index; double *delayed_us; int64_t n_delayed;
+  double delay; int64_t rounds;
+} mp_sim_io;
+
+/* simulate (swapsim.py:349-395): LOAD' overlay + LOAD'' replay with the
+ * fixed-point deadline refinement.  MP_E_SWAP_DEADLOCK (aux0 1: swap-in of
+ * candidate aux1 cannot start) / MP_E_SIM_INDEXERROR mirror the reference. */
+int mp_swap_simulate(mp_ctx *ctx, mp_dprofile *p, const mp_cands_io *c, const int32_t *sel, int64_t n,
+                     int64_t limit, int32_t has_limit, int32_t max_rounds, mp_sim_io *io, mp_err *err);
+
+/* CPython-3.12 compatible standardize (autoswap.py:228-238): Neumaier
+ * sum() and libm pow — host code, since device pow differs from glibc's */
+int mp_standardize(const double *x, int64_t n, double *out);
+
 #ifdef __cplusplus
 }
 #endif

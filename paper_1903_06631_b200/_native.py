@@ -235,6 +235,165 @@ def plan_pool_device(g: DGraph, policy: int):
     return int(fp.value), int(lv.value)
 
 
+def graph_from_csr(row_off, col, size, tiekey) -> DGraph:
+    row_off = np.ascontiguousarray(row_off, np.int64)
+    col = np.ascontiguousarray(col if len(col) else np.zeros(1, np.int32), np.int32)
+    size = np.ascontiguousarray(size, np.int64)
+    tiekey = np.ascontiguousarray(tiekey, np.int64)
+    h = C.c_void_p()
+    err = MpErr()
+    rc = lib().mp_graph_from_csr(ctx(), C.c_int32(size.shape[0]), ptr(row_off), ptr(col), ptr(size), ptr(tiekey),
+                                 C.byref(h), C.byref(err))
+    raise_for(rc, err)
+    return DGraph(h)
+
+
+def profile_loads(dp: DProfile, period: int):
+    loads = np.zeros(max(period, 1), np.int64)
+    pk, pi = C.c_int64(), C.c_int64()
+    err = MpErr()
+    rc = lib().mp_profile_compute_loads(ctx(), dp.h, ptr(loads), C.byref(pk), C.byref(pi), C.byref(err))
+    raise_for(rc, err)
+    return loads[:period], int(pk.value), int(pi.value)
+
+
+# ---------------------------------------------------------------------------
+# swap planning
+
+
+class MpCandsIO(C.Structure):
+    _fields_ = [("k", C.c_int64)] + [(n, C.c_void_p) for n in (
+        "var", "size", "out_index", "out_t", "out_ready", "in_index", "in_t", "dout", "din", "spans",
+        "name_rank")]
+
+
+CAND_COLS = (("var", np.int32), ("size", np.int64), ("out_index", np.int32), ("out_t", np.float64),
+             ("out_ready", np.float64), ("in_index", np.int32), ("in_t", np.float64), ("dout", np.float64),
+             ("din", np.float64), ("spans", np.uint8), ("name_rank", np.int32))
+
+
+class Cands:
+    """Columnar candidates handed to the swap kernels."""
+
+    def __init__(self, k: int, **cols):
+        self.k = k
+        for name, dt in CAND_COLS:
+            setattr(self, name, np.ascontiguousarray(cols.get(name, np.zeros(max(k, 1), dt)), dtype=dt))
+
+    def io(self) -> MpCandsIO:
+        return MpCandsIO(self.k, *[ptr(getattr(self, n)) for n, _ in CAND_COLS])
+
+
+class MpSimIO(C.Structure):
+    _fields_ = [("t_so", C.c_void_p), ("t_eo", C.c_void_p), ("t_si", C.c_void_p), ("t_ei", C.c_void_p),
+                ("event_order", C.c_void_p),
+                ("lp_t", C.c_void_p), ("lp_v", C.c_void_p), ("n_lp", C.c_int64), ("lp_peak", C.c_int64),
+                ("lp_peak_t", C.c_double),
+                ("ldp_t", C.c_void_p), ("ldp_v", C.c_void_p), ("n_ldp", C.c_int64), ("ldp_peak", C.c_int64),
+                ("ldp_peak_t", C.c_double),
+                ("delayed_index", C.c_void_p), ("delayed_us", C.c_void_p), ("n_delayed", C.c_int64),
+                ("delay", C.c_double), ("rounds", C.c_int64)]
+
+
+def swap_candidates(dp: DProfile, nvars: int, threshold: int, bw: float, lat: float) -> Cands:
+    c = Cands(nvars)
+    io = c.io()
+    err = MpErr()
+    rc = lib().mp_swap_candidates(ctx(), dp.h, C.c_int64(threshold), C.c_double(bw), C.c_double(lat),
+                                  C.byref(io), C.byref(err))
+    raise_for(rc, err)
+    c.k = int(io.k)
+    for name, _ in CAND_COLS:
+        setattr(c, name, getattr(c, name)[:c.k])
+    return c
+
+
+def swap_scores(dp: DProfile, c: Cands):
+    k = c.k
+    outs = [np.zeros(max(k, 1)) for _ in range(4)]
+    order = np.zeros(max(k, 1), np.int32)
+    peaks = np.zeros(k + 1)
+    err = MpErr()
+    rc = lib().mp_swap_scores(ctx(), dp.h, C.byref(c.io()), *[ptr(a) for a in outs], ptr(order), ptr(peaks),
+                              C.byref(err))
+    raise_for(rc, err)
+    return [a[:k] for a in outs], order[:k], peaks
+
+
+def swap_gap_area(dp: DProfile, c: Cands, loads=None) -> np.ndarray:
+    out = np.zeros(max(c.k, 1))
+    cur = None if loads is None else np.ascontiguousarray(loads, np.float64)
+    err = MpErr()
+    rc = lib().mp_swap_gap_area(ctx(), dp.h, C.byref(c.io()), ptr(cur), ptr(out), C.byref(err))
+    raise_for(rc, err)
+    return out[:c.k]
+
+
+def swap_select_static(dp: DProfile, c: Cands, ranked, limit: int):
+    sel = np.zeros(max(c.k, 1), np.int32)
+    n = C.c_int64()
+    rk = np.ascontiguousarray(ranked if len(ranked) else np.zeros(1), np.float64)
+    err = MpErr()
+    rc = lib().mp_swap_select_static(ctx(), dp.h, C.byref(c.io()), ptr(rk), C.c_int64(limit), ptr(sel),
+                                     C.byref(n), C.byref(err))
+    raise_for(rc, err)
+    return sel[:n.value]
+
+
+def swap_planned_peak(dp: DProfile, c: Cands, subset=None) -> float:
+    pk = C.c_double()
+    sub = None if subset is None else np.ascontiguousarray(subset if len(subset) else np.zeros(1), np.int32)
+    nsub = 0 if subset is None else len(subset)
+    err = MpErr()
+    rc = lib().mp_swap_planned_peak(ctx(), dp.h, C.byref(c.io()), ptr(sub), C.c_int64(nsub), C.byref(pk),
+                                    C.byref(err))
+    raise_for(rc, err)
+    return float(pk.value)
+
+
+def swap_schedule(c: Cands, sel, ready, deadline):
+    sel = np.ascontiguousarray(sel, np.int32)
+    n = sel.shape[0]
+    t = [np.zeros(max(n, 1)) for _ in range(4)]
+    eo = np.zeros(max(n, 1), np.int32)
+    rd = np.ascontiguousarray(ready if n else np.zeros(1), np.float64)
+    dl = np.ascontiguousarray(deadline if n else np.zeros(1), np.float64)
+    err = MpErr()
+    rc = lib().mp_swap_schedule(ctx(), C.byref(c.io()), ptr(sel if n else np.zeros(1, np.int32)), C.c_int64(n),
+                                ptr(rd), ptr(dl), *[ptr(a) for a in t], ptr(eo), C.byref(err))
+    raise_for(rc, err)
+    return [a[:n] for a in t], eo[:n]
+
+
+def swap_simulate(dp: DProfile, period: int, c: Cands, sel, sched, limit, max_rounds=100, cand_names=None):
+    sel = np.ascontiguousarray(sel, np.int32)
+    n = sel.shape[0]
+    t = [np.array(a, np.float64) if n else np.zeros(1) for a in sched[0]]
+    eo = np.array(sched[1], np.int32) if n else np.zeros(1, np.int32)
+    cap = 1 + period + 2 * n + 2
+    b = dict(lp_t=np.zeros(cap), lp_v=np.zeros(cap, np.int64), ldp_t=np.zeros(cap),
+             ldp_v=np.zeros(cap, np.int64), di=np.zeros(period + 1, np.int64), du=np.zeros(period + 1))
+    io = MpSimIO(ptr(t[0]), ptr(t[1]), ptr(t[2]), ptr(t[3]), ptr(eo), ptr(b["lp_t"]), ptr(b["lp_v"]), 0, 0, 0.0,
+                 ptr(b["ldp_t"]), ptr(b["ldp_v"]), 0, 0, 0.0, ptr(b["di"]), ptr(b["du"]), 0, 0.0, 0)
+    err = MpErr()
+    rc = lib().mp_swap_simulate(ctx(), dp.h, C.byref(c.io()), ptr(sel if n else np.zeros(1, np.int32)),
+                                C.c_int64(n), C.c_int64(0 if limit is None else limit),
+                                C.c_int32(limit is not None), C.c_int32(max_rounds), C.byref(io), C.byref(err))
+    raise_for(rc, err, cand_names=cand_names)
+    return dict(t_so=t[0][:n], t_eo=t[1][:n], t_si=t[2][:n], t_ei=t[3][:n], event_order=eo[:n],
+                lp=(b["lp_t"][:io.n_lp], b["lp_v"][:io.n_lp], int(io.lp_peak), float(io.lp_peak_t)),
+                ldp=(b["ldp_t"][:io.n_ldp], b["ldp_v"][:io.n_ldp], int(io.ldp_peak), float(io.ldp_peak_t)),
+                delayed=(b["di"][:io.n_delayed], b["du"][:io.n_delayed]), delay=float(io.delay),
+                rounds=int(io.rounds))
+
+
+def standardize(x) -> np.ndarray:
+    x = np.ascontiguousarray(x, np.float64)
+    out = np.zeros(max(x.shape[0], 1))
+    lib().mp_standardize(ptr(x if x.shape[0] else np.zeros(1)), C.c_int64(x.shape[0]), ptr(out))
+    return out[:x.shape[0]]
+
+
 STAGES = ("group_sort", "validate", "detect", "extract", "loads", "conflict_prep", "conflict_fill",
           "place_order", "place_split", "place", "footprint", "swap")
 

@@ -1,4 +1,6 @@
 // capi.cu — context and handle management of the C ABI (include/memplan_b200.h).
+#include <math.h>
+
 #include "handles.cuh"
 
 int profile_loads(mp_ctx *ctx, mp_dprofile *P, mp_err *err);
@@ -181,5 +183,61 @@ extern "C" int mp_profile_upload(mp_ctx *ctx, const mp_profile_dims *dims, const
 #undef UL
   CUDA_TRY(cudaStreamSynchronize(st));
   *out = P;
+  return MP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// host-side helpers
+
+// CPython's float pow goes to libm; the compiler must not turn pow(x, 2.0)
+// into x*x (glibc pow is not always correctly rounded)
+static double (*volatile libm_pow)(double, double) = pow;
+
+// builtin sum() over floats in CPython 3.12: Neumaier compensation
+static double py_fsum(const double *x, int64_t n) {
+  if (n == 0) return 0.0;
+  double f = 0.0 + x[0], c = 0.0;
+  for (int64_t i = 1; i < n; i++) {
+    double t = f + x[i];
+    if (fabs(f) >= fabs(x[i])) c += (f - t) + x[i];
+    else c += (x[i] - t) + f;
+    f = t;
+  }
+  if (c != 0.0 && isfinite(c)) f += c;
+  return f;
+}
+
+// standardize, autoswap.py:228-238 (float_pow special cases as CPython)
+extern "C" int mp_standardize(const double *x, int64_t n, double *out) {
+  if (n == 0) return MP_OK;
+  double mean = py_fsum(x, n) / (double)n;
+  std::vector<double> sq((size_t)n);
+  for (int64_t i = 0; i < n; i++) {
+    double dv = x[i] - mean;
+    if (dv == 0.0) sq[i] = 0.0;
+    else if (dv != dv) sq[i] = dv;
+    else {
+      double a = fabs(dv);
+      sq[i] = a == 1.0 ? 1.0 : libm_pow(a, 2.0);
+    }
+  }
+  double var = py_fsum(sq.data(), n) / (double)n;
+  if (var <= 0) {
+    for (int64_t i = 0; i < n; i++) out[i] = 0.0;
+    return MP_OK;
+  }
+  double sd = var == 1.0 ? 1.0 : libm_pow(var, 0.5);
+  for (int64_t i = 0; i < n; i++) out[i] = (x[i] - mean) / sd;
+  return MP_OK;
+}
+
+extern "C" int mp_profile_compute_loads(mp_ctx *ctx, mp_dprofile *P, int64_t *loads, int64_t *peak,
+                                        int64_t *peak_index, mp_err *err) {
+  int rc = profile_loads(ctx, P, err);
+  if (rc) return rc;
+  if (P->d.period) CUDA_TRY(cudaMemcpyAsync(loads, P->loads.p, P->d.period * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  *peak = P->d.peak_bytes;
+  *peak_index = P->d.peak_index;
   return MP_OK;
 }

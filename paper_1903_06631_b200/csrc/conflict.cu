@@ -277,3 +277,60 @@ extern "C" int mp_graph_free(mp_dgraph *g) {
   delete g;
   return MP_OK;
 }
+
+// rows of a host CSR split by placement order (warp per row)
+__global__ void k_partition_rows(int64_t V, const int64_t *row_off, const int32_t *col_in, const int32_t *rank,
+                                 int32_t *col, int32_t *pcnt) {
+  const int lane = threadIdx.x & 31;
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const unsigned lt = lanemask_lt();
+  for (int64_t v = warp; v < V; v += nwarps) {
+    int64_t rb = row_off[v], deg = row_off[v + 1] - rb;
+    int32_t rv = rank[v];
+    int32_t pc = 0, sc = 0;
+    for (int64_t base = 0; base < deg; base += 32) {
+      int64_t idx = base + lane;
+      bool valid = idx < deg;
+      int32_t j = valid ? col_in[rb + idx] : 0;
+      bool isp = valid && rank[j] < rv;
+      unsigned bp = __ballot_sync(FULL_MASK, isp);
+      unsigned bs = __ballot_sync(FULL_MASK, valid && !isp);
+      if (isp) col[rb + pc + __popc(bp & lt)] = j;
+      else if (valid) col[rb + deg - 1 - (sc + __popc(bs & lt))] = j;
+      pc += __popc(bp);
+      sc += __popc(bs);
+    }
+    if (lane == 0) pcnt[v] = pc;
+  }
+}
+
+extern "C" int mp_graph_from_csr(mp_ctx *ctx, int32_t nvars, const int64_t *row_off, const int32_t *col,
+                                 const int64_t *size, const int64_t *tiekey, mp_dgraph **out, mp_err *err) {
+  cudaStream_t st = ctx->stream;
+  int64_t nv = nvars, nnz = row_off[nvars];
+  mp_dgraph *g = new mp_dgraph();
+  g->ctx = ctx;
+  g->nvars = nv;
+  g->nnz = nnz;
+  CUDA_TRY(g->size.alloc(nv, st)); CUDA_TRY(g->row_off.alloc(nv + 1, st)); CUDA_TRY(g->col.alloc(nnz, st));
+  CUDA_TRY(g->rank.alloc(nv, st)); CUDA_TRY(g->pcnt.alloc(nv, st));
+  DBuf<int32_t> cin;
+  CUDA_TRY(cin.alloc(nnz, st));
+  CUDA_TRY(cudaMemcpyAsync(g->row_off.p, row_off, (nv + 1) * 8, cudaMemcpyHostToDevice, st));
+  if (nnz) CUDA_TRY(cudaMemcpyAsync(cin.p, col, nnz * 4, cudaMemcpyHostToDevice, st));
+  if (nv) {
+    CUDA_TRY(cudaMemcpyAsync(g->size.p, size, nv * 8, cudaMemcpyHostToDevice, st));
+    if (tiekey) {
+      CUDA_TRY(g->tiekey.alloc(nv, st));
+      CUDA_TRY(cudaMemcpyAsync(g->tiekey.p, tiekey, nv * 8, cudaMemcpyHostToDevice, st));
+    }
+    int rc = placement_rank(ctx, nv, g->size.p, g->tiekey.p, g->rank.p, err);
+    if (rc) { delete g; return rc; }
+    LAUNCH(ctx, k_partition_rows, grid_for(nv * 32, 256, 148 * 64), 256, 0, nv, g->row_off.p, cin.p, g->rank.p,
+           g->col.p, g->pcnt.p);
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));
+  *out = g;
+  return MP_OK;
+}
