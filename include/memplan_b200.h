@@ -176,6 +176,10 @@ int mp_detect(mp_ctx *ctx, mp_dtrace *t, int64_t *period, mp_err *err);
  * compute_load_profile (iteration.py:135-272, 304-320). */
 int mp_extract(mp_ctx *ctx, mp_dtrace *t, int64_t start, int64_t end,
                mp_dprofile **out, mp_err *err);
+/* extract with caller-given op times / duration (build_profile as used by
+ * combine_with_pool, swapsim.py:491) */
+int mp_extract_times(mp_ctx *ctx, mp_dtrace *t, int64_t start, int64_t end, const double *op_times,
+                     double duration, mp_dprofile **out, mp_err *err);
 int mp_profile_get_dims(mp_dprofile *p, mp_profile_dims *dims);
 int mp_profile_download(mp_ctx *ctx, mp_dprofile *p, mp_profile_out *out, mp_err *err);
 int mp_profile_free(mp_dprofile *p);

@@ -154,6 +154,17 @@ def extract(arrays, start: int, end: int) -> DProfile:
     return DProfile(h)
 
 
+def extract_times(arrays, start: int, end: int, op_times: np.ndarray, duration: float) -> DProfile:
+    t = device_trace(arrays)
+    h = C.c_void_p()
+    err = MpErr()
+    op_times = np.ascontiguousarray(op_times, np.float64)
+    rc = lib().mp_extract_times(ctx(), t.h, C.c_int64(start), C.c_int64(end), ptr(op_times),
+                                C.c_double(duration), C.byref(h), C.byref(err))
+    raise_for(rc, err, arrays.names)
+    return DProfile(h)
+
+
 def download_profile(dp: DProfile, names, name_blob, name_off, window) -> FlatProfile:
     dims = dp.dims()
     arrays, out = FlatProfile.alloc_arrays(dims)

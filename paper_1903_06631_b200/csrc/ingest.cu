@@ -733,3 +733,17 @@ extern "C" int mp_extract(mp_ctx *ctx, mp_dtrace *t, int64_t start, int64_t end,
   *out = P;
   return MP_OK;
 }
+
+// build_profile with explicit op times (iteration.py:135-272 called from
+// combine_with_pool, swapsim.py:491): the window's lifetimes come from the
+// trace, its op times and period duration from the caller
+extern "C" int mp_extract_times(mp_ctx *ctx, mp_dtrace *t, int64_t start, int64_t end, const double *op_times,
+                                double duration, mp_dprofile **out, mp_err *err) {
+  int rc = mp_extract(ctx, t, start, end, out, err);
+  if (rc) return rc;
+  mp_dprofile *P = *out;
+  CUDA_TRY(cudaMemcpyAsync(P->op_times.p, op_times, (end - start) * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  P->d.duration_us = duration;
+  return MP_OK;
+}

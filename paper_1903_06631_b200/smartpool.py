@@ -1,0 +1,316 @@
+"""SmartPool: conflict graph and static pool layout (drop-in for memplan.smartpool).
+
+Reference: pkg/src/memplan/smartpool.py:19-254.  The conflict graph is
+built on the device as a CSR (csrc/conflict.cu) and planned there
+(csrc/placement.cu); ``ConflictGraph.vars`` / ``.adj`` and
+``PoolPlan.offsets`` / ``.sizes`` materialize the reference's Python
+containers only when read.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .errors import GraphTooLarge, MemplanError, MissingVariable
+from .iteration import IterationProfile, Segment, device_profile
+
+POLICY_CODE = {"first_fit": 0, "best_fit": 1}
+
+
+@dataclass
+class PoolVar:
+    var: str
+    size: int
+    alloc_index: int
+    segments: tuple[Segment, ...]
+    persistent: bool
+
+
+class ConflictGraph:
+    """Weighted interval-conflict graph (smartpool.py:28-33)."""
+
+    def __init__(self, period: int, vars: list[PoolVar] | None = None, adj: list[set[int]] | None = None,
+                 peak_load_bytes: int = 0):
+        self.period = period
+        self.peak_load_bytes = peak_load_bytes
+        self._vars = vars
+        self._adj = adj
+        self._dev = None
+        self._vars_fn = None  # builds PoolVar list on demand
+        self._nv = len(vars) if vars is not None else 0
+
+    @property
+    def vars(self) -> list[PoolVar]:
+        if self._vars is None and self._vars_fn is not None:
+            self._vars = self._vars_fn()
+        return self._vars
+
+    @vars.setter
+    def vars(self, value):
+        self._vars = value
+        self._dev = None
+
+    @property
+    def adj(self) -> list[set[int]]:
+        if self._adj is None and self._dev is not None:
+            row, col = N.graph_csr(self._dev)
+            c = col.tolist()
+            r = row.tolist()
+            self._adj = [set(c[r[i]:r[i + 1]]) for i in range(len(r) - 1)]
+        return self._adj
+
+    @adj.setter
+    def adj(self, value):
+        self._adj = value
+        self._dev = None
+
+    @property
+    def nvars(self) -> int:
+        return len(self._vars) if self._vars is not None else self._nv
+
+    def __repr__(self):
+        return f"ConflictGraph(period={self.period}, nvars={self.nvars}, peak={self.peak_load_bytes})"
+
+
+class PoolPlan:
+    """Offsets per variable plus the pool footprint (smartpool.py:36-48)."""
+
+    def __init__(self, policy: str, offsets: dict[str, int] | None = None, sizes: dict[str, int] | None = None,
+                 footprint_bytes: int = 0, peak_load_bytes: int = 0):
+        self.policy = policy
+        self.footprint_bytes = footprint_bytes
+        self.peak_load_bytes = peak_load_bytes
+        self._offsets = offsets
+        self._sizes = sizes
+        self._cols = None  # (names, offsets array, sizes array)
+
+    def _build(self):
+        names, off, size = self._cols
+        if self._offsets is None:
+            self._offsets = dict(zip(names, off.tolist()))
+        if self._sizes is None:
+            self._sizes = dict(zip(names, size.tolist()))
+
+    @property
+    def offsets(self) -> dict[str, int]:
+        if self._offsets is None:
+            self._build()
+        return self._offsets
+
+    @offsets.setter
+    def offsets(self, value):
+        self._offsets = value
+
+    @property
+    def sizes(self) -> dict[str, int]:
+        if self._sizes is None:
+            self._build()
+        return self._sizes
+
+    @sizes.setter
+    def sizes(self, value):
+        self._sizes = value
+
+    @property
+    def offset_array(self) -> np.ndarray:
+        """Offsets in graph vertex order (no dict materialization)."""
+        if self._cols is not None:
+            return self._cols[1]
+        return np.array(list(self.offsets.values()), np.int64)
+
+    @property
+    def competitive_ratio(self) -> float:
+        if self.peak_load_bytes <= 0:
+            return 1.0
+        return self.footprint_bytes / self.peak_load_bytes
+
+    def __eq__(self, other):
+        if not isinstance(other, PoolPlan):
+            return NotImplemented
+        return (self.policy, self.offsets, self.sizes, self.footprint_bytes, self.peak_load_bytes) == \
+            (other.policy, other.offsets, other.sizes, other.footprint_bytes, other.peak_load_bytes)
+
+    def __repr__(self):
+        return (f"PoolPlan(policy={self.policy!r}, footprint_bytes={self.footprint_bytes}, "
+                f"peak_load_bytes={self.peak_load_bytes})")
+
+
+def _tie_ranks(allocs, names) -> np.ndarray:
+    """Rank of (alloc_index, var) per vertex: the placement tie-break after
+    -size (smartpool.py:94-98)."""
+    order = sorted(range(len(names)), key=lambda i: (allocs[i], names[i]))
+    tie = np.zeros(len(names), np.int64)
+    tie[order] = np.arange(len(names), dtype=np.int64)
+    return tie
+
+
+def conflict_graph_from_arcs(period: int, arcs, peak_load_bytes: int) -> ConflictGraph:
+    """Conflict graph of (var, size, alloc_index, segments, persistent) arcs
+    (smartpool.py:51-79); half-open arcs that only touch do not conflict."""
+    pool_vars = [PoolVar(*a) for a in arcs]
+    n = len(pool_vars)
+    seg_off = np.zeros(n + 1, np.int64)
+    seg_off[1:] = np.cumsum([len(pv.segments) for pv in pool_vars]) if n else []
+    lo = np.array([s[0] for pv in pool_vars for s in pv.segments] or [0], np.int32)
+    hi = np.array([s[1] for pv in pool_vars for s in pv.segments] or [0], np.int32)
+    tie = _tie_ranks([pv.alloc_index for pv in pool_vars], [pv.var for pv in pool_vars])
+    g = ConflictGraph(period=period, vars=pool_vars, adj=None, peak_load_bytes=peak_load_bytes)
+    g._dev = N.conflict_from_arcs([pv.size for pv in pool_vars] or [0], tie if n else np.zeros(1, np.int64),
+                                  seg_off, lo, hi)
+    g._nv = n
+    g._names = [pv.var for pv in pool_vars]
+    g._sizes = np.array([pv.size for pv in pool_vars], np.int64)
+    return g
+
+
+def build_conflict_graph(profile: IterationProfile) -> ConflictGraph:
+    """Conflict graph of a profile's lifetimes (smartpool.py:82-88)."""
+    dp = device_profile(profile)
+    g = ConflictGraph(period=profile.period, vars=None, adj=None, peak_load_bytes=profile.peak_bytes)
+    g._dev = N.conflict_from_profile(dp)
+    fp = profile._flat_profile
+    g._nv = int(dp.dims().nvars)
+    g._profile = profile
+
+    def make_vars():
+        return [PoolVar(v.var, v.size, v.alloc_index if v.alloc_index is not None else -1, v.segments,
+                        v.persistent) for v in profile.variables]
+    g._vars_fn = make_vars
+    g._names_fn = lambda: fp().var_names()
+    g._sizes_fn = lambda: fp().size
+    return g
+
+
+def _graph_device(graph: ConflictGraph):
+    """Device CSR of a graph (uploading a hand-built one)."""
+    if graph._dev is None:
+        vars_ = graph.vars
+        adj = graph.adj
+        n = len(vars_)
+        row = np.zeros(n + 1, np.int64)
+        row[1:] = np.cumsum([len(a) for a in adj]) if n else []
+        col = np.array([j for a in adj for j in sorted(a)] or [0], np.int32)
+        tie = _tie_ranks([pv.alloc_index for pv in vars_], [pv.var for pv in vars_])
+        graph._dev = N.graph_from_csr(row, col, [pv.size for pv in vars_] or [0], tie if n else np.zeros(1, np.int64))
+        graph._nv = n
+    return graph._dev
+
+
+def _graph_names_sizes(graph: ConflictGraph):
+    if getattr(graph, "_names_fn", None) is not None and graph._vars is None:
+        return graph._names_fn(), np.asarray(graph._sizes_fn())
+    return [pv.var for pv in graph.vars], np.array([pv.size for pv in graph.vars], np.int64)
+
+
+def plan_pool(graph: ConflictGraph, policy: str = "best_fit") -> PoolPlan:
+    """Greedy placement in (-size, alloc, name) order, first/best fit among
+    placed neighbours (smartpool.py:122-144), on the device."""
+    if policy not in POLICY_CODE:
+        raise ValueError(f"unknown policy {policy!r}")
+    dg = _graph_device(graph)
+    nv = graph.nvars
+    offs, footprint, _levels = N.plan_pool(dg, POLICY_CODE[policy], nv)
+    plan = PoolPlan(policy=policy, footprint_bytes=footprint if nv else 0,
+                    peak_load_bytes=graph.peak_load_bytes)
+    names, sizes = _graph_names_sizes(graph)
+    plan._cols = (names, offs, sizes)
+    plan._levels = _levels
+    return plan
+
+
+def check_plan(plan: PoolPlan, graph: ConflictGraph) -> None:
+    """Raise if conflicting variables overlap or the footprint misses one
+    (smartpool.py:147-164); a host-side safety checker."""
+    offsets = plan.offsets
+    for i, pv in enumerate(graph.vars):
+        oi = offsets[pv.var]
+        if oi < 0:
+            raise MemplanError(f"{pv.var} at negative offset")
+        if oi + pv.size > plan.footprint_bytes:
+            raise MemplanError(f"{pv.var} exceeds footprint")
+        for j in graph.adj[i]:
+            if j <= i:
+                continue
+            qv = graph.vars[j]
+            oj = offsets[qv.var]
+            if oi < oj + qv.size and oj < oi + pv.size:
+                raise MemplanError(f"conflicting vars {pv.var} and {qv.var} overlap")
+
+
+def brute_force_optimal_footprint(graph: ConflictGraph, max_vars: int = 10) -> int:
+    """Exact minimum footprint by exhaustive search over subset-sum offsets
+    (smartpool.py:167-221); a small-instance test oracle, host-side."""
+    n = len(graph.vars)
+    if n > max_vars:
+        raise GraphTooLarge(f"{n} vars exceeds cap {max_vars}")
+    if n == 0:
+        return 0
+    lower = graph.peak_load_bytes
+    best = plan_pool(graph, "best_fit").footprint_bytes
+    if best <= lower:
+        return best
+    order = sorted(range(n), key=lambda i: (-graph.vars[i].size, graph.vars[i].alloc_index, graph.vars[i].var))
+    sizes = [graph.vars[i].size for i in order]
+    pos = {v: k for k, v in enumerate(order)}
+    earlier = [[pos[j] for j in graph.adj[order[k]] if pos[j] < k] for k in range(n)]
+    sums = {0}
+    for s in sizes:
+        sums |= {x + s for x in sums}
+    cands = sorted(sums)
+    offs = [0] * n
+
+    def search(k: int, top: int) -> bool:
+        nonlocal best
+        if k == n:
+            best = top
+            return best <= lower
+        sk = sizes[k]
+        for off in cands:
+            if off + sk >= best:
+                break
+            if any(off < offs[j] + sizes[j] and offs[j] < off + sk for j in earlier[k]):
+                continue
+            offs[k] = off
+            if search(k + 1, max(top, off + sk)):
+                return True
+        return False
+
+    search(0, 0)
+    return best
+
+
+class LookupTable:
+    """Window-relative malloc op index -> (var, pool offset) (smartpool.py:224-243)."""
+
+    def __init__(self, entries: dict[int, tuple[str, int]]):
+        self._entries = dict(entries)
+
+    def __len__(self) -> int:
+        return len(self._entries)
+
+    def __contains__(self, op_index: int) -> bool:
+        return op_index in self._entries
+
+    def offset_for(self, op_index: int) -> int:
+        return self._entries[op_index][1]
+
+    def var_for(self, op_index: int) -> str:
+        return self._entries[op_index][0]
+
+    def items(self):
+        return sorted(self._entries.items())
+
+
+def make_lookup_table(plan: PoolPlan, profile: IterationProfile) -> LookupTable:
+    """Malloc op index -> offset for every window allocation (smartpool.py:246-254)."""
+    offsets = plan.offsets
+    entries = {}
+    for v in profile.variables:
+        if v.alloc_index is None:
+            continue
+        if v.var not in offsets:
+            raise MissingVariable(v.var)
+        entries[v.alloc_index] = (v.var, offsets[v.var])
+    return LookupTable(entries)
