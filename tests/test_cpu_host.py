@@ -1,0 +1,126 @@
+"""CPU-only checks: the C ABI library loads and exports every declared
+symbol, host-side plumbing (text formats, interning, generator) matches the
+reference's fixtures, and the package imports without a GPU."""
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from golden_util import load, trace_arrays
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "memplan_b200.h")
+LIB = os.path.join(ROOT, "paper_1903_06631_b200", "libmemplan_b200.so")
+
+
+def _declared():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^(?:const )?(?:int|void|int64_t)\s*\*?\s*(mp_[a-z0-9_]+)\s*\(", text, re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    if not os.path.exists(LIB):
+        subprocess.run(["make", "-s", "-j8", "-C", os.path.join(ROOT, "paper_1903_06631_b200", "csrc")], check=True)
+    import ctypes
+    lib = ctypes.CDLL(LIB)  # loads without a GPU (CUDA runtime is linked, not initialized)
+    missing = [s for s in _declared() if not hasattr(lib, s)]
+    assert not missing, missing
+    assert lib.mp_version() == 1
+    assert len(_declared()) >= 30
+
+
+def test_library_is_sm100a():
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", LIB], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_standardize_host_matches_cpython():
+    import random
+
+    from paper_1903_06631_b200 import _native as N
+    rng = random.Random(17)
+    for _ in range(2000):
+        xs = [rng.choice((rng.uniform(-1e6, 1e6), rng.randrange(-10 ** 12, 10 ** 12) * 1.0,
+                          rng.uniform(-1, 1) * 10 ** rng.randrange(-30, 30))) for _ in range(rng.randrange(1, 40))]
+        mean = sum(xs) / len(xs)
+        var = sum((x - mean) ** 2 for x in xs) / len(xs)
+        want = [0.0] * len(xs) if var <= 0 else [(x - mean) / var ** 0.5 for x in xs]
+        assert N.standardize(xs).tolist() == want
+
+
+def test_package_imports_and_exports_reference_names():
+    import paper_1903_06631_b200 as mp
+    ref_names = {
+        "Access", "ConflictGraph", "DelayedOp", "DetectedIteration", "EventKind", "GraphTooLarge", "InvalidSpec",
+        "InvariantViolation", "IterationAnalyzer", "IterationProfile", "LimitUnreachable", "LoadCurve",
+        "LoadProfile", "LookupTable", "MalformedRecord", "MemplanError", "MIB", "MissingVariable",
+        "PeriodNotFound", "PoolPlan", "PoolPlanner", "SCORE_NAMES", "ScoreWeights", "SimulationResult",
+        "SwapCandidate", "SwapDeadlock", "SwapEvent", "SwapPlanner", "SwapSchedule", "Trace", "TraceEvent",
+        "TransferModel", "VariableLifetime", "WorkloadSpec", "brute_force_optimal_footprint",
+        "build_conflict_graph", "build_schedule", "check_plan", "conflict_graph_from_arcs", "combine_with_pool",
+        "compute_load_min", "compute_load_profile", "detect_iteration", "extract_lifetimes",
+        "filter_candidates", "generate_synthetic_trace", "load_trace", "make_lookup_table", "optimize_weights",
+        "parse_trace", "plan_pool", "profile_report", "save_trace", "score_aoa", "score_doa", "score_wdoa",
+        "select_by_score", "select_by_swdoa", "absence_slots", "apply_absence", "attach_scores",
+        "combined_scores", "gap_area", "planned_peak", "selection_report", "serialize_trace", "simulate",
+        "standardize", "simulation_report", "swdoa_scores", "validate_trace", "vgg_like", "__version__"}
+    assert len(ref_names) == 73
+    assert ref_names <= set(mp.__all__)
+    for n in ref_names:
+        assert hasattr(mp, n), n
+
+
+def test_generator_reproduces_reference_traces():
+    from paper_1903_06631_b200 import synth
+    shapes = {"vgg_like_d5_s0.5_i5_seed0_t0.5": (5, 0.5, 5, 0, 0.5), "vgg_like_d8_s0.5_i3_seed1_t0.0": (8, 0.5, 3, 1, 0.0),
+              "vgg_like_d9_s0.75_i6_seed8_t0.3": (9, 0.75, 6, 8, 0.3)}
+    for sc in load("generator"):
+        if sc["name"] not in shapes:
+            continue
+        d, s, it, seed, tr = shapes[sc["name"]]
+        t = synth.generate_synthetic_trace(synth.vgg_like(depth=d, scale=s, iterations=it, seed=seed, temp_ratio=tr))
+        assert [e.t_us for e in t] == sc["trace"]["t"]
+        assert [e.var for e in t] == sc["trace"]["var"]
+        assert [e.size for e in t] == sc["trace"]["size"]
+
+
+def test_text_formats_round_trip_and_errors():
+    from paper_1903_06631_b200 import errors, trace
+    text = ('{"index":0,"t_us":0,"kind":"malloc","var":"v1","size":10}\n'
+            '{"index":1,"t_us":5,"kind":"write","var":"v1","size":0}\n')
+    events = trace._read_jsonl(text)
+    t = trace.Trace(events=events)
+    assert trace.serialize_trace(t) == text
+    csv_text = trace.serialize_trace(t, "csv")
+    assert [(e.kind, e.var, e.size) for e in trace._read_csv(csv_text)] == [(e.kind, e.var, e.size) for e in events]
+    with pytest.raises(errors.MalformedRecord) as ei:
+        trace._read_jsonl('{"index":0}\n')
+    assert ei.value.line == 1
+    with pytest.raises(errors.MalformedRecord):
+        trace._read_csv("bad,header\n")
+    with pytest.raises(errors.MalformedRecord) as ei:
+        trace._read_jsonl(text + '{"index":2,"t_us":7,"kind":"poke","var":"v1","size":0}\n')
+    assert ei.value.line == 3
+
+
+def test_interning_is_lexicographic():
+    for sc in load("hand")[:6]:
+        a = trace_arrays(sc)
+        assert a.names == sorted(a.names)
+        assert [a.names[v] for v in a.var.tolist()] == sc["trace"]["var"]
+    from paper_1903_06631_b200.trace import TraceArrays
+    a = TraceArrays.from_columns(np.zeros(4, np.uint8), ["b#1", "b", "aé", "b#10"], np.ones(4, np.int64),
+                                 np.arange(4))
+    assert a.names == sorted(["b#1", "b", "aé", "b#10"])
+
+
+def test_workload_builders_shapes():
+    from paper_1903_06631_b200 import workloads
+    arrays, window = workloads.interval_trace(nvars=500, seed=3)
+    assert len(arrays) == 2 * (2 * 500 + 4) and window == (1004, 2008)
+    acts, wts = workloads.resnet50_layers(32)
+    assert len(acts) == len(wts) == 50
+    acts, wts = workloads.vgg16_layers(64)
+    assert len(acts) == 21
