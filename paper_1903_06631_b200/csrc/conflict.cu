@@ -83,6 +83,50 @@ __global__ void k_iv_counts(int64_t n, const uint32_t *sstart, const uint32_t *p
   }
 }
 
+__global__ void k_iv_minmax(int64_t n, const int32_t *ea, const int32_t *eb, int *mm) {
+  int lo = INT32_MAX, hi = INT32_MIN;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    lo = min(lo, ea[i]);
+    hi = max(hi, eb[i]);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(FULL_MASK, lo, o));
+    hi = max(hi, __shfl_xor_sync(FULL_MASK, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&mm[0], lo);
+    atomicMax(&mm[1], hi);
+  }
+}
+
+__global__ void k_iv_hist(int64_t n, const int32_t *ea, const int32_t *eb, int32_t base, int32_t *hs, int32_t *he) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    atomicAdd(&hs[ea[i] - base], 1);
+    atomicAdd(&he[eb[i] - base], 1);  // exclusive scan: cum_e[x - base + 1] = #ends <= x
+  }
+}
+
+__global__ void k_iv_scatter(int64_t n, const int32_t *ea, int32_t base, const int32_t *offs, int32_t *cur,
+                             uint32_t *perm) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t x = ea[i] - base;
+    perm[offs[x] + atomicAdd(&cur[x], 1)] = (uint32_t)i;
+  }
+}
+
+// forward run = sorted positions (k, #starts < end); backward = k - #ends <= start
+__global__ void k_iv_counts_dense(int64_t n, const uint32_t *perm, const int32_t *ea, const int32_t *eb, int32_t base,
+                                  const int32_t *offs, const int32_t *cum_e, int64_t *cnt, int32_t *fwd) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t iid = perm[k];
+    int64_t f = (int64_t)offs[eb[iid] - base] - k - 1;
+    int64_t bw = k - cum_e[ea[iid] - base + 1];
+    fwd[iid] = (int32_t)f;
+    cnt[iid] = f + bw;
+  }
+}
+
 __global__ void k_row_off(int64_t nv, const int64_t *eoff, const int64_t *sub_off, int64_t *row_off) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v <= nv; v += (int64_t)gridDim.x * blockDim.x)
     row_off[v] = sub_off[eoff[v]];
@@ -165,21 +209,49 @@ static int build_csr(mp_ctx *ctx, int64_t nv, const int64_t *seg_off_d, const in
   CUDA_TRY(fwd.alloc(ni, st)); CUDA_TRY(scur.alloc(nv, st));
   LAUNCH(ctx, k_norm_count, grid_for(nv, 128), 128, 0, nv, seg_off_d, lo_d, hi_d, ecnt.p, ea.p, eb.p,
          d_over, 1, eoff.p, ivar.p);
-  // sort starts (with interval ids) and ends
-  DBuf<uint32_t> skey, perm, ekey, edummy;
+  // order intervals by start.  Interval bounds are op positions, so when
+  // their range is small a counting sort does it (order among equal starts
+  // is irrelevant: each overlapping pair is still emitted exactly once); the
+  // backward counts then need only a histogram of ends, no sorted copy.
+  DBuf<uint32_t> skey, perm;
   CUDA_TRY(skey.alloc(ni, st)); CUDA_TRY(perm.alloc(ni, st));
-  CUDA_TRY(ekey.alloc(ni, st)); CUDA_TRY(edummy.alloc(ni, st));
-  LAUNCH(ctx, k_iv_keys, grid_for(ni, 256), 256, 0, ni, ea.p, skey.p, perm.p);
-  LAUNCH(ctx, k_iv_keys, grid_for(ni, 256), 256, 0, ni, eb.p, ekey.p, edummy.p);
-  int kb = 32;
-  rc = dev_radix_sort_u32(ctx, skey.p, perm.p, ni, kb, err);
-  if (rc) return rc;
-  rc = dev_radix_sort_u32(ctx, ekey.p, edummy.p, ni, kb, err);
-  if (rc) return rc;
   DBuf<int64_t> cnt, sub_off;
   CUDA_TRY(cnt.alloc(ni + 1, st));
   CUDA_TRY(sub_off.alloc(ni + 1, st));
-  LAUNCH(ctx, k_iv_counts, grid_for(ni, 256), 256, 0, ni, skey.p, perm.p, ekey.p, eb.p, cnt.p, fwd.p);
+  int *d_mm = (int *)(ctx->d_small + 4);
+  int mm_init[2] = {INT32_MAX, INT32_MIN};
+  CUDA_TRY(cudaMemcpyAsync(d_mm, mm_init, 8, cudaMemcpyHostToDevice, st));
+  LAUNCH(ctx, k_iv_minmax, grid_for(ni, 256, 1024), 256, 0, ni, ea.p, eb.p, d_mm);
+  int mm[2];
+  rc = dev_read_n(ctx, d_mm, mm, 8, err);
+  if (rc) return rc;
+  int64_t range = ni ? (int64_t)mm[1] - mm[0] + 1 : 1;
+  if (range <= 8 * ni + 4096) {
+    DBuf<int32_t> hs, he, offs_s, cum_e, curs;
+    CUDA_TRY(hs.alloc(range + 1, st)); CUDA_TRY(he.alloc(range + 2, st)); CUDA_TRY(offs_s.alloc(range + 1, st));
+    CUDA_TRY(cum_e.alloc(range + 2, st)); CUDA_TRY(curs.alloc(range + 1, st));
+    CUDA_TRY(cudaMemsetAsync(hs.p, 0, (range + 1) * 4, st));
+    CUDA_TRY(cudaMemsetAsync(he.p, 0, (range + 2) * 4, st));
+    CUDA_TRY(cudaMemsetAsync(curs.p, 0, (range + 1) * 4, st));
+    LAUNCH(ctx, k_iv_hist, grid_for(ni, 256), 256, 0, ni, ea.p, eb.p, mm[0], hs.p, he.p);
+    rc = dev_exclusive_scan<int32_t>(ctx, hs.p, offs_s.p, range + 1, nullptr, err);
+    if (rc) return rc;
+    rc = dev_exclusive_scan<int32_t>(ctx, he.p, cum_e.p, range + 2, nullptr, err);
+    if (rc) return rc;
+    LAUNCH(ctx, k_iv_scatter, grid_for(ni, 256), 256, 0, ni, ea.p, mm[0], offs_s.p, curs.p, perm.p);
+    LAUNCH(ctx, k_iv_counts_dense, grid_for(ni, 256), 256, 0, ni, perm.p, ea.p, eb.p, mm[0], offs_s.p, cum_e.p,
+           cnt.p, fwd.p);
+  } else {
+    DBuf<uint32_t> ekey, edummy;
+    CUDA_TRY(ekey.alloc(ni, st)); CUDA_TRY(edummy.alloc(ni, st));
+    LAUNCH(ctx, k_iv_keys, grid_for(ni, 256), 256, 0, ni, ea.p, skey.p, perm.p);
+    LAUNCH(ctx, k_iv_keys, grid_for(ni, 256), 256, 0, ni, eb.p, ekey.p, edummy.p);
+    rc = dev_radix_sort_u32(ctx, skey.p, perm.p, ni, 32, err);
+    if (rc) return rc;
+    rc = dev_radix_sort_u32(ctx, ekey.p, edummy.p, ni, 32, err);
+    if (rc) return rc;
+    LAUNCH(ctx, k_iv_counts, grid_for(ni, 256), 256, 0, ni, skey.p, perm.p, ekey.p, eb.p, cnt.p, fwd.p);
+  }
   rc = dev_exclusive_scan<int64_t>(ctx, cnt.p, sub_off.p, ni, d_tot, err);
   if (rc) return rc;
   CUDA_TRY(cudaMemcpyAsync(sub_off.p + ni, d_tot, 8, cudaMemcpyDeviceToDevice, st));

@@ -203,14 +203,18 @@ __global__ void __launch_bounds__(DT_THREADS) k_hash_tiles(const uint8_t *kind, 
   if (threadIdx.x == 0) tile_agg[blockIdx.x] = tot;
 }
 
-__global__ void k_hash_tile_prefix(HPair *agg, int64_t ntiles) {
-  // sequential over tiles (ntiles = n / 4096, small)
-  if (threadIdx.x || blockIdx.x) return;
-  HPair run{0, 1};
-  for (int64_t t = 0; t < ntiles; t++) {
-    HPair x = agg[t];
-    agg[t] = run;
-    run = hcombine(run, x);
+// exclusive prefix of the tile aggregates, one CTA in chunks of DT_THREADS
+__global__ void __launch_bounds__(DT_THREADS) k_hash_tile_prefix(HPair *agg, int64_t ntiles) {
+  __shared__ HPair tot;
+  HPair carry{0, 1};
+  for (int64_t base = 0; base < ntiles; base += DT_THREADS) {
+    int64_t t = base + threadIdx.x;
+    HPair x = t < ntiles ? agg[t] : HPair{0, 1};
+    HPair ex = block_scan_hash(x, &tot);
+    __syncthreads();
+    if (t < ntiles) agg[t] = hcombine(carry, ex);
+    carry = hcombine(carry, tot);
+    __syncthreads();
   }
 }
 
@@ -237,12 +241,23 @@ __global__ void __launch_bounds__(DT_THREADS) k_hash_prefix(const uint8_t *kind,
   if (blockIdx.x == 0 && threadIdx.x == 0) P[0] = 0;
 }
 
+// each thread tests a run of PC_RUN consecutive periods, carrying B^p along
+constexpr int PC_RUN = 32;
 __global__ void k_period_candidates(const uint64_t *P, int64_t n, int64_t pmin, unsigned long long *best) {
-  for (int64_t p = pmin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p <= n / 2; p += (int64_t)gridDim.x * blockDim.x) {
-    uint64_t bp = powmod61(HBASE, (uint64_t)p);
-    uint64_t h1 = submod61(P[n], mulmod61(P[n - p], bp));
-    uint64_t h2 = submod61(P[n - p], mulmod61(P[n - 2 * p], bp));
-    if (h1 == h2) atomicMin(best, (unsigned long long)p);
+  int64_t nruns = (n / 2 - pmin + PC_RUN) / PC_RUN;
+  for (int64_t run = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; run < nruns; run += (int64_t)gridDim.x * blockDim.x) {
+    int64_t p0 = pmin + run * PC_RUN;
+    uint64_t bp = powmod61(HBASE, (uint64_t)p0);
+    uint64_t pn = P[n];
+    for (int64_t p = p0; p < p0 + PC_RUN && p <= n / 2; p++) {
+      uint64_t h1 = submod61(pn, mulmod61(P[n - p], bp));
+      uint64_t h2 = submod61(P[n - p], mulmod61(P[n - 2 * p], bp));
+      if (h1 == h2) {
+        atomicMin(best, (unsigned long long)p);
+        break;
+      }
+      bp = mulmod61(bp, HBASE);
+    }
   }
 }
 
@@ -266,14 +281,15 @@ extern "C" int mp_detect(mp_ctx *ctx, mp_dtrace *t, int64_t *period, mp_err *err
   CUDA_TRY(agg.alloc(ntiles, ctx->stream));
   CUDA_TRY(P.alloc(n + 1, ctx->stream));
   LAUNCH(ctx, k_hash_tiles, (unsigned)ntiles, DT_THREADS, 0, t->kind.p, t->size.p, n, agg.p);
-  LAUNCH(ctx, k_hash_tile_prefix, 1, 32, 0, agg.p, ntiles);
+  LAUNCH(ctx, k_hash_tile_prefix, 1, DT_THREADS, 0, agg.p, ntiles);
   LAUNCH(ctx, k_hash_prefix, (unsigned)ntiles, DT_THREADS, 0, t->kind.p, t->size.p, n, agg.p, P.p);
   unsigned long long *d_best = (unsigned long long *)ctx->d_small;
   int *d_bad = (int *)(ctx->d_small + 1);
   int64_t pmin = 1;
   for (;;) {
     CUDA_TRY(cudaMemsetAsync(d_best, 0xff, 8, ctx->stream));
-    LAUNCH(ctx, k_period_candidates, grid_for(n / 2 - pmin + 1, 256, 8192), 256, 0, P.p, n, pmin, d_best);
+    LAUNCH(ctx, k_period_candidates, grid_for((n / 2 - pmin + PC_RUN) / PC_RUN, 256, 8192), 256, 0, P.p, n, pmin,
+           d_best);
     int64_t best;
     int rc = dev_read_i64(ctx, (const int64_t *)d_best, &best, err);
     if (rc) return rc;

@@ -269,12 +269,15 @@ __device__ int64_t place_mem(const PlaceArgs &a, P buf, int64_t rb, int m, int64
 }
 
 constexpr int PLACE_THREADS = 256;
+constexpr int PLACE_MIN_BLOCKS = 5;  // <= 48 registers: 40 resident warps per SM
+
+
 
 // Asynchronous dataflow placement: warps claim ready variables from a
 // queue in order; placing a variable decrements its successors' counters
 // and the last predecessor to finish publishes the successor.  No grid-wide
 // barrier: a variable starts the moment its last predecessor is placed.
-__global__ void __launch_bounds__(PLACE_THREADS) k_place_async(PlaceArgs a) {
+__global__ void __launch_bounds__(PLACE_THREADS, PLACE_MIN_BLOCKS) k_place_async(PlaceArgs a) {
   const int lane = threadIdx.x & 31;
   int64_t gwarp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   long long fp = LLONG_MIN;
@@ -286,11 +289,15 @@ __global__ void __launch_bounds__(PLACE_THREADS) k_place_async(PlaceArgs a) {
     if (i >= a.V) break;
     int v1 = 0;
     if (lane == 0) {
-      volatile int32_t *q = a.queue + i;
-      while ((v1 = *q) == 0) __nanosleep(32);
+      // acquire: the predecessors' offsets were released before this slot was published
+      const int32_t *q = a.queue + i;
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v1) : "l"(q) : "memory");
+        if (v1) break;
+        __nanosleep(20);
+      }
     }
     int32_t v = __shfl_sync(FULL_MASK, v1, 0) - 1;
-    __threadfence();
     int64_t rb = a.row_off[v];
     int m = a.pcnt[v];
     int64_t need = a.size[v];
@@ -320,16 +327,30 @@ __global__ void __launch_bounds__(PLACE_THREADS) k_place_async(PlaceArgs a) {
       a.level[v] = lvl;
       if (o + need > fp) fp = o + need;
       if (lvl > dmax) dmax = lvl;
+      __threadfence();  // offsets visible before any successor counter drops
     }
-    __threadfence();
     __syncwarp();
     int64_t deg = a.row_off[v + 1] - rb;
-    for (int64_t k = m + lane; k < deg; k += 32) {
-      int32_t j = a.col[rb + k];
-      if (atomicSub(&a.remaining[j], 1) == 1) {
-        __threadfence();
-        int slot = atomicAdd(a.tail, 1);
-        *(volatile int32_t *)(a.queue + slot) = j + 1;
+    for (int64_t k = m + lane; k - lane < deg; k += 32) {
+      bool ready = false;
+      int32_t j = 0;
+      if (k < deg) {
+        j = a.col[rb + k];
+        ready = atomicSub(&a.remaining[j], 1) == 1;
+      }
+      // publish the newly ready successors with one tail bump per chunk
+      unsigned bal = __ballot_sync(FULL_MASK, ready);
+      if (bal) {
+        int base = 0;
+        if (lane == __ffs(bal) - 1) {
+          __threadfence();
+          base = atomicAdd(a.tail, __popc(bal));
+        }
+        base = __shfl_sync(FULL_MASK, base, __ffs(bal) - 1);
+        if (ready) {
+          int32_t *q = a.queue + base + __popc(bal & lanemask_lt());
+          asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(q), "r"(j + 1) : "memory");
+        }
       }
     }
   }
