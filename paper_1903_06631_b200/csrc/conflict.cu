@@ -22,6 +22,8 @@ constexpr int MAXSEG = 64;
 __global__ void k_norm_count(int64_t nv, const int64_t *seg_off, const int32_t *lo, const int32_t *hi,
                              int64_t *ecnt, int32_t *ea, int32_t *eb, int *overflow, int write,
                              const int64_t *eoff, int32_t *ivar) {
+  // counting pass (write == 0): eb doubles as the (min start, max end) cell
+  int32_t lmin = INT32_MAX, lmax = INT32_MIN;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
     int32_t L[MAXSEG], H[MAXSEG];
     int m = 0;
@@ -45,11 +47,25 @@ __global__ void k_norm_count(int64_t nv, const int64_t *seg_off, const int32_t *
         ea[out + c] = L[k];
         eb[out + c] = ne;
         ivar[out + c] = (int32_t)v;
+      } else {
+        lmin = min(lmin, L[k]);
+        lmax = max(lmax, ne);
       }
       c++;
       cur_end = ne;
     }
     if (!write) ecnt[v] = c;
+  }
+  if (!write) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      lmin = min(lmin, __shfl_xor_sync(FULL_MASK, lmin, o));
+      lmax = max(lmax, __shfl_xor_sync(FULL_MASK, lmax, o));
+    }
+    if ((threadIdx.x & 31) == 0 && lmin <= lmax) {
+      atomicMin(&eb[0], lmin);
+      atomicMax(&eb[1], lmax);
+    }
   }
 }
 
@@ -81,6 +97,20 @@ __global__ void k_iv_counts(int64_t n, const uint32_t *sstart, const uint32_t *p
     fwd[iid] = (int32_t)f;
     cnt[iid] = f + bw;
   }
+}
+
+__global__ void k_arena_need(int64_t V, const int64_t *row_off, unsigned long long *need) {
+  unsigned long long s = 0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
+    int64_t d = row_off[v + 1] - row_off[v];
+    if (d > 128) {
+      unsigned long long n2 = 64;
+      while (n2 < (unsigned long long)d) n2 <<= 1;
+      s += n2;
+    }
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(need, s);
 }
 
 __global__ void k_iv_minmax(int64_t n, const int32_t *ea, const int32_t *eb, int *mm) {
@@ -180,30 +210,40 @@ static int build_csr(mp_ctx *ctx, int64_t nv, const int64_t *seg_off_d, const in
   // placement order first: the fill writes rows already split by it
   CUDA_TRY(g->rank.alloc(nv, st));
   CUDA_TRY(g->pcnt.alloc(nv, st));
-  if (nv) {
-    int rc0 = placement_rank(ctx, nv, g->size.p, g->tiekey.p, g->rank.p, err);
-    if (rc0) return rc0;
-  }
   StageTimer *tm = new StageTimer(ctx, MP_ST_CONFLICT_PREP);
   DBuf<int64_t> ecnt, eoff;
   CUDA_TRY(ecnt.alloc(nv + 1, st));
   CUDA_TRY(eoff.alloc(nv + 1, st));
+  // d_small: [0] overflow flag, [1] interval count, [4] (min start, max end),
+  // [6..7] size-key range for the placement order — one readback for all
   int *d_over = (int *)ctx->d_small;
+  int *d_mm = (int *)(ctx->d_small + 4);
+  unsigned long long *d_kmm = (unsigned long long *)(ctx->d_small + 6);
   CUDA_TRY(cudaMemsetAsync(d_over, 0, 4, st));
+  int mm_init[2] = {INT32_MAX, INT32_MIN};
+  CUDA_TRY(cudaMemcpyAsync(d_mm, mm_init, 8, cudaMemcpyHostToDevice, st));
+  int rc = placement_rank_keys(ctx, nv, g->size.p, d_kmm, err);
+  if (rc) return rc;
   LAUNCH(ctx, k_norm_count, grid_for(nv, 128), 128, 0, nv, seg_off_d, lo_d, hi_d, ecnt.p, (int32_t *)nullptr,
-         (int32_t *)nullptr, d_over, 0, (const int64_t *)nullptr, (int32_t *)nullptr);
+         d_mm, d_over, 0, (const int64_t *)nullptr, (int32_t *)nullptr);
   int64_t *d_tot = ctx->d_small + 1;
-  int rc = dev_exclusive_scan<int64_t>(ctx, ecnt.p, eoff.p, nv, d_tot, err);
+  rc = dev_exclusive_scan<int64_t>(ctx, ecnt.p, eoff.p, nv, d_tot, err);
   if (rc) return rc;
   CUDA_TRY(cudaMemcpyAsync(eoff.p + nv, d_tot, 8, cudaMemcpyDeviceToDevice, st));
-  int64_t h[2];
-  rc = dev_read_n(ctx, ctx->d_small, h, 16, err);
+  int64_t h[8];
+  rc = dev_read_n(ctx, ctx->d_small, h, 64, err);
   if (rc) return rc;
   if ((int)h[0]) {
     mp_set_err(err, MP_E_UNSUPPORTED, 0, MAXSEG, 0, "more than 64 segments on one variable");
     return MP_E_UNSUPPORTED;
   }
   int64_t ni = h[1];
+  int mm[2];
+  memcpy(mm, &h[4], 8);
+  if (nv) {
+    rc = placement_rank_sort(ctx, nv, g->size.p, g->tiekey.p, g->rank.p, (uint64_t)h[6], (uint64_t)h[7], err);
+    if (rc) return rc;
+  }
   DBuf<int32_t> ea, eb, ivar, fwd, scur;
   CUDA_TRY(ea.alloc(ni, st)); CUDA_TRY(eb.alloc(ni, st)); CUDA_TRY(ivar.alloc(ni, st));
   CUDA_TRY(fwd.alloc(ni, st)); CUDA_TRY(scur.alloc(nv, st));
@@ -218,13 +258,6 @@ static int build_csr(mp_ctx *ctx, int64_t nv, const int64_t *seg_off_d, const in
   DBuf<int64_t> cnt, sub_off;
   CUDA_TRY(cnt.alloc(ni + 1, st));
   CUDA_TRY(sub_off.alloc(ni + 1, st));
-  int *d_mm = (int *)(ctx->d_small + 4);
-  int mm_init[2] = {INT32_MAX, INT32_MIN};
-  CUDA_TRY(cudaMemcpyAsync(d_mm, mm_init, 8, cudaMemcpyHostToDevice, st));
-  LAUNCH(ctx, k_iv_minmax, grid_for(ni, 256, 1024), 256, 0, ni, ea.p, eb.p, d_mm);
-  int mm[2];
-  rc = dev_read_n(ctx, d_mm, mm, 8, err);
-  if (rc) return rc;
   int64_t range = ni ? (int64_t)mm[1] - mm[0] + 1 : 1;
   if (range <= 8 * ni + 4096) {
     DBuf<int32_t> hs, he, offs_s, cum_e, curs;
@@ -255,14 +288,21 @@ static int build_csr(mp_ctx *ctx, int64_t nv, const int64_t *seg_off_d, const in
   rc = dev_exclusive_scan<int64_t>(ctx, cnt.p, sub_off.p, ni, d_tot, err);
   if (rc) return rc;
   CUDA_TRY(cudaMemcpyAsync(sub_off.p + ni, d_tot, 8, cudaMemcpyDeviceToDevice, st));
-  int64_t nnz;
-  rc = dev_read_i64(ctx, d_tot, &nnz, err);
+  CUDA_TRY(g->row_off.alloc(nv + 1, st));
+  LAUNCH(ctx, k_row_off, grid_for(nv + 1, 256), 256, 0, nv, eoff.p, sub_off.p, g->row_off.p);
+  // placement scratch for rows longer than the register sorts (degree bounds
+  // the predecessor count), read back with nnz
+  unsigned long long *d_arena = (unsigned long long *)(ctx->d_small + 2);
+  CUDA_TRY(cudaMemsetAsync(d_arena, 0, 8, st));
+  LAUNCH(ctx, k_arena_need, grid_for(nv, 256, 2048), 256, 0, nv, g->row_off.p, d_arena);
+  int64_t h2[2];
+  rc = dev_read_n(ctx, d_tot, h2, 16, err);
   if (rc) return rc;
+  int64_t nnz = h2[0];
   g->nvars = nv;
   g->nnz = nnz;
-  CUDA_TRY(g->row_off.alloc(nv + 1, st));
+  g->arena_need = h2[1];
   CUDA_TRY(g->col.alloc(nnz, st));
-  LAUNCH(ctx, k_row_off, grid_for(nv + 1, 256), 256, 0, nv, eoff.p, sub_off.p, g->row_off.p);
   CUDA_TRY(cudaMemsetAsync(scur.p, 0, nv * 4, st));
   CUDA_TRY(cudaMemsetAsync(g->pcnt.p, 0, nv * 4, st));
   delete tm;
@@ -401,6 +441,13 @@ extern "C" int mp_graph_from_csr(mp_ctx *ctx, int32_t nvars, const int64_t *row_
     if (rc) { delete g; return rc; }
     LAUNCH(ctx, k_partition_rows, grid_for(nv * 32, 256, 148 * 64), 256, 0, nv, g->row_off.p, cin.p, g->rank.p,
            g->col.p, g->pcnt.p);
+    unsigned long long *d_arena = (unsigned long long *)(ctx->d_small + 2);
+    CUDA_TRY(cudaMemsetAsync(d_arena, 0, 8, st));
+    LAUNCH(ctx, k_arena_need, grid_for(nv, 256, 2048), 256, 0, nv, g->row_off.p, d_arena);
+    int64_t need;
+    rc = dev_read_i64(ctx, (const int64_t *)d_arena, &need, err);
+    if (rc) { delete g; return rc; }
+    g->arena_need = need;
   }
   CUDA_TRY(cudaStreamSynchronize(st));
   *out = g;

@@ -47,8 +47,12 @@ struct mp_dgraph {
   DBuf<int64_t> offsets;  // last plan
   DBuf<int32_t> rank;     // position in the placement order (-size, tie)
   DBuf<int32_t> pcnt;     // row prefix holding the placement predecessors
+  int64_t arena_need = 0; // scratch ranges for rows longer than 128
 };
 
 int build_groups(mp_ctx *ctx, mp_dtrace *t, mp_err *err);
 int placement_rank(mp_ctx *ctx, int64_t V, const int64_t *size, const int64_t *tiekey, int32_t *rank,
                    mp_err *err);
+int placement_rank_keys(mp_ctx *ctx, int64_t V, const int64_t *size, unsigned long long *mm, mp_err *err);
+int placement_rank_sort(mp_ctx *ctx, int64_t V, const int64_t *size, const int64_t *tiekey, int32_t *rank,
+                        uint64_t kmin, uint64_t kmax, mp_err *err);

@@ -261,7 +261,11 @@ __global__ void k_period_candidates(const uint64_t *P, int64_t n, int64_t pmin, 
   }
 }
 
-__global__ void k_period_verify(const uint8_t *kind, const int64_t *size, int64_t n, int64_t p, int *bad) {
+__global__ void k_period_verify(const uint8_t *kind, const int64_t *size, int64_t n, const unsigned long long *pbest,
+                                int *bad) {
+  unsigned long long pb = *pbest;
+  if (pb == ~0ull) return;
+  int64_t p = (int64_t)pb;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < p; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t a = n - p + i, b = n - 2 * p + i;
     if (kind[a] != kind[b] || size[a] != size[b]) *bad = 1;
@@ -288,21 +292,21 @@ extern "C" int mp_detect(mp_ctx *ctx, mp_dtrace *t, int64_t *period, mp_err *err
   int64_t pmin = 1;
   for (;;) {
     CUDA_TRY(cudaMemsetAsync(d_best, 0xff, 8, ctx->stream));
+    CUDA_TRY(cudaMemsetAsync(d_bad, 0, 4, ctx->stream));
     LAUNCH(ctx, k_period_candidates, grid_for((n / 2 - pmin + PC_RUN) / PC_RUN, 256, 8192), 256, 0, P.p, n, pmin,
            d_best);
-    int64_t best;
-    int rc = dev_read_i64(ctx, (const int64_t *)d_best, &best, err);
+    // exact check of the smallest hash match, read back together with it
+    LAUNCH(ctx, k_period_verify, grid_for(n / 2, 256, 4096), 256, 0, t->kind.p, t->size.p, n,
+           (const unsigned long long *)d_best, d_bad);
+    int64_t h[2];
+    int rc = dev_read_n(ctx, d_best, h, 16, err);
     if (rc) return rc;
+    int64_t best = h[0];
     if ((uint64_t)best == ~0ull) {
       mp_set_err(err, MP_E_PERIOD_NOT_FOUND, n, 0, 0, "no period");
       return MP_E_PERIOD_NOT_FOUND;
     }
-    CUDA_TRY(cudaMemsetAsync(d_bad, 0, 4, ctx->stream));
-    LAUNCH(ctx, k_period_verify, grid_for(best, 256, 4096), 256, 0, t->kind.p, t->size.p, n, best, d_bad);
-    int bad = 0;
-    rc = dev_read_n(ctx, d_bad, &bad, 4, err);
-    if (rc) return rc;
-    if (!bad) {
+    if (!(int)h[1]) {
       *period = best;
       return MP_OK;
     }
@@ -597,7 +601,8 @@ __global__ void k_load_argmax(const int64_t *loads, int64_t p, const long long *
 }
 
 // loads + peak for any device profile (also used after uploads)
-int profile_loads(mp_ctx *ctx, mp_dprofile *P, mp_err *err) {
+// loads + peak (left in ctx->d_small[0..1] = peak, earliest argmax)
+int profile_loads_async(mp_ctx *ctx, mp_dprofile *P, mp_err *err) {
   StageTimer tm(ctx, MP_ST_LOADS);
   int64_t p = P->d.period, V = P->d.nvars;
   DBuf<int64_t> diff;
@@ -618,6 +623,13 @@ int profile_loads(mp_ctx *ctx, mp_dprofile *P, mp_err *err) {
   CUDA_TRY(cudaMemsetAsync(d_idx, 0xff, 8, ctx->stream));
   LAUNCH(ctx, k_load_peak, grid_for(p, 256, 2048), 256, 0, P->loads.p, p, d_peak);
   LAUNCH(ctx, k_load_argmax, grid_for(p, 256, 2048), 256, 0, P->loads.p, p, d_peak, d_idx);
+  return MP_OK;
+}
+
+int profile_loads(mp_ctx *ctx, mp_dprofile *P, mp_err *err) {
+  int rc = profile_loads_async(ctx, P, err);
+  if (rc) return rc;
+  int64_t p = P->d.period;
   int64_t h[2];
   rc = dev_read_n(ctx, ctx->d_small, h, 16, err);
   if (rc) return rc;
@@ -673,28 +685,30 @@ extern "C" int mp_extract(mp_ctx *ctx, mp_dtrace *t, int64_t start, int64_t end,
   LAUNCH(ctx, k_ex_var, grid_for(nv, 128), 128, 0, t->kind.p, t->size.p, t->perm.p, t->gstart.p, nv,
          start, end, s, d_first);
   LAUNCH(ctx, k_ex_marks, grid_for(p, 256), 256, 0, t->kind.p, start, p, is_malloc.p);
-  int64_t first;
-  rc = dev_read_i64(ctx, (const int64_t *)d_first, &first, err);
+  // twins and ordinals run before the violation check so one readback
+  // returns both (on a violation their output is simply discarded)
+  LAUNCH(ctx, k_ex_twin, grid_for(nv, 256), 256, 0, t->kind.p, t->size.p, nv, start, p, s);
+  // carry ordinals (surviving carry-ins, by name = var id) and window ordinals
+  int32_t *d_tot = (int32_t *)(ctx->d_small + 1);
+  rc = dev_exclusive_scan<int32_t>(ctx, c_surv.p, carry_ord.p, nv, d_tot, err);
   if (rc) return rc;
-  if ((uint64_t)first != ~0ull) {
-    int64_t r = (int64_t)((uint64_t)first >> 4);
+  rc = dev_exclusive_scan<int32_t>(ctx, is_malloc.p, win_ord.p, p, d_tot + 1, err);
+  if (rc) return rc;
+  int64_t hs[2];
+  rc = dev_read_n(ctx, ctx->d_small, hs, 16, err);
+  if (rc) return rc;
+  uint64_t first = (uint64_t)hs[0];
+  if (first != ~0ull) {
+    int64_t r = (int64_t)(first >> 4);
     int32_t v;
     rc = dev_read_n(ctx, t->var.p + start + r, &v, 4, err);
     if (rc) return rc;
     mp_set_err(err, MP_E_INVARIANT, r, (int64_t)(first & 15), v, "window invariant");
     return MP_E_INVARIANT;
   }
-  LAUNCH(ctx, k_ex_twin, grid_for(nv, 256), 256, 0, t->kind.p, t->size.p, nv, start, p, s);
-  // carry ordinals (surviving carry-ins, by name = var id) and window ordinals
-  int32_t *d_tot = (int32_t *)ctx->d_small;
-  rc = dev_exclusive_scan<int32_t>(ctx, c_surv.p, carry_ord.p, nv, d_tot, err);
-  if (rc) return rc;
-  rc = dev_exclusive_scan<int32_t>(ctx, is_malloc.p, win_ord.p, p, d_tot + 2, err);
-  if (rc) return rc;
-  int32_t tots[4];
-  rc = dev_read_n(ctx, d_tot, tots, 16, err);
-  if (rc) return rc;
-  int64_t ncarry = tots[0], nwin = tots[2];
+  int32_t tots[2];
+  memcpy(tots, &hs[1], 8);
+  int64_t ncarry = tots[0], nwin = tots[1];
 
   mp_dprofile *P = new mp_dprofile();
   P->ctx = ctx;
@@ -723,23 +737,24 @@ extern "C" int mp_extract(mp_ctx *ctx, mp_dtrace *t, int64_t start, int64_t end,
   rc = dev_exclusive_scan<int64_t>(ctx, acc_cnt.p, P->acc_off.p, V, d_atot, err);
   if (rc) return rc;
   CUDA_TRY(cudaMemcpyAsync(P->acc_off.p + V, d_atot, 8, cudaMemcpyDeviceToDevice, st));
-  int64_t A;
-  rc = dev_read_i64(ctx, d_atot, &A, err);
-  if (rc) { delete P; return rc; }
-  P->d.naccess = A;
-  CUDA_TRY(P->acc_index.alloc(A, st)); CUDA_TRY(P->acc_kind.alloc(A, st)); CUDA_TRY(P->acc_next.alloc(A, st));
+  // accesses are window reads/writes: p bounds their count, no readback needed
+  CUDA_TRY(P->acc_index.alloc(p, st)); CUDA_TRY(P->acc_kind.alloc(p, st)); CUDA_TRY(P->acc_next.alloc(p, st));
   o = prof_out(P);
   LAUNCH(ctx, k_ex_access, grid_for(nv, 128), 128, 0, t->kind.p, t->perm.p, t->gstart.p, nv, start, end,
          ncarry, s, carry_ord.p, win_ord.p, o);
   double *d_dur = (double *)(ctx->d_small + 3);
   LAUNCH(ctx, k_ex_times, grid_for(p, 256), 256, 0, t->t_us.p, start, end, P->op_times.p, d_dur);
   delete tm;
-  rc = profile_loads(ctx, P, err);
+  rc = profile_loads_async(ctx, P, err);
   if (rc) { delete P; return rc; }
-  double dur;
-  rc = dev_read_n(ctx, d_dur, &dur, 8, err);
+  // one readback: peak, peak index, access count, period duration
+  int64_t fin[4];
+  rc = dev_read_n(ctx, ctx->d_small, fin, 32, err);
   if (rc) { delete P; return rc; }
-  P->d.duration_us = dur;
+  P->d.peak_bytes = p ? fin[0] : 0;
+  P->d.peak_index = p ? fin[1] : 0;
+  P->d.naccess = fin[2];
+  memcpy(&P->d.duration_us, &fin[3], 8);
   // the profile keeps its own copy of the name table
   P->nnames = t->nvars;
   CUDA_TRY(P->blob.alloc(t->name_bytes, st));

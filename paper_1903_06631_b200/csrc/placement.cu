@@ -428,7 +428,73 @@ __global__ void k_ready_init(int64_t V, const int32_t *pcnt, int32_t *remaining,
 }
 
 // placement rank of every vertex: (-size, tiekey or vertex index)
+__global__ void k_size_range(int64_t V, const int64_t *size, unsigned long long *mm) {
+  unsigned long long lmn = ~0ull, lmx = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t k = desc_size_key(size[i]);
+    lmn = k < lmn ? k : lmn;
+    lmx = k > lmx ? k : lmx;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    unsigned long long a = __shfl_xor_sync(FULL_MASK, lmn, o), b = __shfl_xor_sync(FULL_MASK, lmx, o);
+    lmn = a < lmn ? a : lmn;
+    lmx = b > lmx ? b : lmx;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&mm[0], lmn);
+    atomicMax(&mm[1], lmx);
+  }
+}
+
+// the size-key range (so the order sort only passes over the bits that
+// vary); left in mm[0..1] on the device for the caller's next readback
+int placement_rank_keys(mp_ctx *ctx, int64_t V, const int64_t *size, unsigned long long *mm, mp_err *err) {
+  CUDA_TRY(cudaMemsetAsync(mm, 0xff, 8, ctx->stream));
+  CUDA_TRY(cudaMemsetAsync(mm + 1, 0, 8, ctx->stream));
+  if (V) LAUNCH(ctx, k_size_range, grid_for(V, 256, 1024), 256, 0, V, size, mm);
+  return MP_OK;
+}
+
+// rank[v] = position in (-size, tiekey or vertex) order, size keys in [kmin, kmax]
+int placement_rank_sort(mp_ctx *ctx, int64_t V, const int64_t *size, const int64_t *tiekey, int32_t *rank,
+                        uint64_t kmin, uint64_t kmax, mp_err *err) {
+  StageTimer tm(ctx, MP_ST_PLACE_ORDER);
+  cudaStream_t st = ctx->stream;
+  DBuf<uint64_t> keys;
+  DBuf<uint32_t> order;
+  CUDA_TRY(keys.alloc(V, st));
+  CUDA_TRY(order.alloc(V, st));
+  int rc;
+  if (tiekey) {
+    LAUNCH(ctx, k_tie_keys, grid_for(V, 256), 256, 0, V, tiekey, keys.p, order.p);
+    rc = dev_radix_sort_u64(ctx, keys.p, order.p, V, 64, err);
+    if (rc) return rc;
+  } else {
+    LAUNCH(ctx, k_iota, grid_for(V, 256), 256, 0, V, order.p);
+  }
+  unsigned long long *d_mn = (unsigned long long *)ctx->d_small + 12;
+  CUDA_TRY(cudaMemcpyAsync(d_mn, &kmin, 8, cudaMemcpyHostToDevice, st));
+  LAUNCH(ctx, k_size_keys, grid_for(V, 256, 1024), 256, 0, V, size, order.p, keys.p, d_mn + 1, d_mn + 2);
+  LAUNCH(ctx, k_sub_keys, grid_for(V, 256), 256, 0, V, keys.p, d_mn);
+  rc = dev_radix_sort_u64(ctx, keys.p, order.p, V, bits_for(kmax - kmin), err);
+  if (rc) return rc;
+  LAUNCH(ctx, k_rank, grid_for(V, 256), 256, 0, V, order.p, rank);
+  return MP_OK;
+}
+
 int placement_rank(mp_ctx *ctx, int64_t V, const int64_t *size, const int64_t *tiekey, int32_t *rank, mp_err *err) {
+  unsigned long long *mm = (unsigned long long *)ctx->d_small + 10;
+  int rc = placement_rank_keys(ctx, V, size, mm, err);
+  if (rc) return rc;
+  uint64_t h[2];
+  rc = dev_read_n(ctx, mm, h, 16, err);
+  if (rc) return rc;
+  return placement_rank_sort(ctx, V, size, tiekey, rank, h[0], h[1], err);
+}
+
+int placement_rank_legacy(mp_ctx *ctx, int64_t V, const int64_t *size, const int64_t *tiekey, int32_t *rank,
+                          mp_err *err) {
   StageTimer tm(ctx, MP_ST_PLACE_ORDER);
   cudaStream_t st = ctx->stream;
   DBuf<uint64_t> keys;
@@ -483,16 +549,17 @@ extern "C" int mp_plan_pool(mp_ctx *ctx, mp_dgraph *g, int32_t policy, int64_t *
   CUDA_TRY(cudaMemcpyAsync(d_fp, &lmin, 8, cudaMemcpyHostToDevice, st));
   LAUNCH(ctx, k_ready_init, grid_for(V, 256, 2048), 256, 0, V, g->pcnt.p, remaining.p, queue.p, ctr.p + 1,
          d_need);
-  uint64_t arena_need;
-  int rc = dev_read_n(ctx, d_need, &arena_need, 8, err);
-  if (rc) return rc;
+  // the conflict build bounded the long-row scratch by degree (no readback)
+  uint64_t arena_need = (uint64_t)g->arena_need;
+  int rc = MP_OK;
   delete tm;
+  static int per_sm_cached = 0;
   DBuf<int64_t> &off = g->offsets;
   CUDA_TRY(off.alloc(V, st));
   size_t smem = 0;
-  int per_sm = 0;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_place_async, PLACE_THREADS, smem));
-  if (per_sm < 1) per_sm = 1;
+  if (!per_sm_cached)
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_cached, k_place_async, PLACE_THREADS, smem));
+  int per_sm = per_sm_cached < 1 ? 1 : per_sm_cached;
   // all warps resident: spinning consumers must never starve producers
   int64_t warps_needed = V;
   int64_t nblocks = (int64_t)per_sm * ctx->num_sms;
