@@ -98,11 +98,9 @@ extern "C" int mp_trace_upload(mp_ctx *ctx, const mp_trace_in *in, mp_dtrace **o
     CUDA_TRY(t->index.alloc(n, st));
     CUDA_TRY(cudaMemcpyAsync(t->index.p, in->index, n * 8, cudaMemcpyHostToDevice, st));
   }
-  CUDA_TRY(t->blob.alloc(t->name_bytes, st));
-  CUDA_TRY(t->name_off.alloc((int64_t)in->nvars + 1, st));
-  if (t->name_bytes) CUDA_TRY(cudaMemcpyAsync(t->blob.p, in->name_blob, t->name_bytes, cudaMemcpyHostToDevice, st));
-  if (in->name_off)
-    CUDA_TRY(cudaMemcpyAsync(t->name_off.p, in->name_off, ((int64_t)in->nvars + 1) * 8, cudaMemcpyHostToDevice, st));
+  // Names stay on the host: ids are lexicographic ranks, so every device
+  // tie-break is an id compare (renamed instances only ever tie on alloc,
+  // which is unique), and candidate name ranks arrive with the candidates.
   // inputs are borrowed for the duration of the call only
   CUDA_TRY(cudaStreamSynchronize(st));
   *out = t;
@@ -174,12 +172,9 @@ extern "C" int mp_profile_upload(mp_ctx *ctx, const mp_profile_dims *dims, const
   UL(P->op_times.p, in->op_times, p * 8);
   UL(P->loads.p, in->loads, p * 8);
   UL(P->op_owner.p, in->op_owner, p * 4);
-  int64_t nb = name_off ? name_off[nnames] : 0;
+  (void)name_blob;
+  (void)name_off;
   P->nnames = nnames;
-  CUDA_TRY(P->blob.alloc(nb, st));
-  CUDA_TRY(P->name_off.alloc((int64_t)nnames + 1, st));
-  UL(P->blob.p, name_blob, nb);
-  UL(P->name_off.p, name_off, ((int64_t)nnames + 1) * 8);
 #undef UL
   CUDA_TRY(cudaStreamSynchronize(st));
   *out = P;

@@ -755,12 +755,7 @@ extern "C" int mp_extract(mp_ctx *ctx, mp_dtrace *t, int64_t start, int64_t end,
   P->d.peak_index = p ? fin[1] : 0;
   P->d.naccess = fin[2];
   memcpy(&P->d.duration_us, &fin[3], 8);
-  // the profile keeps its own copy of the name table
   P->nnames = t->nvars;
-  CUDA_TRY(P->blob.alloc(t->name_bytes, st));
-  CUDA_TRY(P->name_off.alloc((int64_t)t->nvars + 1, st));
-  if (t->name_bytes) CUDA_TRY(cudaMemcpyAsync(P->blob.p, t->blob.p, t->name_bytes, cudaMemcpyDeviceToDevice, st));
-  CUDA_TRY(cudaMemcpyAsync(P->name_off.p, t->name_off.p, ((int64_t)t->nvars + 1) * 8, cudaMemcpyDeviceToDevice, st));
   *out = P;
   return MP_OK;
 }

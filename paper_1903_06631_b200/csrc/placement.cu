@@ -39,6 +39,7 @@ struct PlaceArgs {
   int32_t *remaining;   // unplaced preds
   int32_t *queue;       // ready variables, v + 1 (0 = slot not yet published)
   int32_t *head, *tail;
+  int32_t *done;        // variables placed (flushed per queue claim)
   int policy;           // 0 first_fit, 1 best_fit
   IV *wscratch;         // 128 ranges per warp (packed-key fallback)
   IV *arena;            // long rows (> 128 preds) bump-allocate here
@@ -273,6 +274,34 @@ constexpr int PLACE_MIN_BLOCKS = 5;  // <= 48 registers: 40 resident warps per S
 
 
 
+// offset of one variable whose predecessors are all placed (warp-wide)
+__device__ __forceinline__ int64_t place_var(const PlaceArgs &a, int32_t v, int64_t gwarp, int64_t rb, int m,
+                                             int64_t need, int &lvl) {
+  const int lane = threadIdx.x & 31;
+  int64_t o = 0;
+  bool ok = true;
+  lvl = 1;
+  if (m == 0) o = 0;
+  else if (m <= 32) o = place_reg<1>(a, rb, m, need, lvl, ok);
+  else if (m <= 64) o = place_reg<2>(a, rb, m, need, lvl, ok);
+  else if (m <= 128) o = place_reg<4>(a, rb, m, need, lvl, ok);
+  else ok = false;
+  // long rows, or offsets too large to pack: sort (start, end) pairs in
+  // global scratch
+  if (!ok) {
+    IV *buf = a.wscratch + gwarp * 128;
+    if (m > 128) {
+      unsigned long long n2 = 64;
+      while (n2 < (unsigned long long)m) n2 <<= 1;
+      unsigned long long at = 0;
+      if (lane == 0) at = atomicAdd(a.arena_top, n2);
+      buf = a.arena + __shfl_sync(FULL_MASK, at, 0);
+    }
+    o = place_mem(a, buf, rb, m, need, lvl);
+  }
+  return o;
+}
+
 // Asynchronous dataflow placement: warps claim ready variables from a
 // queue in order; placing a variable decrements its successors' counters
 // and the last predecessor to finish publishes the successor.  No grid-wide
@@ -282,46 +311,42 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_MIN_BLOCKS) k_place_async
   int64_t gwarp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   long long fp = LLONG_MIN;
   int dmax = 0;
+  int32_t next = -1;     // a successor this warp made ready and kept
+  int local_done = 0;    // placements not yet added to the global count
   for (;;) {
-    int i = 0;
-    if (lane == 0) i = atomicAdd(a.head, 1);
-    i = __shfl_sync(FULL_MASK, i, 0);
-    if (i >= a.V) break;
-    int v1 = 0;
-    if (lane == 0) {
-      // acquire: the predecessors' offsets were released before this slot was published
-      const int32_t *q = a.queue + i;
-      for (;;) {
-        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v1) : "l"(q) : "memory");
-        if (v1) break;
-        __nanosleep(20);
+    int32_t v;
+    if (next >= 0) {
+      v = next;
+      next = -1;
+    } else {
+      int i = 0;
+      if (lane == 0) {
+        if (local_done) atomicAdd(a.done, local_done);
+        i = atomicAdd(a.head, 1);
       }
+      local_done = 0;
+      int v1 = 0;
+      if (lane == 0) {
+        // acquire: the predecessors' offsets were released before the slot
+        // was published; continuation means not every variable passes
+        // through the queue, so an empty slot ends the warp once all are placed
+        const int32_t *q = a.queue + (i < a.V ? i : 0);
+        for (;;) {
+          if (i < a.V) asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v1) : "l"(q) : "memory");
+          if (v1) break;
+          if (*(volatile int *)a.done >= a.V) { v1 = -1; break; }
+          __nanosleep(20);
+        }
+      }
+      v1 = __shfl_sync(FULL_MASK, v1, 0);
+      if (v1 < 0) break;
+      v = v1 - 1;
     }
-    int32_t v = __shfl_sync(FULL_MASK, v1, 0) - 1;
-    int64_t rb = a.row_off[v];
+    int64_t rb = a.row_off[v], re = a.row_off[v + 1];
     int m = a.pcnt[v];
     int64_t need = a.size[v];
-    int lvl = 1;
-    int64_t o = 0;
-    bool ok = true;
-    if (m == 0) o = 0;
-    else if (m <= 32) o = place_reg<1>(a, rb, m, need, lvl, ok);
-    else if (m <= 64) o = place_reg<2>(a, rb, m, need, lvl, ok);
-    else if (m <= 128) o = place_reg<4>(a, rb, m, need, lvl, ok);
-    else ok = false;
-    // long rows, or offsets too large to pack: sort (start, end) pairs in the
-    // warp's global scratch
-    if (!ok) {
-      IV *buf = a.wscratch + gwarp * 128;
-      if (m > 128) {
-        unsigned long long n2 = 64;
-        while (n2 < (unsigned long long)m) n2 <<= 1;
-        unsigned long long at = 0;
-        if (lane == 0) at = atomicAdd(a.arena_top, n2);
-        buf = a.arena + __shfl_sync(FULL_MASK, at, 0);
-      }
-      o = place_mem(a, buf, rb, m, need, lvl);
-    }
+    int lvl;
+    int64_t o = place_var(a, v, gwarp, rb, m, need, lvl);
     if (lane == 0) {
       a.off[v] = o;
       a.level[v] = lvl;
@@ -329,23 +354,27 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_MIN_BLOCKS) k_place_async
       if (lvl > dmax) dmax = lvl;
       __threadfence();  // offsets visible before any successor counter drops
     }
+    local_done++;
     __syncwarp();
-    int64_t deg = a.row_off[v + 1] - rb;
-    for (int64_t k = m + lane; k - lane < deg; k += 32) {
+    for (int64_t k = rb + m + lane; k - lane < re; k += 32) {
       bool ready = false;
       int32_t j = 0;
-      if (k < deg) {
-        j = a.col[rb + k];
+      if (k < re) {
+        j = a.col[k];
         ready = atomicSub(&a.remaining[j], 1) == 1;
+        if (ready) __threadfence();  // acquire the other predecessors' offsets
       }
-      // publish the newly ready successors with one tail bump per chunk
       unsigned bal = __ballot_sync(FULL_MASK, ready);
+      if (bal && next < 0) {
+        // keep the first newly ready successor; publish the rest
+        int keep = __ffs(bal) - 1;
+        next = __shfl_sync(FULL_MASK, j, keep);
+        bal &= bal - 1;
+        if (lane == keep) ready = false;
+      }
       if (bal) {
         int base = 0;
-        if (lane == __ffs(bal) - 1) {
-          __threadfence();
-          base = atomicAdd(a.tail, __popc(bal));
-        }
+        if (lane == __ffs(bal) - 1) base = atomicAdd(a.tail, __popc(bal));
         base = __shfl_sync(FULL_MASK, base, __ffs(bal) - 1);
         if (ready) {
           int32_t *q = a.queue + base + __popc(bal & lanemask_lt());
@@ -542,7 +571,7 @@ extern "C" int mp_plan_pool(mp_ctx *ctx, mp_dgraph *g, int32_t policy, int64_t *
   CUDA_TRY(ctr.alloc(16, st));
   CUDA_TRY(cudaMemsetAsync(queue.p, 0, V * 4, st));
   CUDA_TRY(cudaMemsetAsync(ctr.p, 0, 64, st));
-  // ctr: [0] head [1] tail [2] - [3] depth [4..5] footprint [6..7] arena need [8..9] arena top
+  // ctr: [0] head [1] tail [2] done [3] depth [4..5] footprint [6..7] arena need [8..9] arena top
   long long *d_fp = (long long *)(ctr.p + 4);
   unsigned long long *d_need = (unsigned long long *)(ctr.p + 6);
   const long long lmin = LLONG_MIN;
@@ -571,7 +600,7 @@ extern "C" int mp_plan_pool(mp_ctx *ctx, mp_dgraph *g, int32_t policy, int64_t *
   CUDA_TRY(wscratch.alloc(128 * nblocks * (PLACE_THREADS / 32), st));
   CUDA_TRY(arena.alloc((int64_t)arena_need, st));
   PlaceArgs a{V, g->row_off.p, g->col.p, g->pcnt.p, g->size.p, off.p, level.p, remaining.p, queue.p,
-              ctr.p, ctr.p + 1, policy, wscratch.p, arena.p, (unsigned long long *)(ctr.p + 8), d_fp, ctr.p + 3};
+              ctr.p, ctr.p + 1, ctr.p + 2, policy, wscratch.p, arena.p, (unsigned long long *)(ctr.p + 8), d_fp, ctr.p + 3};
   {
     StageTimer ptm(ctx, MP_ST_PLACE);
     LAUNCH(ctx, k_place_async, (unsigned)nblocks, PLACE_THREADS, smem, a);
