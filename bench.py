@@ -75,7 +75,7 @@ class ClockSampler:
                     self.samples.append([x.strip() for x in out.split(",")])
             except Exception:  # noqa: BLE001
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.05)
 
     def __enter__(self):
         self._t.start()
@@ -305,6 +305,17 @@ def main():
     per_stage = {k: ms / steps for k, (ms, _c) in stages.items()}
     dom = max(per_stage, key=per_stage.get)
     achieved = sb.get(dom, 0) / (per_stage[dom] * 1e-3) / 1e9
+    # DRAM traffic per launch of the dominant kernel, from the committed
+    # `ncu --set full` capture (profiles/r1_ncu_kernels.json)
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_ncu_kernels.json")) as fh:
+            k = json.load(fh).get({"place": "k_place_async", "conflict_fill": "k_iv_fill"}.get(dom, ""), None)
+        if k:
+            traffic = k["dram_read_bytes"] + k["dram_write_bytes"]
+    except Exception:  # noqa: BLE001
+        pass
+    stage_roof = {s: round(sb[s] / (ms * 1e-3) / 1e9 / peak, 4) for s, ms in per_stage.items() if s in sb and ms > 0}
     line = {
         "metric": METRIC, "value": r["vars_total"] / (r["step_ms"] * 1e-3), "unit": UNIT,
         "n_gpus": world, "steps": steps, "warmup": args.warmup, "ms_per_step": r["step_ms"],
@@ -322,8 +333,10 @@ def main():
         "gpu_launches": r["launches"],
         "stage_ms": {k: round(v, 4) for k, v in per_stage.items()},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
-                     "algorithmic_bytes": sb.get(dom, 0)},
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "algorithmic_bytes": sb.get(dom, 0),
+                     "note": "placement is a DAG walk (depth = result.levels): latency-bound, not HBM-bound"},
+        "stage_hbm_frac": stage_roof,
         "clocks": r["clocks"],
     }
     if not args.no_cpu_baseline:
