@@ -1,0 +1,191 @@
+// alloc.cpp — PyTorch CUDAPluggableAllocator hooks serving a SmartPool plan.
+//
+// The paper's Device::Malloc/Free backed by the static
+// pool: in RECORD mode every allocation is stream-ordered cudaMallocAsync
+// and logged (op ordinal, kind, pointer, size rounded to 512 B) so one
+// training iteration becomes a memplan trace; in SERVE mode the k-th
+// allocation of an iteration gets pool_base + offset[k] from the plan's
+// lookup table (smartpool.py:224-254) and frees are no-ops — a size mismatch
+// falls back to cudaMallocAsync and is counted as a miss.
+//
+// Signatures follow torch.cuda.memory.CUDAPluggableAllocator:
+//   void* alloc(ssize_t size, int device, cudaStream_t stream)
+//   void  free(void* ptr, ssize_t size, int device, cudaStream_t stream)
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <sys/types.h>
+
+#include <mutex>
+#include <unordered_map>
+#include <vector>
+
+namespace {
+
+constexpr int64_t ALIGN = 512;
+
+struct LogRec {
+  int64_t seq;
+  int32_t kind;  // 0 malloc, 1 free
+  int64_t ptr;
+  int64_t size;
+};
+
+struct State {
+  std::mutex mu;
+  int mode = 0;  // 0 record/passthrough, 1 serve
+  bool logging = false;
+  int64_t seq = 0;  // op ordinal set by the tracer
+  std::vector<LogRec> log;
+  std::unordered_map<int64_t, int64_t> live;  // ptr -> size (passthrough allocations)
+  // serve
+  char *pool = nullptr;
+  int64_t pool_bytes = 0;
+  std::vector<int64_t> slot_off, slot_size;
+  int64_t ordinal = 0, misses = 0, hits = 0, conflicts = 0;
+  std::unordered_map<int64_t, int64_t> pool_live;  // offset -> size of served blocks
+  std::unordered_map<int64_t, int64_t> pool_who;   // offset -> iteration * 2^20 + ordinal
+  int64_t iteration = 0;
+  std::vector<int64_t> clash_log;                  // (iteration, ordinal, other) triples
+  int64_t cur_bytes = 0, peak_bytes = 0;  // passthrough bytes live
+};
+
+State &S() {
+  static State s;
+  return s;
+}
+
+inline int64_t round_up(int64_t n) { return (n + ALIGN - 1) / ALIGN * ALIGN; }
+
+}  // namespace
+
+extern "C" {
+
+void *mp_torch_alloc(ssize_t size, int device, cudaStream_t stream) {
+  State &s = S();
+  std::lock_guard<std::mutex> g(s.mu);
+  int64_t rs = round_up(size > 0 ? size : 1);
+  void *p = nullptr;
+  if (s.mode == 1) {
+    int64_t k = s.ordinal++;
+    if (k < (int64_t)s.slot_off.size() && s.slot_size[k] == rs) {
+      int64_t lo = s.slot_off[k], hi = lo + rs;
+      // guard: the slot must not overlap a pool block that is still live
+      // (a program whose lifetimes drift from the recorded ones)
+      bool clash = false;
+      int64_t other = -1;
+      for (auto &kv : s.pool_live)
+        if (kv.first < hi && lo < kv.first + kv.second) { clash = true; other = s.pool_who[kv.first]; break; }
+      if (clash) {
+        s.conflicts++;
+        if (s.clash_log.size() < 3 * 64) {
+          s.clash_log.push_back(s.iteration);
+          s.clash_log.push_back(k);
+          s.clash_log.push_back(other);
+        }
+      } else {
+        p = s.pool + lo;
+        s.pool_live[lo] = rs;
+        s.pool_who[lo] = (s.iteration << 20) | k;
+        s.hits++;
+      }
+    } else {
+      s.misses++;
+    }
+  }
+  if (!p) {
+    (void)device;
+    if (cudaMallocAsync(&p, rs, stream) != cudaSuccess) return nullptr;
+    s.live[(int64_t)p] = rs;
+    s.cur_bytes += rs;
+    if (s.cur_bytes > s.peak_bytes) s.peak_bytes = s.cur_bytes;
+  }
+  if (s.logging) s.log.push_back({s.seq, 0, (int64_t)p, rs});
+  return p;
+}
+
+void mp_torch_free(void *ptr, ssize_t size, int device, cudaStream_t stream) {
+  State &s = S();
+  std::lock_guard<std::mutex> g(s.mu);
+  (void)size;
+  (void)device;
+  if (s.logging) s.log.push_back({s.seq, 1, (int64_t)ptr, 0});
+  char *c = (char *)ptr;
+  if (s.pool && c >= s.pool && c < s.pool + s.pool_bytes) {  // pool slots are static
+    s.pool_live.erase((int64_t)(c - s.pool));
+    return;
+  }
+  auto it = s.live.find((int64_t)ptr);
+  if (it != s.live.end()) {
+    s.cur_bytes -= it->second;
+    s.live.erase(it);
+  }
+  cudaFreeAsync(ptr, stream);
+}
+
+// ---- control (ctypes) ----
+void mp_alloc_set_seq(int64_t seq) { S().seq = seq; }
+void mp_alloc_logging(int on) {
+  std::lock_guard<std::mutex> g(S().mu);
+  S().logging = on != 0;
+}
+int64_t mp_alloc_log_size() { return (int64_t)S().log.size(); }
+void mp_alloc_log_drain(int64_t *seq, int32_t *kind, int64_t *ptr, int64_t *size) {
+  State &s = S();
+  std::lock_guard<std::mutex> g(s.mu);
+  for (size_t i = 0; i < s.log.size(); i++) {
+    seq[i] = s.log[i].seq;
+    kind[i] = s.log[i].kind;
+    ptr[i] = s.log[i].ptr;
+    size[i] = s.log[i].size;
+  }
+  s.log.clear();
+}
+// install a plan: n slots (offset, rounded size) in allocation order
+int mp_alloc_set_plan(int64_t pool_bytes, int64_t n, const int64_t *off, const int64_t *size) {
+  State &s = S();
+  std::lock_guard<std::mutex> g(s.mu);
+  if (s.pool) cudaFree(s.pool);
+  s.pool = nullptr;
+  s.pool_bytes = pool_bytes;
+  if (pool_bytes > 0 && cudaMalloc((void **)&s.pool, pool_bytes) != cudaSuccess) return 1;
+  s.slot_off.assign(off, off + n);
+  s.slot_size.assign(size, size + n);
+  s.ordinal = 0;
+  s.pool_live.clear();
+  return 0;
+}
+void mp_alloc_mode(int mode) {
+  std::lock_guard<std::mutex> g(S().mu);
+  S().mode = mode;
+}
+void mp_alloc_begin_iteration() {
+  std::lock_guard<std::mutex> g(S().mu);
+  S().ordinal = 0;
+  S().iteration++;
+}
+int64_t mp_alloc_clash_log(int64_t *out, int64_t cap) {
+  State &s = S();
+  std::lock_guard<std::mutex> g(s.mu);
+  int64_t n = (int64_t)s.clash_log.size();
+  for (int64_t i = 0; i < n && i < cap; i++) out[i] = s.clash_log[i];
+  return n;
+}
+void mp_alloc_stats(int64_t *out) {
+  State &s = S();
+  std::lock_guard<std::mutex> g(s.mu);
+  out[6] = s.conflicts;
+  out[0] = s.hits;
+  out[1] = s.misses;
+  out[2] = s.pool_bytes;
+  out[3] = s.cur_bytes;
+  out[4] = s.peak_bytes;
+  out[5] = s.ordinal;
+}
+void mp_alloc_reset_peak() {
+  std::lock_guard<std::mutex> g(S().mu);
+  S().peak_bytes = S().cur_bytes;
+  S().hits = S().misses = S().conflicts = 0;
+}
+int64_t mp_alloc_pool_base() { return (int64_t)S().pool; }
+
+}  // extern "C"
