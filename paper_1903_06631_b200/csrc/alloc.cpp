@@ -47,6 +47,14 @@ struct State {
   int64_t iteration = 0;
   std::vector<int64_t> clash_log;                  // (iteration, ordinal, other) triples
   int64_t cur_bytes = 0, peak_bytes = 0;  // passthrough bytes live
+  // address ranges of pools replaced by a later plan: blocks served from
+  // them may still be referenced (e.g. gradients freed by the next
+  // iteration's zero_grad); their frees are no-ops
+  std::vector<std::pair<int64_t, int64_t>> retired;
+  // offsets of swapped-out blocks: PyTorch still holds their pointers, so
+  // no other block may be served at the same address while they are out
+  std::unordered_map<int64_t, int64_t> swapped_out;
+  int64_t aliases = 0;
 };
 
 State &S() {
@@ -71,9 +79,11 @@ void *mp_torch_alloc(ssize_t size, int device, cudaStream_t stream) {
       int64_t lo = s.slot_off[k], hi = lo + rs;
       // guard: the slot must not overlap a pool block that is still live
       // (a program whose lifetimes drift from the recorded ones)
-      bool clash = false;
+      bool clash = s.swapped_out.count(lo) != 0;
       int64_t other = -1;
-      for (auto &kv : s.pool_live)
+      if (clash) s.aliases++;
+      if (!clash)
+        for (auto &kv : s.pool_live)
         if (kv.first < hi && lo < kv.first + kv.second) { clash = true; other = s.pool_who[kv.first]; break; }
       if (clash) {
         s.conflicts++;
@@ -118,6 +128,9 @@ void mp_torch_free(void *ptr, ssize_t size, int device, cudaStream_t stream) {
   if (it != s.live.end()) {
     s.cur_bytes -= it->second;
     s.live.erase(it);
+  } else {
+    for (auto &r : s.retired)
+      if ((int64_t)c >= r.first && (int64_t)c < r.first + r.second) return;
   }
   cudaFreeAsync(ptr, stream);
 }
@@ -144,7 +157,10 @@ void mp_alloc_log_drain(int64_t *seq, int32_t *kind, int64_t *ptr, int64_t *size
 int mp_alloc_set_plan(int64_t pool_bytes, int64_t n, const int64_t *off, const int64_t *size) {
   State &s = S();
   std::lock_guard<std::mutex> g(s.mu);
-  if (s.pool) cudaFree(s.pool);
+  if (s.pool) {
+    cudaFree(s.pool);
+    s.retired.push_back({(int64_t)s.pool, s.pool_bytes});
+  }
   s.pool = nullptr;
   s.pool_bytes = pool_bytes;
   if (pool_bytes > 0 && cudaMalloc((void **)&s.pool, pool_bytes) != cudaSuccess) return 1;
@@ -152,6 +168,7 @@ int mp_alloc_set_plan(int64_t pool_bytes, int64_t n, const int64_t *off, const i
   s.slot_size.assign(size, size + n);
   s.ordinal = 0;
   s.pool_live.clear();
+  s.swapped_out.clear();
   return 0;
 }
 void mp_alloc_mode(int mode) {
@@ -180,12 +197,44 @@ void mp_alloc_stats(int64_t *out) {
   out[3] = s.cur_bytes;
   out[4] = s.peak_bytes;
   out[5] = s.ordinal;
+  out[7] = (int64_t)s.pool_live.size();
+  out[8] = s.aliases;
+}
+// swap executor: a swapped-out block's bytes are free for the planned
+// co-tenants until it is swapped back in
+void mp_alloc_pool_release(int64_t off) {
+  std::lock_guard<std::mutex> g(S().mu);
+  auto it = S().pool_live.find(off);
+  if (it != S().pool_live.end()) {
+    S().swapped_out[off] = it->second;
+    S().pool_live.erase(it);
+  }
+}
+// returns 0, or 1 if a live block still overlaps [off, off+size)
+int mp_alloc_pool_reclaim(int64_t off, int64_t size) {
+  State &s = S();
+  std::lock_guard<std::mutex> g(s.mu);
+  for (auto &kv : s.pool_live)
+    if (kv.first < off + size && off < kv.first + kv.second) {
+      s.conflicts++;
+      return 1;
+    }
+  s.swapped_out.erase(off);
+  s.pool_live[off] = size;
+  return 0;
 }
 void mp_alloc_reset_peak() {
   std::lock_guard<std::mutex> g(S().mu);
   S().peak_bytes = S().cur_bytes;
-  S().hits = S().misses = S().conflicts = 0;
+  S().hits = S().misses = S().conflicts = S().aliases = 0;
 }
 int64_t mp_alloc_pool_base() { return (int64_t)S().pool; }
+int mp_alloc_peek_error() { return (int)cudaPeekAtLastError(); }
+// swap executor copies: d2h=1 copies dev -> host, else host -> dev
+int mp_alloc_copy_async(void *dev, void *host, int64_t n, int d2h, cudaStream_t stream) {
+  cudaError_t e = d2h ? cudaMemcpyAsync(host, dev, n, cudaMemcpyDeviceToHost, stream)
+                      : cudaMemcpyAsync(dev, host, n, cudaMemcpyHostToDevice, stream);
+  return (int)e;
+}
 
 }  // extern "C"

@@ -49,27 +49,36 @@ def install():
 
 
 def stats() -> dict:
-    out = (C.c_int64 * 8)()
+    out = (C.c_int64 * 9)()
     ctl().mp_alloc_stats(out)
     return {"hits": out[0], "misses": out[1], "pool_bytes": out[2], "outside_live_bytes": out[3],
-            "outside_peak_bytes": out[4], "ordinal": out[5], "conflicts": out[6]}
+            "outside_peak_bytes": out[4], "ordinal": out[5], "conflicts": out[6], "pool_live_blocks": out[7],
+            "swap_alias_fallbacks": out[8]}
 
 
 class Tracer:
     """Record allocations + per-op reads/writes of the code run inside it."""
 
-    def __init__(self, sync_times: bool = True, dispatch: bool = True):
+    def __init__(self, sync_times: bool = True, dispatch: bool = True, device_times: bool = False):
         """dispatch=False records allocations only (no per-op reads/writes,
         timestamps = event order): the program runs exactly as when served,
         so the recorded lifetimes are the served ones (enough for pool
-        planning; swap planning needs the accesses and op times)."""
+        planning; swap planning needs the accesses and op times).
+        device_times=True stamps each op with a CUDA event recorded before
+        it instead of synchronising: op times are the device timeline of an
+        unsynchronised run (what a swap plan must hide transfers behind)."""
         from torch.utils._python_dispatch import TorchDispatchMode
         tracer = self
-        self.sync_times = sync_times
+        self.sync_times = sync_times and not device_times
+        self.device_times = device_times
+        self._events = []  # (seq, cuda event) when device_times
         self.dispatch = dispatch
         self.ops = []  # (seq, t_us, [read ptrs], [write ptrs])
+        self.spans = {}  # seq -> allocator-log range [lo, hi) recorded inside the op
         self.seq = 0
         self.t0 = None
+        self.hook = None  # executor callbacks around each op (swapexec)
+        self.record = True
 
         class Mode(TorchDispatchMode):
             def __torch_dispatch__(self, func, types, args=(), kwargs=None):
@@ -99,10 +108,20 @@ class Tracer:
         if self.sync_times:
             torch.cuda.synchronize()
         t = int((time.perf_counter() - self.t0) * 1e6)
+        if self.device_times:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            self._events.append((self.seq, ev))
         reads = []
         self._ptrs(args, reads)
         self._ptrs(kwargs, reads)
+        lo = int(ctl().mp_alloc_log_size())
+        if self.hook is not None:
+            self.hook.before(self.seq)
         out = func(*args, **kwargs)
+        if self.hook is not None:
+            self.hook.after(self.seq)
+        self.spans[self.seq] = (lo, int(ctl().mp_alloc_log_size()))
         writes = []
         self._ptrs(out, writes)
         # in-place / out= ops write their mutated inputs too
@@ -125,9 +144,15 @@ class Tracer:
         if self.sync_times:
             torch.cuda.synchronize()
         t = int((time.perf_counter() - self.t0) * 1e6)
+        if self.device_times:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            self._events.append((self.seq, ev))
         if not self.dispatch:
             t = self.seq
         self.marks.append((self.seq, t))
+        n = int(ctl().mp_alloc_log_size())
+        self.spans[self.seq] = (n, n)
         self.ops.append((self.seq, t, [], []))
 
     def __enter__(self):
@@ -135,6 +160,9 @@ class Tracer:
         self.marks = []
         torch.cuda.synchronize()
         self.t0 = time.perf_counter()
+        if self.device_times:
+            self._ev0 = torch.cuda.Event(enable_timing=True)
+            self._ev0.record()
         self._drain()
         ctl().mp_alloc_set_seq(self.seq)
         ctl().mp_alloc_logging(1)
@@ -149,6 +177,11 @@ class Tracer:
         torch.cuda.synchronize()
         ctl().mp_alloc_logging(0)
         self.alloc_log = self._drain()
+        if self.device_times:
+            t_of = {s: int(self._ev0.elapsed_time(ev) * 1000.0) for s, ev in self._events}
+            self.ops = [(s, t_of.get(s, t), r, w) for s, t, r, w in self.ops]
+            self.marks = [(s, t_of.get(s, t)) for s, t in self.marks]
+            self._events = []
 
     @staticmethod
     def _drain():
@@ -158,13 +191,12 @@ class Tracer:
         return [c[:n] for c in cols]
 
     def trace(self):
-        """Merge allocator and dispatch logs into TraceArrays (events per op:
-        reads, mallocs, writes, frees)."""
+        """Merge allocator and dispatch logs into TraceArrays.  Dispatch
+        mode: per op its reads, the allocator records made inside it (log
+        order), its writes; ``self.event_seq[i]`` = the op ordinal event i
+        belongs to (what a swap executor keys its actions on)."""
         from .trace import KIND_CODE, TraceArrays
         seq, kind, ptr, size = self.alloc_log
-        by_seq: dict[int, list] = {}
-        for s, k, p, z in zip(seq.tolist(), kind.tolist(), ptr.tolist(), size.tolist()):
-            by_seq.setdefault(s, []).append((k, p, z))
         live: dict[int, str] = {}
         counter = 0
         kinds, names, sizes, times = [], [], [], []
@@ -197,38 +229,57 @@ class Tracer:
                     emit(kk, MARK_NAME, 1 if kk == "malloc" else 0, 0)
             return TraceArrays.from_columns(np.array(kinds, np.uint8), names, np.array(sizes, np.int64),
                                             np.arange(len(kinds), dtype=np.int64))
-        t_of = {s: t for s, t, _r, _w in self.ops}
-        t_last = 0
-        # allocator records before the first op (seq 0) and between ops
-        seqs = sorted(set(t_of) | set(by_seq))
-        ops_by_seq = {s: (r, w) for s, _t, r, w in self.ops}
+        # dispatch mode: per op, its reads, the allocator records made inside
+        # it (log order), its writes; records between ops follow in log order
+        nlog = len(seq)
+        recs = list(zip(kind.tolist(), ptr.tolist(), size.tolist()))
         mark_seqs = {s for s, _t in self.marks}
-        for s in seqs:
-            t = t_of.get(s, t_last)
-            t_last = t
-            if s in mark_seqs:
-                for k in ("malloc", "write", "read", "free"):
-                    emit(k, MARK_NAME, 1 if k == "malloc" else 0, t)
-            reads, writes = ops_by_seq.get(s, ([], []))
-            recs = by_seq.get(s, [])
-            for p in dict.fromkeys(reads):
-                if p in live:
-                    emit("read", live[p], 0, t)
-            for k, p, z in recs:
+        pos = 0
+        self.event_seq = []
+        self._event_where = []  # 0: at/inside the op, 1: between it and the next
+
+        def run_recs(upto, t, s, where=0):
+            nonlocal pos, counter
+            while pos < upto:
+                k, p, z = recs[pos]
+                pos += 1
                 if k == 0:
-                    if p in live:  # the pointer was reused without a logged free
+                    if p in live:
                         emit("free", live.pop(p), 0, t)
+                        self.event_seq.append(s)
+                        self._event_where.append(where)
                     counter += 1
                     live[p] = f"a{counter:07d}"
                     emit("malloc", live[p], z, t)
+                    self.event_seq.append(s)
+                    self._event_where.append(where)
+                elif p in live:
+                    emit("free", live.pop(p), 0, t)
+                    self.event_seq.append(s)
+                    self._event_where.append(where)
+        t_prev = 0
+        for s, t, reads, writes in self.ops:
+            lo, hi = self.spans[s]
+            run_recs(lo, t_prev, s - 1, 1)   # records between the previous op and this one
+            if s in mark_seqs:
+                for k in ("malloc", "write", "read", "free"):
+                    emit(k, MARK_NAME, 1 if k == "malloc" else 0, t)
+                    self.event_seq.append(s)
+                    self._event_where.append(0)
+                continue
+            for p in dict.fromkeys(reads):
+                if p in live:
+                    emit("read", live[p], 0, t)
+                    self.event_seq.append(s)
+                    self._event_where.append(0)
+            run_recs(hi, t, s)
             for p in dict.fromkeys(writes):
                 if p in live:
                     emit("write", live[p], 0, t)
-            for k, p, z in recs:
-                if k == 1 and p in live:
-                    emit("free", live.pop(p), 0, t)
-        if not self.dispatch:
-            times = list(range(len(kinds)))
+                    self.event_seq.append(s)
+                    self._event_where.append(0)
+            t_prev = t
+        run_recs(nlog, t_prev, self.seq, 1)
         return TraceArrays.from_columns(np.array(kinds, np.uint8), names, np.array(sizes, np.int64),
                                         np.array(times, np.int64))
 
