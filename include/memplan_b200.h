@@ -153,6 +153,7 @@ enum {
   MP_ST_PLACE,          /* wavefront placement kernel */
   MP_ST_FOOTPRINT,
   MP_ST_SWAP,           /* swap planning kernels */
+  MP_ST_SWEEP,          /* batched sweep: upload, one-CTA-per-trace kernel, download */
   MP_NSTAGES = 16
 };
 int mp_ctx_set_timing(mp_ctx *ctx, int on);
@@ -288,6 +289,90 @@ int mp_swap_simulate(mp_ctx *ctx, mp_dprofile *p, const mp_cands_io *c, const in
 /* CPython-3.12 compatible standardize (autoswap.py:228-238): Neumaier
  * sum() and libm pow — host code, since device pow differs from glibc's */
 int mp_standardize(const double *x, int64_t n, double *out);
+
+/* ---------------------------------------------------------------------- */
+/* Batched sweep (BASELINE configs[4]): many independent traces in one      */
+/* launch, one CTA per trace.  Each trace runs what the reference's         */
+/* estimators do for it (estimators.py:20-130): validate_trace ->            */
+/* detect_iteration -> extract_lifetimes -> build_conflict_graph +          */
+/* plan_pool -> filter_candidates -> compute_load_min -> the SWDOA greedy,  */
+/* then per budget SwapPlanner(limit, score="swdoa").fit: the limit checks,  */
+/* select_by_swdoa (the prefix of the greedy order), build_schedule and      */
+/* simulate.  Budgets are fractions of each trace's own peak:               */
+/* limit_bytes = int(peak_bytes * frac).                                    */
+
+#define MP_SWEEP_MAX_BUDGETS 8
+
+typedef struct mp_sweep_params {
+  int32_t policy;      /* plan_pool policy: 0 first_fit, 1 best_fit */
+  int32_t nbudget;     /* 0 .. MP_SWEEP_MAX_BUDGETS */
+  int32_t max_rounds;  /* simulate(max_rounds=...) (swapsim.py:350) */
+  int32_t validate;    /* 1: validate_trace first (IterationAnalyzer.fit) */
+  int64_t threshold;   /* filter_candidates threshold_bytes */
+  double bw, lat;      /* TransferModel(bandwidth_bytes_per_s, latency_us) */
+  double budget_frac[MP_SWEEP_MAX_BUDGETS];
+} mp_sweep_params;
+
+/* traces concatenated column-wise; var ids are trace-local lexicographic
+ * ranks of that trace's names */
+typedef struct mp_sweep_in {
+  int64_t ntraces;
+  const int64_t *ev_off;   /* [ntraces + 1] */
+  const uint8_t *kind;
+  const int32_t *var;
+  const int64_t *size;
+  const int64_t *t_us;
+  const int64_t *var_off;  /* [ntraces + 1]: trace t owns name ids var_off[t] .. var_off[t+1] */
+  const uint8_t *name_blob;
+  const int64_t *name_off; /* [var_off[ntraces] + 1] */
+} mp_sweep_in;
+
+/* per-trace result; status is MP_OK or the first failing stage's code
+ * (MP_E_INVARIANT: err_index = event position / window op, err_code = MP_V_*;
+ * MP_E_PERIOD_NOT_FOUND; MP_E_NOMEM when a trace outgrows the scratch) */
+typedef struct mp_sweep_trace {
+  int32_t status, err_code;
+  int64_t err_index;
+  int64_t period, nvars, ncarry, naccess;
+  int64_t peak_bytes, peak_index;
+  double duration_us;
+  int64_t footprint_bytes;
+  int64_t edges;     /* undirected conflict edges (ConflictGraph.adj) */
+  int64_t ncand;     /* filter_candidates */
+  int64_t load_min;  /* compute_load_min */
+} mp_sweep_trace;
+
+/* per (trace, budget) result of SwapPlanner.fit; status MP_OK,
+ * MP_E_VALUE (limit <= 0), MP_E_LIMIT_UNREACHABLE (err_aux = achievable),
+ * MP_E_SWAP_DEADLOCK (err_index = absolute op index) or MP_E_SIM_INDEXERROR */
+typedef struct mp_sweep_budget {
+  int64_t limit_bytes;
+  int32_t status, rounds;
+  int64_t nsel;            /* selection = the first nsel greedy picks */
+  int64_t selected_bytes;
+  int64_t err_index, err_aux;
+  double overhead_us;      /* SimulationResult.overhead_us */
+  int64_t achieved_peak_bytes; /* LOAD'' peak */
+  int64_t planned_peak_bytes;  /* LOAD' peak */
+} mp_sweep_budget;
+
+typedef struct mp_dsweep mp_dsweep; /* device-resident batch */
+
+/* copy a batch to the device (stream-ordered on ctx) */
+int mp_sweep_upload(mp_ctx *ctx, const mp_sweep_in *in, mp_dsweep **out, mp_err *err);
+int mp_sweep_free(mp_dsweep *s);
+/* run the sweep on the device; results stay in HBM until downloaded */
+int mp_sweep_run(mp_ctx *ctx, mp_dsweep *s, const mp_sweep_params *prm, mp_err *err);
+/* copy results out: traces[ntraces], budgets[ntraces * nbudget];
+ * offsets / cand_order are laid out like the events (trace t's rows start
+ * at ev_off[t]): plan_pool offsets in profile variable order, and the SWDOA
+ * greedy order as profile variable indices.  Any pointer may be NULL. */
+int mp_sweep_download(mp_ctx *ctx, mp_dsweep *s, mp_sweep_trace *traces, mp_sweep_budget *budgets,
+                      int64_t *offsets, int32_t *cand_order, mp_err *err);
+/* diagnostics: per-trace clock64() at 8 phase marks of the sweep kernel
+ * (start, extract, plan, candidates, greedy, simulate prep, budgets, end) */
+int mp_sweep_set_profile(mp_ctx *ctx, mp_dsweep *s, int on, mp_err *err);
+int mp_sweep_profile_download(mp_ctx *ctx, mp_dsweep *s, long long *out /* [ntraces * 8] */, mp_err *err);
 
 #ifdef __cplusplus
 }

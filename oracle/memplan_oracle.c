@@ -1184,3 +1184,125 @@ int orc_simulate(const mp_profile_dims *d, const mp_profile_out *P, int64_t wind
   free(R.in_done); free(R.in_has); free(R.out_trigger); free(R.in_wait); free(R.actual);
   return rc;
 }
+
+/* ---------------------------------------------------------------------- */
+/* one sweep unit — what the estimators run for a trace (estimators.py:20-130):
+ * validate_trace, detect_iteration, extract_lifetimes, build_conflict_graph +
+ * plan_pool, filter_candidates, compute_load_min, then per budget
+ * SwapPlanner(limit_bytes=int(peak * frac), score="swdoa").fit: the limit
+ * checks (validation.py:32-34, estimators.py:98-100), select_by_score
+ * (autoswap.py:285-301 -> select_by_swdoa, rerun per budget as the reference
+ * does), build_schedule and simulate.  Records mirror mp_sweep_trace /
+ * mp_sweep_budget; offsets and cand_order are sized to the trace's events. */
+
+int orc_sweep_unit(const mp_trace_in *t, const mp_sweep_params *prm, mp_sweep_trace *rec,
+                   mp_sweep_budget *brec, int64_t *offsets, int32_t *cand_order) {
+  mp_err err;
+  memset(rec, 0, sizeof *rec);
+  for (int b = 0; b < prm->nbudget; b++) memset(&brec[b], 0, sizeof brec[b]);
+  int rc = MP_OK;
+  if (prm->validate) rc = orc_validate(t, &err);
+  if (rc == MP_OK) {
+    int64_t p;
+    rc = orc_detect(t, &p, &err);
+    if (rc == MP_OK) rec->period = p;
+  }
+  orc_profile *P = NULL;
+  if (rc == MP_OK) rc = orc_extract(t, t->n - rec->period, t->n, &P, &err);
+  if (rc != MP_OK) {
+    rec->status = rc;
+    rec->err_code = rc == MP_E_INVARIANT ? (int32_t)err.aux0 : 0;
+    rec->err_index = err.index;
+    for (int b = 0; b < prm->nbudget; b++) brec[b].status = rc;
+    return rc;
+  }
+  mp_profile_dims d = P->d;
+  int64_t V = d.nvars, p = d.period;
+  rec->nvars = V; rec->ncarry = d.ncarry; rec->naccess = d.naccess;
+  rec->peak_bytes = d.peak_bytes; rec->peak_index = d.peak_index; rec->duration_us = d.duration_us;
+  mp_profile_out po = {P->base, P->size, P->alloc, P->free_, P->nseg, P->seg, P->flags, P->acc_off,
+                       P->acc_index, P->acc_kind, P->acc_next, P->op_times, P->loads, P->op_owner};
+  orc_names names = {t->name_blob, t->name_off};
+  /* build_conflict_graph + plan_pool */
+  int64_t *seg_off = malloc((size_t)(V + 1) * 8);
+  int32_t *lo = malloc((size_t)(2 * V + 1) * 4), *hi = malloc((size_t)(2 * V + 1) * 4);
+  int64_t *alloc64 = malloc((size_t)(V + 1) * 8);
+  int32_t *ralloc = malloc((size_t)(V + 1) * 4);
+  int64_t ns = 0;
+  for (int64_t i = 0; i < V; i++) {
+    seg_off[i] = ns;
+    for (int s = 0; s < P->nseg[i]; s++) { lo[ns] = P->seg[4 * i + 2 * s]; hi[ns] = P->seg[4 * i + 2 * s + 1]; ns++; }
+    alloc64[i] = P->alloc[i];
+    ralloc[i] = (P->flags[i] & MP_F_RENAMED) ? P->alloc[i] : -1;
+  }
+  seg_off[V] = ns;
+  orc_graph *g;
+  orc_conflict((int32_t)V, seg_off, lo, hi, &g);
+  rec->edges = orc_graph_nnz(g) / 2;
+  orc_plan(g, P->size, alloc64, P->base, ralloc, names, prm->policy, offsets, &rec->footprint_bytes);
+  orc_graph_free(g);
+  /* filter_candidates + compute_load_min + the unbudgeted greedy order */
+  orc_cands C;
+  C.var = malloc((size_t)(V + 1) * 4); C.size = malloc((size_t)(V + 1) * 8);
+  C.out_index = malloc((size_t)(V + 1) * 4); C.out_t = malloc((size_t)(V + 1) * 8);
+  C.out_ready = malloc((size_t)(V + 1) * 8); C.in_index = malloc((size_t)(V + 1) * 4);
+  C.in_t = malloc((size_t)(V + 1) * 8); C.dout = malloc((size_t)(V + 1) * 8);
+  C.din = malloc((size_t)(V + 1) * 8); C.spans = malloc((size_t)(V + 1));
+  C.name_base = malloc((size_t)(V + 1) * 4); C.name_ralloc = malloc((size_t)(V + 1) * 4);
+  int64_t k = orc_candidates(&d, &po, prm->threshold, prm->bw, prm->lat, &C);
+  rec->ncand = k;
+  orc_load L = {p, P->loads, P->op_times, d.duration_us};
+  int64_t load_min = orc_load_min(L, &C);
+  rec->load_min = load_min;
+  double *sc[4];
+  for (int i = 0; i < 4; i++) sc[i] = malloc((size_t)(k + 1) * 8);
+  int32_t *order = malloc((size_t)(k + 1) * 4);
+  orc_scores(L, &C, names, sc[0], sc[1], sc[2], sc[3], order);
+  for (int64_t q = 0; q < k; q++) cand_order[q] = C.var[order[q]];
+  /* per budget: SwapPlanner.fit */
+  int32_t *sel = malloc((size_t)(k + 1) * 4);
+  int64_t cap = 1 + p + 2 * k + 2;
+  orc_sim_out so;
+  double *tt[4];
+  for (int i = 0; i < 4; i++) tt[i] = malloc((size_t)(k + 1) * 8);
+  int32_t *eo = malloc((size_t)(k + 1) * 4);
+  double *lp_t = malloc((size_t)cap * 8), *ldp_t = malloc((size_t)cap * 8), *du = malloc((size_t)(p + 1) * 8);
+  int64_t *lp_v = malloc((size_t)cap * 8), *ldp_v = malloc((size_t)cap * 8), *di = malloc((size_t)(p + 1) * 8);
+  for (int b = 0; b < prm->nbudget; b++) {
+    mp_sweep_budget *rb = &brec[b];
+    int64_t limit = (int64_t)((double)d.peak_bytes * prm->budget_frac[b]);
+    rb->limit_bytes = limit;
+    if (limit <= 0) { rb->status = MP_E_VALUE; continue; }
+    if (limit < d.peak_bytes && limit < load_min) {
+      rb->status = MP_E_LIMIT_UNREACHABLE; rb->err_aux = load_min; continue;
+    }
+    int64_t nsel = 0;
+    int rs = orc_select(L, &C, names, 0, NULL, limit, sel, &nsel, &err);
+    if (rs != MP_OK) { rb->status = rs; rb->err_aux = err.aux1; continue; }
+    orc_schedule(&d, P->op_times, &C, names, sel, nsel, tt[0], tt[1], tt[2], tt[3], eo);
+    so = (orc_sim_out){tt[0], tt[1], tt[2], tt[3], eo, lp_t, lp_v, 0, 0, 0.0, ldp_t, ldp_v, 0, 0, 0.0,
+                       di, du, 0, 0.0, 0};
+    int sr = orc_simulate(&d, &po, t->n - p, &C, names, sel, nsel, limit, 1, prm->max_rounds, &so, &err);
+    int64_t bytes = 0;
+    for (int64_t q = 0; q < nsel; q++) bytes += C.size[sel[q]];
+    rb->status = sr;
+    rb->nsel = nsel;
+    rb->selected_bytes = bytes;
+    if (sr == MP_OK) {
+      rb->rounds = (int32_t)so.rounds;
+      rb->overhead_us = so.delay;
+      rb->achieved_peak_bytes = so.ldp_peak;
+      rb->planned_peak_bytes = so.lp_peak;
+    } else if (sr == MP_E_SWAP_DEADLOCK) {
+      rb->err_index = err.index;
+      rb->err_aux = err.aux1;
+    }
+  }
+  free(seg_off); free(lo); free(hi); free(alloc64); free(ralloc);
+  free(C.var); free(C.size); free(C.out_index); free(C.out_t); free(C.out_ready); free(C.in_index);
+  free(C.in_t); free(C.dout); free(C.din); free(C.spans); free(C.name_base); free(C.name_ralloc);
+  for (int i = 0; i < 4; i++) { free(sc[i]); free(tt[i]); }
+  free(order); free(sel); free(eo); free(lp_t); free(ldp_t); free(du); free(lp_v); free(ldp_v); free(di);
+  orc_profile_free(P);
+  return MP_OK;
+}

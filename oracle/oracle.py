@@ -256,3 +256,44 @@ def simulate(fp: FlatProfile, c: CandArrays, names: Names, sel, sched, limit,
 
 lib_loaded = lib
 _ = (MpProfileOut,)
+
+
+# ---------------------------------------------------------------------------
+# batched sweep unit (orc_sweep_unit): the checker / CPU baseline of
+# paper_1903_06631_b200.sweep
+
+
+def sweep_unit(arrays, params):
+    """One unit of a sweep on the CPU: (trace record, budget records,
+    offsets, greedy order) with the dtypes of paper_1903_06631_b200.sweep."""
+    from paper_1903_06631_b200.sweep import BUDGET_DTYPE, TRACE_DTYPE
+    L = lib()
+    L.orc_sweep_unit.restype = C.c_int
+    prm = params.struct()
+    rec = np.zeros(1, TRACE_DTYPE)
+    nb = len(params.budgets)
+    brec = np.zeros(max(nb, 1), BUDGET_DTYPE)
+    n = len(arrays)
+    offs = np.zeros(max(n, 1), np.int64)
+    order = np.zeros(max(n, 1), np.int32)
+    L.orc_sweep_unit(C.byref(trace_in(arrays)), C.byref(prm), ptr(rec), ptr(brec), ptr(offs), ptr(order))
+    r = rec[0]
+    return r, brec[:nb], offs[:int(r["nvars"])], order[:int(r["ncand"])]
+
+
+def sweep(batch, params, indices=None):
+    """Every unit of a SweepBatch (or the given subset) on one host core."""
+    from paper_1903_06631_b200.sweep import BUDGET_DTYPE, TRACE_DTYPE
+    idx = range(batch.ntraces) if indices is None else indices
+    idx = list(idx)
+    nb = len(params.budgets)
+    recs = np.zeros(len(idx), TRACE_DTYPE)
+    brecs = np.zeros((len(idx), nb), BUDGET_DTYPE)
+    offs, orders = [], []
+    for q, t in enumerate(idx):
+        r, b, o, od = sweep_unit(batch.trace(t), params)
+        recs[q] = r
+        brecs[q] = b
+        offs.append(o)
+        orders.append(od)
+    return recs, brecs, offs, orders

@@ -406,7 +406,7 @@ def standardize(x) -> np.ndarray:
 
 
 STAGES = ("group_sort", "validate", "detect", "extract", "loads", "conflict_prep", "conflict_fill",
-          "place_order", "place_split", "place", "footprint", "swap")
+          "place_order", "place_split", "place", "footprint", "swap", "sweep")
 
 
 def set_timing(on: bool) -> None:

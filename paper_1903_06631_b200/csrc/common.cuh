@@ -245,3 +245,34 @@ __device__ __forceinline__ T warp_sum(T v) {
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL_MASK, v, o);
   return v;
 }
+
+// ----------------------------------------------------------------------------
+// thread groups for CTA-level helpers: the whole CTA, or a run of warps
+// synchronizing on a named barrier (so different warps of one CTA can run
+// different stages of a trace concurrently)
+
+struct CtaGroup {
+  __device__ __forceinline__ int idx() const { return threadIdx.x; }
+  __device__ __forceinline__ int size() const { return blockDim.x; }
+  __device__ __forceinline__ void sync() const { __syncthreads(); }
+  __device__ __forceinline__ bool sync_and(bool v) const { return __syncthreads_and(v); }
+};
+
+struct WarpGroup {
+  int first_warp, nwarps, bar;  // bar: named barrier 1..15
+  __device__ __forceinline__ int idx() const { return (int)threadIdx.x - 32 * first_warp; }
+  __device__ __forceinline__ int size() const { return 32 * nwarps; }
+  __device__ __forceinline__ void sync() const {
+    asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(32 * nwarps) : "memory");
+  }
+  __device__ __forceinline__ bool sync_and(bool v) const {
+    unsigned r;
+    asm volatile(
+        "{\n\t.reg .pred p, q;\n\tsetp.ne.u32 p, %1, 0;\n\tbar.red.and.pred q, %2, %3, p;\n\t"
+        "selp.u32 %0, 1, 0, q;\n\t}"
+        : "=r"(r)
+        : "r"((unsigned)v), "r"(bar), "r"(32 * nwarps)
+        : "memory");
+    return r != 0;
+  }
+};

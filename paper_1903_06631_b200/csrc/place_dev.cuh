@@ -1,0 +1,156 @@
+// place_dev.cuh — warp-level pieces of the SmartPool placement step
+// (_pick_offset, smartpool.py:101-119): bitonic sorts of neighbour ranges
+// and the hole scan.  Shared by the grid-wide dataflow placement
+// (placement.cu) and the one-CTA-per-trace sweep (sweep.cu).
+#pragma once
+
+#include <climits>
+
+#include "common.cuh"
+
+struct IV {
+  int64_t s, e;
+};
+
+__device__ __forceinline__ bool iv_less(int64_t as, int64_t ae, int64_t bs, int64_t be) {
+  return as < bs || (as == bs && ae < be);
+}
+
+// bitonic sort of 32*K (start, end) pairs held as element i = r*32 + lane
+template <int K>
+__device__ __forceinline__ void warp_bitonic_reg(int64_t (&s)[K], int64_t (&e)[K]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 2; k <= 32 * K; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+        const int jr = j >> 5;
+#pragma unroll
+        for (int r = 0; r < K; r++) {
+          if ((r & jr) == 0) {
+            const int r2 = r | jr;
+            const bool up = ((r * 32) & k) == 0;
+            bool gt = iv_less(s[r2], e[r2], s[r], e[r]);
+            if (up == gt) {
+              int64_t ts = s[r], te = e[r];
+              s[r] = s[r2]; e[r] = e[r2]; s[r2] = ts; e[r2] = te;
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < K; r++) {
+          int64_t os = __shfl_xor_sync(FULL_MASK, s[r], j);
+          int64_t oe = __shfl_xor_sync(FULL_MASK, e[r], j);
+          const bool up = ((r * 32 + lane) & k) == 0;
+          const bool lower = (lane & j) == 0;
+          bool take = (lower == up) ? iv_less(os, oe, s[r], e[r]) : iv_less(s[r], e[r], os, oe);
+          if (take) { s[r] = os; e[r] = oe; }
+        }
+      }
+    }
+  }
+}
+
+// bitonic sort of n2 pairs in memory (shared or global), one warp
+template <typename P>
+__device__ void warp_bitonic_mem(P buf, int n2) {
+  const int lane = threadIdx.x & 31;
+  for (int k = 2; k <= n2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = lane; i < n2; i += 32) {
+        int ixj = i ^ j;
+        if (ixj > i) {
+          bool up = (i & k) == 0;
+          IV a = buf[i], b = buf[ixj];
+          bool sw = up ? iv_less(b.s, b.e, a.s, a.e) : iv_less(a.s, a.e, b.s, b.e);
+          if (sw) { buf[i] = b; buf[ixj] = a; }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+struct HoleState {
+  int64_t top;       // running max end (starts at 0)
+  int64_t best_len;  // best_fit candidate
+  int64_t best_off;
+  bool found;
+};
+
+// one chunk of 32 sorted ranges; returns true when first_fit is decided
+__device__ __forceinline__ bool hole_chunk(HoleState &h, int64_t s, int64_t e, bool valid, int64_t need,
+                                           int policy) {
+  const int lane = threadIdx.x & 31;
+  int64_t incl = warp_incl_scan_max(valid ? e : INT64_MIN);
+  int64_t excl = __shfl_up_sync(FULL_MASK, incl, 1);
+  if (lane == 0) excl = INT64_MIN;
+  int64_t tb = excl > h.top ? excl : h.top;
+  bool ok = valid && s > tb && s - tb >= need;
+  int64_t len = s - tb;
+  unsigned bal = __ballot_sync(FULL_MASK, ok);
+  if (policy == 0) {
+    if (bal) {
+      h.best_off = __shfl_sync(FULL_MASK, tb, __ffs(bal) - 1);
+      h.found = true;
+      return true;
+    }
+  } else if (bal) {
+    int64_t bl = ok ? len : INT64_MAX, bo = ok ? tb : INT64_MAX;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      int64_t ol = __shfl_xor_sync(FULL_MASK, bl, o), oo = __shfl_xor_sync(FULL_MASK, bo, o);
+      if (ol < bl || (ol == bl && oo < bo)) { bl = ol; bo = oo; }
+    }
+    if (!h.found || bl < h.best_len || (bl == h.best_len && bo < h.best_off)) {
+      h.best_len = bl;
+      h.best_off = bo;
+      h.found = true;
+    }
+  }
+  int64_t cmax = __shfl_sync(FULL_MASK, incl, 31);
+  if (cmax > h.top) h.top = cmax;
+  return false;
+}
+
+__device__ __forceinline__ int warp_max_i32(int v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(FULL_MASK, v, o));
+  return v;
+}
+
+// bitonic sort of 32*K unsigned keys held as element i = r*32 + lane
+template <int K>
+__device__ __forceinline__ void warp_bitonic_keys(uint64_t (&x)[K]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 2; k <= 32 * K; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+        const int jr = j >> 5;
+#pragma unroll
+        for (int r = 0; r < K; r++) {
+          if ((r & jr) == 0) {
+            const int r2 = r | jr;
+            const bool up = ((r * 32) & k) == 0;
+            uint64_t lo = min(x[r], x[r2]), hi = max(x[r], x[r2]);
+            x[r] = up ? lo : hi;
+            x[r2] = up ? hi : lo;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < K; r++) {
+          uint64_t o = __shfl_xor_sync(FULL_MASK, x[r], j);
+          const bool up = ((r * 32 + lane) & k) == 0;
+          const bool lower = (lane & j) == 0;
+          x[r] = (lower == up) ? min(x[r], o) : max(x[r], o);
+        }
+      }
+    }
+  }
+}
+

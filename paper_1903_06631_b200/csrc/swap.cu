@@ -17,12 +17,8 @@
 //
 // Every float operation and comparison follows the reference's order and
 // Python's max/min argument semantics, so results are bit-identical.
-#include <climits>
-
 #include "handles.cuh"
-
-#define INF_D (__longlong_as_double(0x7ff0000000000000ll))
-#define EPS_US 1e-6
+#include "swap_dev.cuh"
 
 struct CandDev {
   int64_t k = 0;
@@ -30,14 +26,6 @@ struct CandDev {
   DBuf<int64_t> size;
   DBuf<double> out_t, out_ready, in_t, dout, din;
   DBuf<uint8_t> spans;
-};
-
-struct CandView {
-  int64_t k;
-  const int64_t *size;
-  const int32_t *out_index, *in_index, *name_rank;
-  const double *out_t, *out_ready, *in_t, *dout, *din;
-  const uint8_t *spans;
 };
 
 static int upload_cands(mp_ctx *ctx, const mp_cands_io *c, CandDev &d, CandView &v, mp_err *err) {
@@ -65,87 +53,16 @@ static int upload_cands(mp_ctx *ctx, const mp_cands_io *c, CandDev &d, CandView 
   return MP_OK;
 }
 
-struct LoadView {
-  int64_t p;
-  const int64_t *loads;
-  const double *op_times;
-  double duration;
-};
-
 // ---------------------------------------------------------------------------
 // filter_candidates
 
-struct CandOut {
-  int32_t *var, *out_index, *in_index;
-  int64_t *size;
-  double *out_t, *out_ready, *in_t, *dout, *din;
-  uint8_t *spans;
-};
-
-// coordinate q-th in sorted order of the access multiset (successor walk
-// when the stored order is not already sorted)
 __global__ void k_swap_candidates(int64_t V, int64_t p, int64_t peak, const int64_t *size, const uint8_t *flags,
                                   const int64_t *acc_off, const int32_t *acc_index, const uint8_t *acc_next,
                                   const double *op_times, double duration, int64_t threshold, double bw, double lat,
                                   int32_t *flag, CandOut o) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
-    flag[v] = 0;
-    if (size[v] < threshold) continue;
-    int64_t a0 = acc_off[v], m = acc_off[v + 1] - a0;
-    auto coord = [&](int64_t q) -> int64_t { return acc_index[a0 + q] + (acc_next[a0 + q] ? p : 0); };
-    bool sorted = true;
-    for (int64_t q = 1; q < m && sorted; q++) sorted = coord(q - 1) <= coord(q);
-    // iterate consecutive pairs of the sorted multiset
-    int64_t prev = 0, prev_q = -1, first = 0;
-    bool found = false;
-    int64_t c1 = 0, c2 = 0;
-    int64_t last_v = -1, last_q = -1;  // successor-walk cursor
-    for (int64_t q = 0; q < m && !found; q++) {
-      int64_t cur;
-      if (sorted) {
-        cur = coord(q);
-      } else {
-        // smallest (value, index) strictly after (last_v, last_q)
-        int64_t bv = LLONG_MAX, bq = -1;
-        for (int64_t t = 0; t < m; t++) {
-          int64_t cv = coord(t);
-          bool after = cv > last_v || (cv == last_v && t > last_q);
-          if (after && (cv < bv || (cv == bv && t < bq))) { bv = cv; bq = t; }
-        }
-        cur = bv;
-        last_v = bv;
-        last_q = bq;
-      }
-      if (q == 0) first = cur;
-      if (q > 0 && prev < cur) {
-        int64_t a = prev, b = cur;
-        if (a >= p) { a -= p; b -= p; }
-        if ((a < peak && peak < b) || (a < peak + p && peak + p < b)) { c1 = a; c2 = b; found = true; }
-      }
-      prev = cur;
-      prev_q = q;
-    }
-    (void)prev_q;
-    if (!found && (flags[v] & MP_F_PERSISTENT) && m > 0) {
-      int64_t a = prev, b = first + p;  // wrap pair (last, first + period)
-      if (a >= p) { a -= p; b -= p; }
-      if ((a < peak && peak < b) || (a < peak + p && peak + p < b)) { c1 = a; c2 = b; found = true; }
-    }
-    if (!found) continue;
-    bool spans = c2 >= p;
-    flag[v] = 1;
-    o.var[v] = (int32_t)v;
-    o.size[v] = size[v];
-    o.out_index[v] = (int32_t)c1;
-    o.out_t[v] = op_times[c1];
-    o.out_ready[v] = c1 + 1 < p ? op_times[c1 + 1] : duration;
-    o.in_index[v] = (int32_t)(c2 % p);
-    o.in_t[v] = op_times[c2 % p] + (spans ? duration : 0.0);
-    double delta = (double)size[v] / bw * 1e6 + lat;
-    o.dout[v] = delta;
-    o.din[v] = delta;
-    o.spans[v] = spans;
-  }
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x)
+    flag[v] = cand_item(v, v, p, peak, size, flags, acc_off, acc_index, acc_next, op_times, duration, threshold, bw,
+                        lat, o);
 }
 
 template <typename T>
@@ -211,161 +128,19 @@ extern "C" int mp_swap_candidates(mp_ctx *ctx, mp_dprofile *P, int64_t threshold
 // ---------------------------------------------------------------------------
 // gap areas
 
-// _step_area, autoswap.py:145-161 (left fold in slot order)
-__device__ double step_area(const LoadView &L, const double *cur, const int64_t *iloads, double a, double b) {
-  if (b <= a) return 0.0;
-  int64_t p = L.p;
-  int64_t lo = 0, hi = p;  // bisect_right(op_times, a)
-  while (lo < hi) {
-    int64_t mid = (lo + hi) >> 1;
-    if (a < L.op_times[mid]) hi = mid; else lo = mid + 1;
-  }
-  int64_t r0 = lo - 1 < 0 ? 0 : lo - 1;
-  double total = 0.0;
-  for (int64_t r = r0; r < p; r++) {
-    double s = L.op_times[r];
-    double e = r + 1 < p ? L.op_times[r + 1] : L.duration;
-    if (s >= b) break;
-    double ov = pymin(b, e) - pymax(a, s);
-    if (ov > 0) total += (cur ? cur[r] : (double)iloads[r]) * ov;
-  }
-  return total;
-}
-
-// gap_area, autoswap.py:164-174
-__device__ double gap_area(const LoadView &L, const double *cur, double a, double b) {
-  double d = L.duration;
-  if (b <= d) return step_area(L, cur, L.loads, a, b);
-  return step_area(L, cur, L.loads, a, d) + step_area(L, cur, L.loads, 0.0, b - d);
-}
-
 __global__ void k_gap_areas(LoadView L, CandView c, const double *cur, double *area) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.k; i += (int64_t)gridDim.x * blockDim.x)
     area[i] = gap_area(L, cur, c.out_t[i], c.in_t[i]);
 }
 
-// ---------------------------------------------------------------------------
-// absence bookkeeping: slots strictly between the two accesses, modulo p
-// (autoswap.py:119-129); a slot can be hit more than once only if the gap
-// exceeds a period, and then the reference subtracts once per hit
-
-__device__ __forceinline__ int absence_hits(int64_t r, int64_t lo, int64_t hi, int64_t p) {
-  // number of x in (lo, hi) with x % p == r, for lo >= 0
-  int h = 0;
-  for (int64_t x = r; x < hi; x += p)
-    if (x > lo) h++;
-  return h;
-}
-
-__device__ __forceinline__ double block_max(double v, double *red) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v = pymax(v, __shfl_xor_sync(FULL_MASK, v, o));
-  if (lane == 0) red[w] = v;
-  __syncthreads();
-  if (w == 0) {
-    double x = lane < nw ? red[lane] : -INF_D;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) x = pymax(x, __shfl_xor_sync(FULL_MASK, x, o));
-    if (lane == 0) red[32] = x;
-  }
-  __syncthreads();
-  double r = red[32];
-  __syncthreads();
-  return r;
-}
-
-__device__ void apply_absence_block(double *cur, int64_t p, const CandView &c, int32_t i) {
-  int64_t lo = c.out_index[i];
-  int64_t hi = c.in_index[i] + (c.spans[i] ? p : 0);
-  double sz = (double)c.size[i];
-  if (hi - lo - 1 <= p) {
-    for (int64_t x = lo + 1 + threadIdx.x; x < hi; x += blockDim.x) cur[x % p] -= sz;
-  } else {
-    for (int64_t r = threadIdx.x; r < p; r += blockDim.x) {
-      int h = absence_hits(r, lo, hi, p);
-      for (int q = 0; q < h; q++) cur[r] -= sz;
-    }
-  }
-  __syncthreads();
-}
-
-__device__ double max_cur(const double *cur, int64_t p, double *red) {
-  double m = -INF_D;
-  bool have = false;
-  for (int64_t r = threadIdx.x; r < p; r += blockDim.x) {
-    m = have ? pymax(m, cur[r]) : cur[r];
-    have = true;
-  }
-  return block_max(m, red);
-}
-
 // scores + the unbudgeted SWDOA greedy, one CTA
 __global__ void __launch_bounds__(512) k_swap_greedy(LoadView L, CandView c, double *cur, uint8_t *taken,
                                                      double *doa, double *aoa, double *wdoa, double *swdoa,
-                                                     int32_t *order, double *peaks) {
+                                                     int32_t *order, double *peaks, int64_t *W, int32_t *jx) {
   __shared__ double red[33];
-  __shared__ double s_area[32];
-  __shared__ int32_t s_idx[32];
-  __shared__ int32_t s_best;
-  __shared__ double s_best_area;
-  const int64_t p = L.p, k = c.k;
-  for (int64_t r = threadIdx.x; r < p; r += blockDim.x) cur[r] = (double)L.loads[r];
-  for (int64_t i = threadIdx.x; i < k; i += blockDim.x) {
-    double gap = c.in_t[i] - c.out_t[i];
-    double d = gap - (c.dout[i] + c.din[i]);
-    doa[i] = d;
-    aoa[i] = d >= 0 ? (double)c.size[i] * d : d / (double)c.size[i];
-    wdoa[i] = gap_area(L, nullptr, c.out_t[i], c.in_t[i]);
-    taken[i] = 0;
-  }
-  __syncthreads();
-  peaks[0] = max_cur(cur, p, red);  // all threads agree
-  for (int64_t round = 0; round < k; round++) {
-    // best key: max (area, size), ties to the smaller name
-    int32_t bi = -1;
-    double ba = 0;
-    for (int64_t i = threadIdx.x; i < k; i += blockDim.x) {
-      if (taken[i]) continue;
-      double area = gap_area(L, cur, c.out_t[i], c.in_t[i]);
-      bool better = bi < 0 || area > ba || (area == ba && (c.size[i] > c.size[bi] ||
-                                                          (c.size[i] == c.size[bi] && c.name_rank[i] < c.name_rank[bi])));
-      if (better) { bi = (int32_t)i; ba = area; }
-    }
-    // warp then block reduction of the argmax
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      int32_t oi = __shfl_xor_sync(FULL_MASK, bi, o);
-      double oa = __shfl_xor_sync(FULL_MASK, ba, o);
-      bool take = oi >= 0 && (bi < 0 || oa > ba || (oa == ba && (c.size[oi] > c.size[bi] ||
-                                                                  (c.size[oi] == c.size[bi] && c.name_rank[oi] < c.name_rank[bi]))));
-      if (take) { bi = oi; ba = oa; }
-    }
-    if (lane == 0) { s_idx[w] = bi; s_area[w] = ba; }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int32_t b = -1;
-      double a = 0;
-      for (int q = 0; q < nw; q++) {
-        int32_t oi = s_idx[q];
-        double oa = s_area[q];
-        bool take = oi >= 0 && (b < 0 || oa > a || (oa == a && (c.size[oi] > c.size[b] ||
-                                                                (c.size[oi] == c.size[b] && c.name_rank[oi] < c.name_rank[b]))));
-        if (take) { b = oi; a = oa; }
-      }
-      s_best = b;
-      s_best_area = a;
-      order[round] = b;
-      swdoa[b] = a;
-      taken[b] = 1;
-    }
-    __syncthreads();
-    apply_absence_block(cur, p, c, s_best);
-    double pk = max_cur(cur, p, red);
-    if (threadIdx.x == 0) peaks[round + 1] = pk;
-  }
-  (void)s_best_area;
+  __shared__ SwKey keys[33];
+  __shared__ long long sm[33];
+  swdoa_greedy_block(CtaGroup{}, L, c, cur, taken, doa, aoa, wdoa, swdoa, order, peaks, W, jx, red, keys, sm);
 }
 
 static LoadView load_view(mp_dprofile *P) { return LoadView{P->d.period, P->loads.p, P->op_times.p, P->d.duration_us}; }
@@ -385,8 +160,11 @@ extern "C" int mp_swap_scores(mp_ctx *ctx, mp_dprofile *P, const mp_cands_io *c,
   CUDA_TRY(cur.alloc(p, st)); CUDA_TRY(o_doa.alloc(k, st)); CUDA_TRY(o_aoa.alloc(k, st));
   CUDA_TRY(o_wdoa.alloc(k, st)); CUDA_TRY(o_sw.alloc(k, st)); CUDA_TRY(o_peaks.alloc(k + 1, st));
   CUDA_TRY(o_order.alloc(k, st)); CUDA_TRY(taken.alloc(k, st));
+  DBuf<int64_t> W;
+  DBuf<int32_t> jx;
+  CUDA_TRY(W.alloc(p + 1, st)); CUDA_TRY(jx.alloc(2 * k, st));
   LAUNCH(ctx, k_swap_greedy, 1, 512, 0, load_view(P), cv, cur.p, taken.p, o_doa.p, o_aoa.p, o_wdoa.p, o_sw.p,
-         o_order.p, o_peaks.p);
+         o_order.p, o_peaks.p, W.p, jx.p);
   if (k) {
     CUDA_TRY(cudaMemcpyAsync(doa, o_doa.p, k * 8, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaMemcpyAsync(aoa, o_aoa.p, k * 8, cudaMemcpyDeviceToHost, st));
@@ -446,14 +224,14 @@ __global__ void __launch_bounds__(512) k_swap_static(LoadView L, CandView c, con
   for (int64_t r = threadIdx.x; r < p; r += blockDim.x) cur[r] = (double)L.loads[r];
   __syncthreads();
   int64_t n = 0;
-  double pk = max_cur(cur, p, red);
+  double pk = max_cur(CtaGroup{}, cur, p, red);
   for (int64_t q = 0; q < k; q++) {
     if (f_le_i(pk, limit)) break;
     int32_t i = ord[q];
-    apply_absence_block(cur, p, c, i);
+    apply_absence_block(CtaGroup{}, cur, p, c, i);
     if (threadIdx.x == 0) sel[n] = i;
     n++;
-    pk = max_cur(cur, p, red);
+    pk = max_cur(CtaGroup{}, cur, p, red);
   }
   if (threadIdx.x == 0) {
     *nsel = n;
@@ -558,73 +336,9 @@ extern "C" int mp_swap_planned_peak(mp_ctx *ctx, mp_dprofile *P, const mp_cands_
 // ---------------------------------------------------------------------------
 // _make_schedule + simulate: one thread
 
-struct SimScratch {
-  int32_t *ord;        // n
-  double *desired;     // n
-  int64_t *in_order;   // n
-  double *plan_in, *in_done; uint8_t *in_has;  // n
-  double *comp_t; int64_t *comp_sz;            // n
-  int32_t *out_trigger, *in_wait;              // p
-  int64_t *delta;                              // p
-  double *actual;                              // p
-  double *ready, *deadline;                    // n
-  double *ev_t; int64_t *ev_d;                 // p + 2n (overlay events)
-  double *ev2_t; int64_t *ev2_d;               // 2n
-};
-
-// insertion sort of positions by (key, name rank, position)
-__device__ void sort_by_key_name(int32_t *ord, int64_t n, const double *key, const int32_t *sel, const CandView &c) {
-  for (int64_t q = 0; q < n; q++) ord[q] = (int32_t)q;
-  for (int64_t q = 1; q < n; q++) {
-    int32_t x = ord[q];
-    int64_t j = q - 1;
-    while (j >= 0) {
-      int32_t y = ord[j];
-      bool gt = key[y] > key[x] || (key[y] == key[x] && (c.name_rank[sel[y]] > c.name_rank[sel[x]] ||
-                                                       (c.name_rank[sel[y]] == c.name_rank[sel[x]] && y > x)));
-      if (!gt) break;
-      ord[j + 1] = y;
-      j--;
-    }
-    ord[j + 1] = x;
-  }
-}
-
-// _make_schedule, swapsim.py:62-108
-__device__ void make_schedule(const CandView &c, const int32_t *sel, int64_t n, const double *ready,
-                              const double *deadline, double *t_so, double *t_eo, double *t_si, double *t_ei,
-                              int32_t *eord, SimScratch &S) {
-  sort_by_key_name(S.ord, n, ready, sel, c);
-  double busy = 0.0;
-  for (int64_t q = 0; q < n; q++) {
-    int32_t s = S.ord[q];
-    double start = pymax(ready[s], busy);
-    t_so[s] = start;
-    busy = start + c.dout[sel[s]];
-    t_eo[s] = busy;
-  }
-  sort_by_key_name(S.ord, n, deadline, sel, c);
-  double cap = INF_D;
-  for (int64_t q = n - 1; q >= 0; q--) {
-    int32_t s = S.ord[q];
-    double end = pymin(deadline[s], cap);
-    S.desired[q] = end - c.din[sel[s]];
-    cap = S.desired[q];
-  }
-  double prev_end = 0.0;
-  for (int64_t q = 0; q < n; q++) {
-    int32_t s = S.ord[q];
-    double start = pymax(pymax(S.desired[q], t_eo[s]), prev_end);
-    t_si[s] = start;
-    prev_end = start + c.din[sel[s]];
-    t_ei[s] = prev_end;
-  }
-  sort_by_key_name(eord, n, t_so, sel, c);
-}
-
 __global__ void k_swap_schedule(CandView c, const int32_t *sel, int64_t n, const double *ready, const double *deadline,
                                 double *t_so, double *t_eo, double *t_si, double *t_ei, int32_t *eord, SimScratch S) {
-  if (threadIdx.x || blockIdx.x) return;
+  if (blockIdx.x || threadIdx.x >= 32) return;
   make_schedule(c, sel, n, ready, deadline, t_so, t_eo, t_si, t_ei, eord, S);
 }
 
@@ -659,18 +373,6 @@ extern "C" int mp_swap_schedule(mp_ctx *ctx, const mp_cands_io *c, const int32_t
   return MP_OK;
 }
 
-struct Curve {
-  double *t;
-  int64_t *v;
-  int64_t n, peak, load;
-  double peak_t;
-  __device__ void point(double tt) {
-    if (t[n - 1] == tt) v[n - 1] = load;
-    else { t[n] = tt; v[n] = load; n++; }
-    if (load > peak) { peak = load; peak_t = tt; }
-  }
-};
-
 struct SimOutDev {
   double *t_so, *t_eo, *t_si, *t_ei;
   int32_t *eord;
@@ -679,155 +381,6 @@ struct SimOutDev {
   int64_t *dl_idx; double *dl_us;
   int64_t *scalars;  // n_lp, lp_peak, lp_peak_t, n_ldp, ldp_peak, ldp_peak_t, n_delayed, delay, rounds, status, idx, aux0, aux1
 };
-
-struct Replay {
-  int64_t k_in, k_out, ncomp, n;
-  double in_busy, head_floor, out_busy, delay;
-  Curve cv;
-  int64_t ndl;
-  bool has_limit;
-  int64_t limit;
-};
-
-// 1 stepped, 0 beyond horizon, -1 IndexError (swapsim.py:266-267)
-__device__ int rp_step(Replay &R, SimScratch &S, const CandView &c, const int32_t *sel, double horizon) {
-  double t_out = R.k_out < R.ncomp ? S.comp_t[R.k_out] : INF_D;
-  double t_in = INF_D;
-  int64_t hv = -1;
-  if (R.k_in < R.n) {
-    hv = S.in_order[R.k_in];
-    double start = pymax(pymax(S.plan_in[hv], R.in_busy), R.head_floor);
-    if (R.has_limit && R.cv.load + c.size[sel[hv]] > R.limit) start = INF_D;
-    t_in = start;
-  }
-  double t = pymin(t_out, t_in);
-  if (t > horizon) return 0;
-  if (t_out <= t_in) {
-    if (R.k_out >= R.ncomp) return -1;
-    int64_t sz = S.comp_sz[R.k_out++];
-    R.cv.load -= sz;
-    R.head_floor = pymax(R.head_floor, t_out);
-    R.cv.point(t_out);
-  } else {
-    R.cv.load += c.size[sel[hv]];
-    R.cv.point(t_in);
-    double end = t_in + c.din[sel[hv]];
-    R.in_busy = end;
-    S.in_done[hv] = end;
-    S.in_has[hv] = 1;
-    R.k_in++;
-  }
-  return 1;
-}
-
-struct ProfView {
-  int64_t p, V, window0;
-  double duration;
-  const double *tau;
-  const int32_t *nseg, *seg;
-  const int64_t *size;
-};
-
-// one _Replay(...).run(), swapsim.py:205-346; returns status
-__device__ int replay_run(Replay &R, SimScratch &S, const ProfView &P, const int64_t live0, const CandView &c,
-                          const int32_t *sel, const double *t_si, const double *t_ei, const int32_t *eord,
-                          double d_actual, int64_t *eidx, int64_t *eaux0, int64_t *eaux1) {
-  const int64_t p = P.p, n = R.n;
-  R.cv.load = live0;
-  for (int64_t q = 0; q < n; q++) {
-    int32_t s = eord[q];
-    int32_t ci = sel[s];
-    if (c.spans[ci]) {
-      R.cv.load -= c.size[ci];
-      S.plan_in[s] = pymax(t_si[s] - d_actual, 0.0);
-    } else {
-      S.plan_in[s] = t_si[s];
-    }
-  }
-  // in_order: (plan_in, deadline, name)
-  for (int64_t q = 0; q < n; q++) S.in_order[q] = eord[q];
-  for (int64_t q = 1; q < n; q++) {
-    int64_t x = S.in_order[q];
-    int64_t j = q - 1;
-    while (j >= 0) {
-      int64_t y = S.in_order[j];
-      bool gt = S.plan_in[y] > S.plan_in[x] ||
-                (S.plan_in[y] == S.plan_in[x] && (t_ei[y] > t_ei[x] ||
-                                                  (t_ei[y] == t_ei[x] && c.name_rank[sel[y]] > c.name_rank[sel[x]])));
-      if (!gt) break;
-      S.in_order[j + 1] = y;
-      j--;
-    }
-    S.in_order[j + 1] = x;
-  }
-  for (int64_t r = 0; r < p; r++) { S.out_trigger[r] = -1; S.in_wait[r] = -1; }
-  for (int64_t s = 0; s < n; s++) {  // dict comprehension: later entries win
-    S.out_trigger[c.out_index[sel[s]]] = (int32_t)s;
-    S.in_wait[c.in_index[sel[s]]] = (int32_t)s;
-  }
-  R.k_in = 0; R.in_busy = 0.0; R.head_floor = 0.0; R.ncomp = 0; R.k_out = 0;
-  R.out_busy = 0.0; R.delay = 0.0; R.ndl = 0;
-  for (int64_t s = 0; s < n; s++) S.in_has[s] = 0;
-  R.cv.n = 1; R.cv.t[0] = 0.0; R.cv.v[0] = R.cv.load; R.cv.peak = R.cv.load; R.cv.peak_t = 0.0;
-  for (int64_t r = 0; r < p; r++) {
-    double t0 = P.tau[r] + R.delay, t = t0;
-    int st;
-    while ((st = rp_step(R, S, c, sel, t)) == 1) {}
-    if (st < 0) return MP_E_SIM_INDEXERROR;
-    int32_t w = S.in_wait[r];
-    if (w >= 0) {
-      while (!S.in_has[w]) {
-        st = rp_step(R, S, c, sel, INF_D);
-        if (st < 0) return MP_E_SIM_INDEXERROR;
-        if (st == 0) { *eidx = P.window0 + r; *eaux0 = 1; *eaux1 = sel[w]; return MP_E_SWAP_DEADLOCK; }
-      }
-      if (S.in_done[w] > t + EPS_US) {
-        t = S.in_done[w];
-        while ((st = rp_step(R, S, c, sel, t)) == 1) {}
-        if (st < 0) return MP_E_SIM_INDEXERROR;
-      }
-    }
-    int64_t dd = S.delta[r];
-    if (dd > 0 && R.has_limit) {
-      while (R.cv.load + dd > R.limit) {
-        if (R.k_out >= R.ncomp) { *eidx = P.window0 + r; *eaux0 = 0; *eaux1 = 0; return MP_E_SWAP_DEADLOCK; }
-        double t_free = S.comp_t[R.k_out];
-        int64_t sz = S.comp_sz[R.k_out++];
-        R.cv.load -= sz;
-        R.head_floor = pymax(R.head_floor, t_free);
-        R.cv.point(t_free);
-        t = pymax(t, t_free);
-      }
-    }
-    if (t > t0 + EPS_US) {
-      R.ndl++;  // the list itself is rebuilt from actual starts (k_sim_delays)
-      R.delay += t - t0;
-    } else {
-      t = t0;
-    }
-    S.actual[r] = t;
-    if (dd != 0) {
-      R.cv.load += dd;
-      R.cv.point(t);
-      if (dd < 0) {
-        R.head_floor = pymax(R.head_floor, t);
-        while ((st = rp_step(R, S, c, sel, t)) == 1) {}
-        if (st < 0) return MP_E_SIM_INDEXERROR;
-      }
-    }
-    int32_t trig = S.out_trigger[r];
-    if (trig >= 0) {
-      double op_end = r + 1 < p ? P.tau[r + 1] : P.duration;
-      double ready = t + (op_end - P.tau[r]);
-      double start = pymax(ready, R.out_busy);
-      R.out_busy = start + c.dout[sel[trig]];
-      S.comp_t[R.ncomp] = R.out_busy;
-      S.comp_sz[R.ncomp] = c.size[sel[trig]];
-      R.ncomp++;
-    }
-  }
-  return MP_OK;
-}
 
 __global__ void k_op_deltas(ProfView P, int64_t *delta, unsigned long long *live0) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < P.V; v += (int64_t)gridDim.x * blockDim.x) {
@@ -840,105 +393,41 @@ __global__ void k_op_deltas(ProfView P, int64_t *delta, unsigned long long *live
   }
 }
 
-// (t, d) lexicographic
-__device__ __forceinline__ bool td_less(double ta, int64_t da, double tb, int64_t db) {
-  return ta < tb || (ta == tb && da < db);
-}
-
 __global__ void k_swap_simulate(ProfView P, CandView c, const int32_t *sel, int64_t n, int64_t limit, int has_limit,
                                 int max_rounds, const unsigned long long *live0p, SimScratch S, SimOutDev O) {
-  if (threadIdx.x || blockIdx.x) return;
-  const int64_t p = P.p;
-  const double dnat = P.duration;
+  if (blockIdx.x || threadIdx.x >= 32) return;  // one warp
+  const int lane = threadIdx.x;
   int64_t live0 = (int64_t)*live0p;
   int64_t *sc = O.scalars;
   // ---- LOAD' overlay (swapsim.py:184-202) on the initial schedule ----
   {
-    // op events are already in time order; sort equal-time runs by delta
     int64_t na = 0;
-    for (int64_t r = 0; r < p; r++)
-      if (S.delta[r] != 0) { S.ev_t[na] = P.tau[r]; S.ev_d[na] = S.delta[r]; na++; }
-    for (int64_t q = 1; q < na; q++) {
-      double xt = S.ev_t[q];
-      int64_t xd = S.ev_d[q];
-      int64_t j = q - 1;
-      while (j >= 0 && td_less(xt, xd, S.ev_t[j], S.ev_d[j])) { S.ev_t[j + 1] = S.ev_t[j]; S.ev_d[j + 1] = S.ev_d[j]; j--; }
-      S.ev_t[j + 1] = xt;
-      S.ev_d[j + 1] = xd;
+    if (lane == 0) na = sim_op_events(P, S.delta, S.ev_t, S.ev_d);
+    na = __shfl_sync(FULL_MASK, na, 0);
+    __syncwarp();
+    Curve cv{O.lp_t, O.lp_v, 1, 0, 0, 0.0};
+    sim_overlay(P, c, sel, n, live0, O.t_eo, O.t_si, O.eord, S.ev_t, S.ev_d, na, S, cv);
+    if (lane == 0) {
+      sc[0] = cv.n; sc[1] = cv.peak;
+      memcpy(&sc[2], &cv.peak_t, 8);
     }
-    int64_t nb = 0, l0 = live0;
-    for (int64_t q = 0; q < n; q++) {
-      int32_t s = O.eord[q];
-      int32_t ci = sel[s];
-      S.ev2_t[nb] = O.t_eo[s]; S.ev2_d[nb] = -c.size[ci]; nb++;
-      if (c.spans[ci]) { l0 -= c.size[ci]; S.ev2_t[nb] = pymax(O.t_si[s] - dnat, 0.0); }
-      else S.ev2_t[nb] = O.t_si[s];
-      S.ev2_d[nb] = c.size[ci];
-      nb++;
-    }
-    for (int64_t q = 1; q < nb; q++) {
-      double xt = S.ev2_t[q];
-      int64_t xd = S.ev2_d[q];
-      int64_t j = q - 1;
-      while (j >= 0 && td_less(xt, xd, S.ev2_t[j], S.ev2_d[j])) { S.ev2_t[j + 1] = S.ev2_t[j]; S.ev2_d[j + 1] = S.ev2_d[j]; j--; }
-      S.ev2_t[j + 1] = xt;
-      S.ev2_d[j + 1] = xd;
-    }
-    Curve cv{O.lp_t, O.lp_v, 1, l0, l0, 0.0};
-    cv.t[0] = 0.0;
-    cv.v[0] = l0;
-    int64_t ia = 0, ib = 0;
-    while (ia < na || ib < nb) {
-      bool take_a = ib >= nb || (ia < na && !td_less(S.ev2_t[ib], S.ev2_d[ib], S.ev_t[ia], S.ev_d[ia]));
-      double t;
-      int64_t d;
-      if (take_a) { t = S.ev_t[ia]; d = S.ev_d[ia]; ia++; }
-      else { t = S.ev2_t[ib]; d = S.ev2_d[ib]; ib++; }
-      cv.load += d;
-      cv.point(t);
-    }
-    sc[0] = cv.n; sc[1] = cv.peak;
-    memcpy(&sc[2], &cv.peak_t, 8);
   }
   // ---- LOAD'' replay with the fixed point (swapsim.py:349-395) ----
-  Replay R{};
-  R.n = n;
-  R.has_limit = has_limit;
-  R.limit = limit;
+  Replay<Curve> R{};
   R.cv.t = O.ldp_t;
   R.cv.v = O.ldp_v;
-  double prev_delay = 0.0;
-  bool have_prev = false;
-  int rc = MP_OK;
-  int64_t rounds = 0, eidx = 0, ea0 = 0, ea1 = 0;
-  for (int it = 0; it < max_rounds; it++) {
-    rc = replay_run(R, S, P, live0, c, sel, O.t_si, O.t_ei, O.eord, dnat + (have_prev ? prev_delay : 0.0),
-                    &eidx, &ea0, &ea1);
-    if (rc) break;
-    rounds++;
-    if (n == 0 || R.delay == 0.0) break;
-    if (have_prev && fabs(R.delay - prev_delay) < 1e-6) break;
-    prev_delay = R.delay;
-    have_prev = true;
-    double d_act = dnat + R.delay;
-    for (int64_t s = 0; s < n; s++) {
-      int32_t ci = sel[s];
-      int64_t oi = c.out_index[ci];
-      double op_end = oi + 1 < p ? P.tau[oi + 1] : dnat;
-      double dur = op_end - P.tau[oi];
-      S.ready[s] = S.actual[oi] + dur;
-      S.deadline[s] = S.actual[c.in_index[ci]] + (c.spans[ci] ? d_act : 0.0);
+  SimTimes T{O.t_so, O.t_eo, O.t_si, O.t_ei, O.eord};
+  SimResult res = sim_fixed_point<true>(P, c, sel, n, limit, has_limit, max_rounds, live0, S, T, R);
+  if (lane == 0) {
+    sc[9] = res.status;
+    sc[10] = res.eidx; sc[11] = res.eaux0; sc[12] = res.eaux1;
+    if (res.status == MP_OK) {
+      sc[3] = R.cv.n; sc[4] = R.cv.peak;
+      memcpy(&sc[5], &R.cv.peak_t, 8);
+      sc[6] = R.ndl;
+      memcpy(&sc[7], &res.delay, 8);
+      sc[8] = res.rounds;
     }
-    make_schedule(c, sel, n, S.ready, S.deadline, O.t_so, O.t_eo, O.t_si, O.t_ei, O.eord, S);
-  }
-  sc[9] = rc;
-  sc[10] = eidx; sc[11] = ea0; sc[12] = ea1;
-  if (rc == MP_OK) {
-    sc[3] = R.cv.n; sc[4] = R.cv.peak;
-    memcpy(&sc[5], &R.cv.peak_t, 8);
-    sc[6] = R.ndl;
-    memcpy(&sc[7], &R.delay, 8);
-    sc[8] = rounds;
   }
 }
 
@@ -972,9 +461,10 @@ extern "C" int mp_swap_simulate(mp_ctx *ctx, mp_dprofile *P, const mp_cands_io *
   int rc = upload_cands(ctx, c, d, cv, err);
   if (rc) return rc;
   int64_t p = P->d.period, cap = 1 + p + 2 * n;
-  DBuf<int32_t> dsel, ord, eord, out_trigger, in_wait;
+  DBuf<int32_t> dsel, ord, eord, out_trigger, in_wait, in_order, ev2_ord;
+  DBuf<uint32_t> busy_op;
   DBuf<double> desired, plan_in, in_done, comp_t, actual, ready, deadline, ev_t, ev2_t, so, eo, si, ei, lp_t, ldp_t, dl_us;
-  DBuf<int64_t> in_order, comp_sz, delta, ev_d, ev2_d, lp_v, ldp_v, dl_idx, scal;
+  DBuf<int64_t> comp_sz, delta, ev_d, ev2_d, lp_v, ldp_v, dl_idx, scal;
   DBuf<uint8_t> in_has;
   int64_t nn = n > 0 ? n : 1;
   CUDA_TRY(dsel.alloc(nn, st)); CUDA_TRY(ord.alloc(nn, st)); CUDA_TRY(eord.alloc(nn, st));
@@ -986,7 +476,7 @@ extern "C" int mp_swap_simulate(mp_ctx *ctx, mp_dprofile *P, const mp_cands_io *
   CUDA_TRY(lp_t.alloc(cap, st)); CUDA_TRY(lp_v.alloc(cap, st)); CUDA_TRY(ldp_t.alloc(cap, st)); CUDA_TRY(ldp_v.alloc(cap, st));
   CUDA_TRY(dl_idx.alloc(p, st)); CUDA_TRY(dl_us.alloc(p, st)); CUDA_TRY(scal.alloc(16, st));
   CUDA_TRY(in_order.alloc(nn, st)); CUDA_TRY(comp_sz.alloc(nn, st)); CUDA_TRY(delta.alloc(p, st));
-  CUDA_TRY(in_has.alloc(nn, st));
+  CUDA_TRY(in_has.alloc(nn, st)); CUDA_TRY(ev2_ord.alloc(2 * nn, st)); CUDA_TRY(busy_op.alloc((p + 31) / 32, st));
   if (n) {
     CUDA_TRY(cudaMemcpyAsync(dsel.p, sel, n * 4, cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaMemcpyAsync(so.p, io->t_so, n * 8, cudaMemcpyHostToDevice, st));
@@ -1001,7 +491,8 @@ extern "C" int mp_swap_simulate(mp_ctx *ctx, mp_dprofile *P, const mp_cands_io *
   ProfView pv{p, P->d.nvars, P->window0, P->d.duration_us, P->op_times.p, P->nseg.p, P->seg.p, P->size.p};
   LAUNCH(ctx, k_op_deltas, grid_for(P->d.nvars, 256), 256, 0, pv, delta.p, d_live0);
   SimScratch S{ord.p, desired.p, in_order.p, plan_in.p, in_done.p, in_has.p, comp_t.p, comp_sz.p,
-               out_trigger.p, in_wait.p, delta.p, actual.p, ready.p, deadline.p, ev_t.p, ev_d.p, ev2_t.p, ev2_d.p};
+               out_trigger.p, in_wait.p, busy_op.p, delta.p, actual.p, ready.p, deadline.p, ev_t.p, ev_d.p,
+               ev2_t.p, ev2_d.p, ev2_ord.p};
   SimOutDev O{so.p, eo.p, si.p, ei.p, eord.p, lp_t.p, lp_v.p, ldp_t.p, ldp_v.p, dl_idx.p, dl_us.p, scal.p};
   LAUNCH(ctx, k_swap_simulate, 1, 32, 0, pv, cv, dsel.p, n, limit, has_limit, max_rounds, d_live0, S, O);
   int64_t h[16];

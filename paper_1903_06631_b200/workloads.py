@@ -223,3 +223,36 @@ def random_periodic_trace(seed: int, slots: int = 40, nvars: int = 10,
         events.append(TraceEvent(i, t, EventKind(kind), var, size))
         t += 0 if rng.random() < zero_dt else rng.randrange(1, 25)
     return Trace(events=events, meta={"template_period": S})
+
+
+# ---------------------------------------------------------------------------
+# config 5
+
+
+SWEEP_BUDGETS = (0.9, 0.8, 0.7, 0.6)
+
+
+def sweep_specs(n_models: int = 64, n_scales: int = 16, iterations: int = 3, seed: int = 0):
+    """The (model shape x batch scale) grid of BASELINE configs[4]: model 0
+    is VGG-16, model 1 ResNet-50 (batch 8 * (s + 1)), the rest ``vgg_like``
+    depths 6-16 with alternating temporaries and their own seeds (activation
+    scale (s + 1) / 8).  With 4 budgets per trace, 64 x 16 x 4 = 4096 units."""
+    from .synth import vgg_like
+    specs = []
+    for m in range(n_models):
+        for s in range(n_scales):
+            sd = seed + 1000 * m + s
+            if m == 0:
+                specs.append(vgg16_spec(batch=8 * (s + 1), iterations=iterations, seed=sd))
+            elif m == 1:
+                specs.append(resnet50_spec(batch=8 * (s + 1), iterations=iterations, seed=sd))
+            else:
+                depth = 6 + (m - 2) % 11
+                specs.append(vgg_like(depth=depth, scale=(s + 1) / 8, iterations=iterations, seed=sd,
+                                      temp_ratio=0.5 if m % 2 else 0.0))
+    return specs
+
+
+def sweep_traces(n_models: int = 64, n_scales: int = 16, iterations: int = 3, seed: int = 0):
+    from .synth import generate_synthetic_trace
+    return [generate_synthetic_trace(sp) for sp in sweep_specs(n_models, n_scales, iterations, seed)]
