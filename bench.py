@@ -217,6 +217,109 @@ def run_ours(args, rank, world, local_rank):
     return arrays, res
 
 
+# ---------------------------------------------------------------------------
+# config 5: batched sweep of 1024 traces x 4 budgets = 4096 units, sharded
+# over ranks (LPT on event counts, no collective on the data path)
+
+
+def _sweep_oracle_chunk(idx):
+    import oracle as orc
+    t0 = time.perf_counter()
+    recs, brecs, offs, orders = orc.sweep(_SWEEP_BATCH, _SWEEP_PARAMS, idx)
+    return time.perf_counter() - t0, recs, brecs, offs, orders
+
+
+_SWEEP_BATCH = None
+_SWEEP_PARAMS = None
+
+
+def sweep_cpu_baseline(batch, params, procs):
+    """The C oracle over the whole batch on `procs` host processes (fork)."""
+    global _SWEEP_BATCH, _SWEEP_PARAMS
+    import multiprocessing as mp
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    _SWEEP_BATCH, _SWEEP_PARAMS = batch, params
+    chunks = [list(range(i, batch.ntraces, procs)) for i in range(procs)]
+    chunks = [c for c in chunks if c]
+    with mp.get_context("fork").Pool(len(chunks)) as pool:
+        pool.map(_sweep_oracle_chunk, chunks[:1])  # warm the workers
+        t0 = time.perf_counter()
+        outs = pool.map(_sweep_oracle_chunk, chunks)
+        dt = time.perf_counter() - t0
+    return dt, chunks, outs
+
+
+def run_sweep_bench(args, rank, world, local_rank):
+    import torch
+    from paper_1903_06631_b200 import _native as N
+    from paper_1903_06631_b200 import sweep, workloads
+    batch = sweep.SweepBatch.from_traces(workloads.sweep_traces())
+    params = sweep.SweepParams(budgets=workloads.SWEEP_BUDGETS)
+    parts = sweep.shard([batch.events_of(t) for t in range(batch.ntraces)], world)
+    mine = batch.subset(parts[rank]) if world > 1 else batch
+    stream = torch.cuda.ExternalStream(N.stream_ptr())
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def timed(fn):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        out = fn()
+        e.record(stream)
+        e.synchronize()
+        return s.elapsed_time(e), out
+
+    ds = sweep.DeviceSweep(mine)
+    for _ in range(args.warmup):
+        ds.run(params)
+    l0 = N.launches()
+    res_ms = [timed(lambda: ds.run(params))[0] for _ in range(args.steps)]
+    launches = (N.launches() - l0) / max(args.steps, 1)
+    res = ds.download()
+    ds.close()
+    e2e_ms = []
+    for i in range(args.warmup + args.steps):
+        ms, out = timed(lambda: sweep.run_sweep(mine, params))
+        if i >= args.warmup:
+            e2e_ms.append(ms)
+    step_ms, e2e_step = float(np.mean(res_ms)), float(np.mean(e2e_ms))
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([step_ms, e2e_step], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        step_ms, e2e_step = float(tt[0]), float(tt[1])
+    units = batch.ntraces * len(params.budgets)
+    vars_total = int(res.traces["nvars"].sum())
+    if world > 1:
+        import torch.distributed as dist
+        tv = torch.tensor([vars_total], device="cuda", dtype=torch.int64)
+        dist.all_reduce(tv)
+        vars_total = int(tv[0])
+    out = {"workload": "sweep_4096 (BASELINE configs[4]): 64 model shapes x 16 batch scales x 4 budgets",
+           "traces": batch.ntraces, "units": units, "events": int(batch.ev_off[-1]),
+           "value": units / (step_ms * 1e-3), "unit": "units/s", "ms_per_step": step_ms,
+           "planned_vars_per_s": vars_total / (step_ms * 1e-3), "scaling": "strong",
+           "sharding": f"LPT over {world} rank(s), no data-path collective",
+           "gpu_launches": launches,
+           "e2e": {"value": units / (e2e_step * 1e-3), "unit": "units/s", "ms_per_step": e2e_step,
+                   "h2d_bytes_per_step": int(mine.nbytes),
+                   "d2h_bytes_per_step": int(res.traces.nbytes + res.budgets.nbytes + 12 * mine.ev_off[-1])},
+           "budget_status": {str(k): int(v) for k, v in zip(*np.unique(res.budgets["status"], return_counts=True))}}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        procs = os.cpu_count() or 1
+        dt, chunks, outs = sweep_cpu_baseline(batch, params, procs)
+        ok = True
+        for idx, (_, recs, brecs, offs, orders) in zip(chunks, outs):
+            for q, t in enumerate(idx):
+                ok &= (res.traces[t].tobytes() == recs[q].tobytes() and res.budgets[t].tobytes() == brecs[q].tobytes()
+                       and np.array_equal(res.offsets_of(t), offs[q]) and np.array_equal(res.order_of(t), orders[q]))
+        out["cpu_baseline"] = {"value": units / dt, "unit": "units/s", "cores": procs, "kind": "port",
+                               "sample": f"the whole 4096-unit batch, C oracle in {procs} processes, {dt:.3f} s"}
+        out["parity"] = {"units_equal_oracle": bool(ok)}
+    return out
+
+
 def cpu_baseline(arrays):
     """C oracle on this host: detect + extract + conflict + best_fit plan, 1 thread."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -278,6 +381,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--accesses", action="store_true", help="config-4 variant with write/read per var")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the config-5 batched sweep leg")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -292,6 +396,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         dist.barrier()
     arrays, r = run_ours(args, rank, world, local_rank)
+    r["sweep"] = None if args.no_sweep else run_sweep_bench(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
@@ -339,6 +444,8 @@ def main():
         "stage_hbm_frac": stage_roof,
         "clocks": r["clocks"],
     }
+    if r.get("sweep") is not None:
+        line["sweep"] = r["sweep"]
     if not args.no_cpu_baseline:
         cb = cpu_baseline(arrays)
         line["cpu_baseline"] = {"value": cb["value"], "unit": UNIT, "cores": 1, "kind": "port",

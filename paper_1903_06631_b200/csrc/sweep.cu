@@ -902,6 +902,9 @@ extern "C" int mp_sweep_upload(mp_ctx *ctx, const mp_sweep_in *in, mp_dsweep **o
   if (e == cudaSuccess) e = up(s->work, work.data(), T);
   if (e == cudaSuccess) e = s->offsets.alloc(N, st);
   if (e == cudaSuccess) e = s->cand_order.alloc(N, st);
+  // rows past a trace's variable / candidate count stay zero
+  if (e == cudaSuccess && N) e = cudaMemsetAsync(s->offsets.p, 0, N * 8, st);
+  if (e == cudaSuccess && N) e = cudaMemsetAsync(s->cand_order.p, 0, N * 4, st);
   if (e == cudaSuccess) e = s->rec.alloc(T, st);
   if (e == cudaSuccess) e = s->counter.alloc(1, st);
   // host staging (work) must outlive the async copy

@@ -162,6 +162,7 @@ class SweepResult:
     cand_order: np.ndarray      # int32[N]: trace t's SWDOA greedy picks (profile variable indices)
     ev_off: np.ndarray
     params: SweepParams = field(default_factory=SweepParams)
+    batch: "SweepBatch | None" = None
 
     def offsets_of(self, t: int) -> np.ndarray:
         e0 = int(self.ev_off[t])
@@ -193,12 +194,20 @@ class SweepResult:
         err = MpErr()
         err.code = code
         err.index = int(rec["err_index"])
+        names = None
         if b is None:
             err.aux0 = int(rec["err_code"])
+            if code == 1 and self.batch is not None:
+                # the offending event: absolute for validate_trace, window-relative
+                # for extract_lifetimes (codes >= 9)
+                e0 = int(self.batch.ev_off[t])
+                pos = err.index + (self.batch.events_of(t) - int(rec["period"]) if err.aux0 >= 9 else 0)
+                err.aux1 = int(self.batch.kind[e0 + pos]) if err.aux0 == 6 else int(self.batch.var[e0 + pos])
+                names = self.batch.trace(t).names
         else:
             err.aux0 = int(rec["limit_bytes"])
             err.aux1 = int(rec["err_aux"])
-        raise_for(code, err)
+        raise_for(code, err, names)
 
 
 def _lib():
@@ -240,7 +249,7 @@ class DeviceSweep:
         rc = _lib().mp_sweep_download(N.ctx(), self._h, ptr(traces), ptr(budgets) if nb else None,
                                       ptr(offsets), ptr(cand_order), C.byref(err))
         raise_for(rc, err)
-        return SweepResult(traces, budgets, offsets[:Nev], cand_order[:Nev], b.ev_off, self.params)
+        return SweepResult(traces, budgets, offsets[:Nev], cand_order[:Nev], b.ev_off, self.params, b)
 
     def set_profile(self, on: bool = True) -> None:
         """Diagnostics: record clock64() at the kernel's 8 phase marks."""
@@ -296,3 +305,49 @@ def shard(costs: Sequence[float], world: int) -> list[list[int]]:
         parts[r].append(i)
         load[r] += float(costs[i])
     return [sorted(p) for p in parts]
+
+
+def concat_results(parts: Sequence[tuple[Sequence[int], SweepResult]], batch: SweepBatch) -> SweepResult:
+    """Reassemble per-shard results (shard trace indices, result) into one
+    result in the batch's trace order."""
+    T, Nev = batch.ntraces, int(batch.ev_off[-1])
+    params = next((r.params for _, r in parts if r is not None), SweepParams())
+    nb = len(params.budgets)
+    traces = np.zeros(T, TRACE_DTYPE)
+    budgets = np.zeros((T, nb), BUDGET_DTYPE)
+    offsets = np.zeros(max(Nev, 1), np.int64)
+    cand_order = np.zeros(max(Nev, 1), np.int32)
+    for idx, res in parts:
+        for q, t in enumerate(idx):
+            traces[t] = res.traces[q]
+            budgets[t] = res.budgets[q]
+            e0, n = int(batch.ev_off[t]), batch.events_of(t)
+            s0 = int(res.ev_off[q])
+            offsets[e0:e0 + n] = res.offsets[s0:s0 + n]
+            cand_order[e0:e0 + n] = res.cand_order[s0:s0 + n]
+    return SweepResult(traces, budgets, offsets[:Nev], cand_order[:Nev], batch.ev_off, params, batch)
+
+
+def run_sweep_sharded(batch: SweepBatch, params: SweepParams | None = None, rank: int = 0, world: int = 1,
+                      runner=None, group=None) -> SweepResult | None:
+    """One rank's share of a sweep, then a gather on rank 0.
+
+    Units are partitioned by ``shard`` on event counts (every rank computes
+    the same split), each rank plans its own traces on its own device with
+    no collective on the data path, and the fixed-size records are gathered
+    to rank 0 with ``torch.distributed.gather_object`` once at the end.
+    Returns the whole batch's result on rank 0 and None elsewhere.
+    """
+    params = params or SweepParams()
+    runner = runner or run_sweep
+    parts = shard([batch.events_of(t) for t in range(batch.ntraces)], world)
+    mine = parts[rank]
+    res = runner(batch.subset(mine), params) if mine else None
+    if world == 1:
+        return concat_results([(mine, res)], batch)
+    import torch.distributed as dist
+    gathered = [None] * world if rank == 0 else None
+    dist.gather_object((mine, res), gathered, dst=0, group=group)
+    if rank != 0:
+        return None
+    return concat_results([g for g in gathered if g[1] is not None], batch)

@@ -106,3 +106,55 @@ def canon_schedule(cnames, sel, t_so, t_eo, t_si, t_ei, event_order, sizes, dura
 def canon_curve(t, v, peak, peak_t) -> dict:
     return {"points": pack([[fhex(a), int(b)] for a, b in zip(t.tolist(), v.tolist())]),
             "peak": int(peak), "peak_t": fhex(peak_t)}
+
+
+# ---------------------------------------------------------------------------
+# batched sweep units (tests/golden/sweep.json.gz, make_golden_sweep.py)
+
+V_REASON = {1: "not contiguous", 2: "negative timestamp", 3: "timestamp decreases",
+            4: "malloc size must be > 0", 5: "malloc of live id", 6: "size must be 0",
+            7: "free of dead id", 8: "use of dead id"}
+
+
+def sweep_params(prm: dict):
+    from paper_1903_06631_b200.sweep import SweepParams
+    return SweepParams(budgets=tuple(prm["budgets"]), policy=prm["policy"], threshold_bytes=prm["threshold"],
+                       bandwidth_bytes_per_s=prm["bw"], latency_us=prm["lat"], max_rounds=prm["max_rounds"])
+
+
+def check_sweep_unit(rec, brec, offsets, order, gold: dict) -> None:
+    """One unit's flat records (oracle or device) against the reference's."""
+    if "error" in gold:
+        kind = gold["error"][0]
+        if kind == "InvariantViolation":
+            assert int(rec["status"]) == 1 and int(rec["err_index"]) == gold["error"][1], (rec, gold)
+            assert V_REASON[int(rec["err_code"])] in gold["error"][2], (rec, gold)
+        else:
+            assert kind == "PeriodNotFound" and int(rec["status"]) == 2, (rec, gold)
+        return
+    assert int(rec["status"]) == 0, rec
+    got = {"period": int(rec["period"]), "nvars": int(rec["nvars"]), "ncarry": int(rec["ncarry"]),
+           "naccess": int(rec["naccess"]), "peak": int(rec["peak_bytes"]),
+           "peak_index": int(rec["peak_index"]), "duration": fhex(rec["duration_us"]),
+           "footprint": int(rec["footprint_bytes"]), "edges": int(rec["edges"]),
+           "ncand": int(rec["ncand"]), "load_min": int(rec["load_min"]),
+           "offsets": [int(x) for x in offsets], "order": [int(x) for x in order]}
+    want = {k: gold[k] for k in got}
+    assert got == want
+    assert len(brec) == len(gold["budgets"])
+    code = {"ValueError": 6, "LimitUnreachable": 3, "SwapDeadlock": 4, "IndexError": 5}
+    for b, g in zip(brec, gold["budgets"]):
+        assert int(b["limit_bytes"]) == g["limit"], (b, g)
+        if "error" in g:
+            e = g["error"]
+            assert int(b["status"]) == code[e[0]], (b, g)
+            if e[0] == "LimitUnreachable":
+                assert int(b["err_aux"]) == e[2], (b, g)
+            if e[0] == "SwapDeadlock":
+                assert int(b["err_index"]) == e[1], (b, g)
+            continue
+        nsel = int(b["nsel"])
+        got_b = {"selection": [int(x) for x in order[:nsel]], "selected_bytes": int(b["selected_bytes"]),
+                 "rounds": int(b["rounds"]), "overhead_us": fhex(b["overhead_us"]),
+                 "achieved": int(b["achieved_peak_bytes"]), "planned": int(b["planned_peak_bytes"])}
+        assert int(b["status"]) == 0 and got_b == {k: g[k] for k in got_b}, (b, g)
