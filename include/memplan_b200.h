@@ -372,7 +372,8 @@ int mp_sweep_download(mp_ctx *ctx, mp_dsweep *s, mp_sweep_trace *traces, mp_swee
 /* diagnostics: per-trace clock64() at 8 phase marks of the sweep kernel
  * (start, extract, plan, candidates, greedy, simulate prep, budgets, end) */
 int mp_sweep_set_profile(mp_ctx *ctx, mp_dsweep *s, int on, mp_err *err);
-int mp_sweep_profile_download(mp_ctx *ctx, mp_dsweep *s, long long *out /* [ntraces * 8] */, mp_err *err);
+int mp_sweep_profile_download(mp_ctx *ctx, mp_dsweep *s, long long *out /* [ntraces * 16]: 8 marks + 8 counters */,
+                              mp_err *err);
 
 #ifdef __cplusplus
 }

@@ -137,10 +137,9 @@ __global__ void k_gap_areas(LoadView L, CandView c, const double *cur, double *a
 __global__ void __launch_bounds__(512) k_swap_greedy(LoadView L, CandView c, double *cur, uint8_t *taken,
                                                      double *doa, double *aoa, double *wdoa, double *swdoa,
                                                      int32_t *order, double *peaks, int64_t *W, int32_t *jx) {
-  __shared__ double red[33];
   __shared__ SwKey keys[33];
-  __shared__ long long sm[33];
-  swdoa_greedy_block(CtaGroup{}, L, c, cur, taken, doa, aoa, wdoa, swdoa, order, peaks, W, jx, red, keys, sm);
+  __shared__ long long sm[PM_SMEM];
+  swdoa_greedy_block(CtaGroup{}, L, c, cur, taken, doa, aoa, wdoa, swdoa, order, peaks, W, jx, keys, sm);
 }
 
 static LoadView load_view(mp_dprofile *P) { return LoadView{P->d.period, P->loads.p, P->op_times.p, P->d.duration_us}; }

@@ -266,55 +266,88 @@ __device__ __forceinline__ int64_t gap_area_exact(const LoadView &L, const doubl
   return ex < (int64_t)EXACT_2_53 ? ex : -1;
 }
 
-// W = exclusive prefix of cur[q] * len_q (p + 1 entries, group-wide);
-// returns false when some cur is not an integer in [0, 2^53) or
-// cur * duration may overflow.  sm: >= 33 long longs of shared memory.
+// One pass over the current load: max(cur) (Python max: the first maximal
+// value) and, when `exact` is requested and holds, W = the exclusive prefix
+// of cur[q] * len_q (p + 1 entries).  `exact` comes back false when some cur
+// is not an integer in [0, 2^53) or cur * duration may overflow.  Group-wide;
+// sm: >= PM_SMEM long longs of shared memory.
+constexpr int PM_SUM = 0, PM_TOT = 32, PM_MAX = 33, PM_MXR = 65, PM_OK = 66, PM_OKR = 98, PM_SMEM = 100;
+
 template <class G>
-__device__ bool exact_prefix_block(const G &g, const LoadView &L, const double *cur, int64_t *W, long long *sm) {
-  const int tid = g.idx(), nt = g.size(), nw = (nt + 31) >> 5;
+__device__ double prefix_max_block(const G &g, const LoadView &L, const double *cur, int64_t *W, long long *sm,
+                                   bool &exact) {
+  const int tid = g.idx(), nt = g.size(), nw = (nt + 31) >> 5, lane = tid & 31;
   const int64_t p = L.p;
   int64_t per = (p + nt - 1) / nt;
   int64_t lo = tid * per, hi = lo + per < p ? lo + per : p;
-  bool ok = true;
+  bool ok = exact;
   long long s = 0;
+  double m = -INF_D;
   for (int64_t q = lo; q < hi; q++) {
     double c = cur[q];
-    ok &= int_valued(c) && c * L.duration < EXACT_2_62;
-    double e = q + 1 < p ? L.op_times[q + 1] : L.duration;
-    if (ok) s += (long long)c * (long long)(e - L.op_times[q]);
+    m = q == lo ? c : pymax(m, c);
+    if (ok) {
+      ok = int_valued(c) && c * L.duration < EXACT_2_62;
+      double e = q + 1 < p ? L.op_times[q + 1] : L.duration;
+      s += ok ? (long long)c * (long long)(e - L.op_times[q]) : 0;
+    }
   }
-  ok = g.sync_and(ok);
-  if (!ok) return false;
+  // threads are contiguous chunks in slot order, so combining in thread order
+  // keeps Python's first-maximal semantics
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    double u = __shfl_up_sync(FULL_MASK, m, o);
+    if (lane >= o) m = pymax(u, m);
+  }
   long long incl = warp_incl_scan_add(s);
-  if ((tid & 31) == 31) sm[tid >> 5] = incl;
+  unsigned allok = __ballot_sync(FULL_MASK, ok);
+  double *smd = reinterpret_cast<double *>(sm);
+  if (lane == 31) {
+    sm[PM_SUM + (tid >> 5)] = incl;
+    smd[PM_MAX + (tid >> 5)] = m;
+    sm[PM_OK + (tid >> 5)] = allok == FULL_MASK;
+  }
   g.sync();
   if (tid == 0) {
-    long long acc = 0;
-    for (int w = 0; w < nw; w++) { long long x = sm[w]; sm[w] = acc; acc += x; }
-    sm[32] = acc;
+    long long acc = 0, all = 1;
+    double mx = smd[PM_MAX];
+    for (int w = 0; w < nw; w++) {
+      long long x = sm[PM_SUM + w];
+      sm[PM_SUM + w] = acc;
+      acc += x;
+      if (w) mx = pymax(mx, smd[PM_MAX + w]);
+      all &= sm[PM_OK + w];
+    }
+    smd[PM_MXR] = mx;
+    sm[PM_TOT] = acc;
+    sm[PM_OKR] = all;
   }
   g.sync();
-  long long run = sm[tid >> 5] + incl - s;
-  for (int64_t q = lo; q < hi; q++) {
-    W[q] = run;
-    double e = q + 1 < p ? L.op_times[q + 1] : L.duration;
-    run += (long long)cur[q] * (long long)(e - L.op_times[q]);
+  const bool all_exact = exact && sm[PM_OKR] != 0;
+  const double mx = smd[PM_MXR];
+  if (all_exact) {
+    long long run = sm[PM_SUM + (tid >> 5)] + incl - s;
+    for (int64_t q = lo; q < hi; q++) {
+      W[q] = run;
+      double e = q + 1 < p ? L.op_times[q + 1] : L.duration;
+      run += (long long)cur[q] * (long long)(e - L.op_times[q]);
+    }
+    if (tid == 0) W[p] = sm[PM_TOT];
   }
-  if (tid == 0) W[p] = sm[32];
   g.sync();
-  return true;
+  exact = all_exact;
+  return mx;
 }
 
 // scores + the unbudgeted SWDOA greedy (autoswap.py:132-215), group-wide.
 // peaks[j] = max(cur) after j picks, so a budgeted select_by_swdoa is the
 // prefix order[0..m) with m the first j where peaks[j] <= limit.  Any of
 // doa/aoa/wdoa/swdoa may be null.  Scratch: W[p + 1], jx[2k]; shared
-// memory red >= 33 doubles, keys >= 33 SwKey, sm >= 33 long longs.
+// memory keys >= 33 SwKey, sm >= PM_SMEM long longs.
 template <class G>
 __device__ void swdoa_greedy_block(const G &g, const LoadView &L, const CandView &c, double *cur, uint8_t *taken,
                                    double *doa, double *aoa, double *wdoa, double *swdoa, int32_t *order,
-                                   double *peaks, int64_t *W, int32_t *jx, double *red, SwKey *keys,
-                                   long long *sm) {
+                                   double *peaks, int64_t *W, int32_t *jx, SwKey *keys, long long *sm) {
   const int64_t p = L.p, k = c.k;
   const int tid = g.idx(), nt = g.size();
   bool times_ok = int_valued(L.duration);
@@ -335,11 +368,12 @@ __device__ void swdoa_greedy_block(const G &g, const LoadView &L, const CandView
     jx[2 * i + 1] = slot_of(L, b <= L.duration ? b : b - L.duration);
   }
   times_ok = g.sync_and(times_ok);
-  double pk0 = max_cur(g, cur, p, red);  // all threads agree
-  if (tid == 0) peaks[0] = pk0;
   const int lane = tid & 31, w = tid >> 5, nw = (nt + 31) >> 5;
-  for (int64_t round = 0; round < k; round++) {
-    const bool exact = times_ok && exact_prefix_block(g, L, cur, W, sm);
+  for (int64_t round = 0;; round++) {
+    bool exact = times_ok;
+    const double pk = prefix_max_block(g, L, cur, W, sm, exact);
+    if (tid == 0) peaks[round] = pk;
+    if (round == k) break;
     SwKey best{-1, 0, 0.0, 0};
     for (int64_t i = tid; i < k; i += nt) {
       if (taken[i]) continue;
@@ -368,8 +402,6 @@ __device__ void swdoa_greedy_block(const G &g, const LoadView &L, const CandView
     g.sync();
     const int32_t pick = keys[32].i;
     apply_absence_block(g, cur, p, c, pick);
-    double pk = max_cur(g, cur, p, red);
-    if (tid == 0) peaks[round + 1] = pk;
   }
 }
 
@@ -498,7 +530,7 @@ struct Replay {
 // _Replay._step, swapsim.py:256-282: 1 stepped, 0 beyond horizon,
 // -1 IndexError (the reference defect at swapsim.py:266-267)
 template <class CurveT>
-__device__ int rp_step(Replay<CurveT> &R, SimScratch &S, const CandView &c, const int32_t *sel, double horizon) {
+__device__ __forceinline__ int rp_step(Replay<CurveT> &R, SimScratch &S, const CandView &c, const int32_t *sel, double horizon) {
   double t_out = R.k_out < R.ncomp ? S.comp_t[R.k_out] : INF_D;
   double t_in = INF_D;
   int64_t hv = -1;

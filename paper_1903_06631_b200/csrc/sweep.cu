@@ -34,7 +34,8 @@
 
 constexpr int SW_THREADS = 128;
 constexpr int SW_WARPS = SW_THREADS / 32;
-constexpr size_t SW_FAST_BYTES = 64 * 1024;  // per-CTA shared-memory arena
+constexpr size_t SW_FAST_BYTES = 72 * 1024;
+constexpr int PL_K = 4;  // placement list entries per lane per pass  // per-CTA shared-memory arena
 
 // ---------------------------------------------------------------------------
 // scratch allocation.  Each CTA owns a slab of global scratch (bump
@@ -172,45 +173,58 @@ struct PlaceArrays {
   }
 };
 
-struct SwapArrays {
-  int32_t *flag, *pos;
-  CandOut tmp, c;
-  int32_t *name_rank;
-  double *peaks;
-  int32_t *order;
-  int64_t *delta;
-  double *ev_t;
-  int64_t *ev_d;
-  template <class A>
-  __host__ __device__ void take_cols(A &b, CandOut &o, int64_t V) {
-    o.var = b.template take<int32_t>(V); o.out_index = b.template take<int32_t>(V);
-    o.in_index = b.template take<int32_t>(V); o.size = b.template take<int64_t>(V);
-    o.out_t = b.template take<double>(V); o.out_ready = b.template take<double>(V);
-    o.in_t = b.template take<double>(V); o.dout = b.template take<double>(V);
-    o.din = b.template take<double>(V); o.spans = b.template take<uint8_t>(V);
-  }
+// swap-path arrays that live until the budgets are done (shared memory
+// when they fit: the budget phase refills the arena above them)
+struct SwapKeep {
+  CandOut c;
+  int32_t *name_rank, *order;
+  double *peaks, *tau, *ev_t;
+  int64_t *delta, *ev_d;
   template <class A>
   __host__ __device__ void take(A &b, int64_t p, int64_t V) {
-    flag = b.template take<int32_t>(V); pos = b.template take<int32_t>(V);
-    take_cols(b, tmp, V);
-    take_cols(b, c, V);
+    c.var = b.template take<int32_t>(V); c.out_index = b.template take<int32_t>(V);
+    c.in_index = b.template take<int32_t>(V); c.size = b.template take<int64_t>(V);
+    c.out_t = b.template take<double>(V); c.out_ready = b.template take<double>(V);
+    c.in_t = b.template take<double>(V); c.dout = b.template take<double>(V);
+    c.din = b.template take<double>(V); c.spans = b.template take<uint8_t>(V);
     name_rank = b.template take<int32_t>(V);
-    peaks = b.template take<double>(V + 1);
     order = b.template take<int32_t>(V);
-    delta = b.template take<int64_t>(p); ev_t = b.template take<double>(p); ev_d = b.template take<int64_t>(p);
+    peaks = b.template take<double>(V + 1);
+    tau = b.template take<double>(p);
+    delta = b.template take<int64_t>(p);
+    ev_t = b.template take<double>(p);
+    ev_d = b.template take<int64_t>(p);
   }
 };
 
-// the greedy's working set (shared memory when it fits)
+// candidates before compaction, and per-op scratch of the swap path
+struct SwapScratch {
+  int32_t *flag, *pos, *evpos, *cbase, *cralloc;
+  CandOut tmp;
+  int64_t *lmdiff;
+  template <class A>
+  __host__ __device__ void take(A &b, int64_t p, int64_t V) {
+    flag = b.template take<int32_t>(V); pos = b.template take<int32_t>(V);
+    cbase = b.template take<int32_t>(V); cralloc = b.template take<int32_t>(V);
+    evpos = b.template take<int32_t>(p + 1);
+    tmp.var = b.template take<int32_t>(V); tmp.out_index = b.template take<int32_t>(V);
+    tmp.in_index = b.template take<int32_t>(V); tmp.size = b.template take<int64_t>(V);
+    tmp.out_t = b.template take<double>(V); tmp.out_ready = b.template take<double>(V);
+    tmp.in_t = b.template take<double>(V); tmp.dout = b.template take<double>(V);
+    tmp.din = b.template take<double>(V); tmp.spans = b.template take<uint8_t>(V);
+    lmdiff = b.template take<int64_t>(p + 1);
+  }
+};
+
+// the greedy's working set
 struct GreedyArrays {
-  double *cur, *op_times;
+  double *cur;
   int64_t *W;
   int32_t *jx;
   uint8_t *taken;
   template <class A>
   __host__ __device__ void take(A &b, int64_t p, int64_t k) {
     cur = b.template take<double>(p);
-    op_times = b.template take<double>(p);
     W = b.template take<int64_t>(p + 1);
     jx = b.template take<int32_t>(2 * k);
     taken = b.template take<uint8_t>(k);
@@ -251,7 +265,8 @@ static size_t slab_bound(int64_t n, int64_t nv, int nb) {
   TimeArrays ta; ta.take(b, p);
   ProfileArrays pa; pa.take(b, p, V);
   PlaceArrays pl; pl.take(b, V);
-  SwapArrays sw; sw.take(b, p, V);
+  SwapKeep kp; kp.take(b, p, V);
+  SwapScratch ss; ss.take(b, p, V);
   GreedyArrays gr; gr.take(b, p, V);
   for (int i = 0; i < nb; i++) { BudgetArrays ba; ba.take(b, p, V); }
   return (b.top + 255) & ~(size_t)255;
@@ -343,19 +358,20 @@ struct SweepArgs {
 };
 
 #define SW_MARK(i) \
-  do { if (a.prof && threadIdx.x == 0) a.prof[t * 8 + (i)] = clock64(); } while (0)
+  do { if (a.prof && threadIdx.x == 0) a.prof[t * 16 + (i)] = clock64(); } while (0)
 
 struct SweepShared {
   unsigned long long first;
   long long best_p;
-  long long sm[33];     // CTA reductions
-  long long gsm[33];    // swap-group reductions (concurrent with placement)
+  long long sm[33];          // CTA reductions
+  long long gsm[PM_SMEM];    // swap-group reductions (concurrent with placement)
   double dur;
   long long edges;
   long long na;
   int bad, unsorted;
   double red[33];
   SwKey keys[33];
+  int lm_ok, ev_ok;
 };
 
 __device__ void sweep_fail(const SweepArgs &a, int64_t t, int status, int code, int64_t index,
@@ -548,12 +564,15 @@ __device__ void sweep_one(const SweepArgs &a, int64_t t, char *slab, char *fast,
   // ---- placement order + conflict rows (whole CTA), swap arrays ----
   SW_MARK(2);
   ar.phase();
+  SwapKeep kp;
+  kp.take(ar, p, V);
+  const size_t keep_top = ar.fast.top;  // the budget phase refills the arena from here
   PlaceArrays pl;
   pl.take(ar, V);
   GreedyArrays gr;
   gr.take(ar, p, V);
-  SwapArrays sw;
-  sw.take(bump, p, V);
+  SwapScratch ss;
+  ss.take(ar, p, V);
   if (bump.over) return sweep_fail(a, t, MP_E_NOMEM, 0, 0, R);
   for (int64_t i = tid; i < V; i += SW_THREADS) {
     pl.ksize[i] = pa.size[i];
@@ -603,131 +622,224 @@ __device__ void sweep_one(const SweepArgs &a, int64_t t, char *slab, char *fast,
   __syncthreads();
 
   int64_t k = 0, load_min = 0, live0 = 0, na = 0;
-  const LoadView L{p, loads, gr.op_times, dur};
-  const ProfView P{p, V, start, dur, ta.op_times, pa.nseg, pa.seg, pa.size};
+  const LoadView L{p, loads, kp.tau, dur};
+  const ProfView P{p, V, start, dur, kp.tau, pa.nseg, pa.seg, pa.size};
   if (warp == 0) {
     // ---- plan_pool (smartpool.py:122-144), concurrently with the swap path ----
     // One warp walks the order.  All placed ranges are kept in one list
     // sorted by start; a step scans it with its conflict row as the validity
     // mask, so the placed neighbours arrive already sorted and _pick_offset
-    // (smartpool.py:101-119) is one pass of hole_chunk — then the new range
+    // (smartpool.py:101-119) is one pass over it — then the new range
     // is inserted in order.
     int64_t edges = 0;
-    int cb = 0;
+    // the two list buffers, swapped each step (kept in registers)
+    int64_t *ls = pl.ls[0], *le = pl.le[0], *ds = pl.ls[1], *de = pl.le[1];
+    int32_t *lr = pl.lr[0], *dr = pl.lr[1];
+    long long c_scan = 0, c_ins = 0, c_t0 = clock64();
     for (int64_t q = 0; q < V; q++) {
       const uint32_t *row = pl.adj + q * pl.words;
+      long long c_a = clock64();
       const int64_t need = pl.rsize[q];
-      const int64_t *ls = pl.ls[cb], *le = pl.le[cb];
-      const int32_t *lr = pl.lr[cb];
       for (int64_t w = lane; w * 32 < q; w += 32) edges += __popc(row[w]);
-      HoleState h{0, 0, 0, false};
-      for (int64_t c0 = 0; c0 < q; c0 += 32) {
-        int64_t i = c0 + lane;
-        bool valid = false;
-        int64_t st = 0, en = 0;
-        if (i < q) {
-          int32_t j = lr[i];
-          valid = (row[j >> 5] >> (j & 31)) & 1u;
-          st = ls[i];
-          en = le[i];
+      // _pick_offset over the list, PL_K consecutive entries per lane: a hole
+      // opens where a start exceeds the running max of earlier ends
+      int64_t top = 0, ff_off = 0;
+      bool ff_found = false;
+      int64_t bl = INT64_MAX, bo = INT64_MAX;  // this lane's best fit (length, offset)
+      for (int64_t c0 = 0; c0 < q && !ff_found; c0 += 32 * PL_K) {
+        int64_t st[PL_K], en[PL_K];
+        bool valid[PL_K];
+        int64_t lmax = INT64_MIN;
+#pragma unroll
+        for (int jj = 0; jj < PL_K; jj++) {
+          int64_t i = c0 + lane * PL_K + jj;
+          valid[jj] = false;
+          st[jj] = en[jj] = 0;
+          if (i < q) {
+            int32_t j = lr[i];
+            valid[jj] = (row[j >> 5] >> (j & 31)) & 1u;
+            st[jj] = ls[i];
+            en[jj] = le[i];
+            if (valid[jj] && en[jj] > lmax) lmax = en[jj];
+          }
         }
-        if (hole_chunk(h, st, en, valid, need, prm.policy)) break;
+        int64_t incl = warp_incl_scan_max(lmax);
+        int64_t excl = __shfl_up_sync(FULL_MASK, incl, 1);
+        int64_t run = lane == 0 || excl < top ? top : excl;
+        bool mine = false;
+        int64_t my_off = 0;
+#pragma unroll
+        for (int jj = 0; jj < PL_K; jj++) {
+          if (!valid[jj]) continue;
+          if (st[jj] > run && st[jj] - run >= need) {
+            int64_t len = st[jj] - run;
+            if (!mine) { mine = true; my_off = run; }
+            if (len < bl || (len == bl && run < bo)) { bl = len; bo = run; }
+          }
+          if (en[jj] > run) run = en[jj];
+        }
+        if (prm.policy == 0) {
+          unsigned bal = __ballot_sync(FULL_MASK, mine);
+          if (bal) {
+            ff_off = __shfl_sync(FULL_MASK, my_off, __ffs(bal) - 1);
+            ff_found = true;
+          }
+        }
+        int64_t cmax = __shfl_sync(FULL_MASK, incl, 31);
+        if (cmax > top) top = cmax;
       }
-      const int64_t off = h.found ? h.best_off : h.top;
+      int64_t off;
+      if (prm.policy == 0) {
+        off = ff_found ? ff_off : top;
+      } else {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          int64_t ol = __shfl_xor_sync(FULL_MASK, bl, o), oo = __shfl_xor_sync(FULL_MASK, bo, o);
+          if (ol < bl || (ol == bl && oo < bo)) { bl = ol; bo = oo; }
+        }
+        off = bl != INT64_MAX ? bo : top;
+      }
+      long long c_b = clock64();
+      c_scan += c_b - c_a;
       // insert (off, off + need, q) before the first range starting at or after off
       int64_t pos = 0;
       for (int64_t c0 = 0; c0 < q; c0 += 32) {
         int64_t i = c0 + lane;
         pos += __popc(__ballot_sync(FULL_MASK, i < q && ls[i] < off));
       }
-      int64_t *ds = pl.ls[cb ^ 1], *de = pl.le[cb ^ 1];
-      int32_t *dr = pl.lr[cb ^ 1];
       for (int64_t i = lane; i <= q; i += 32) {
         if (i < pos) { ds[i] = ls[i]; de[i] = le[i]; dr[i] = lr[i]; }
         else if (i == pos) { ds[i] = off; de[i] = off + need; dr[i] = (int32_t)q; }
         else { ds[i] = ls[i - 1]; de[i] = le[i - 1]; dr[i] = lr[i - 1]; }
       }
-      cb ^= 1;
+      { int64_t *x = ls; ls = ds; ds = x; x = le; le = de; de = x; int32_t *y = lr; lr = dr; dr = y; }
       __syncwarp();
+      c_ins += clock64() - c_b;
     }
+    if (lane == 0 && a.prof) { a.prof[t * 16 + 8] = c_t0; a.prof[t * 16 + 9] = clock64(); a.prof[t * 16 + 10] = c_scan; a.prof[t * 16 + 11] = c_ins; }
     edges = warp_sum(edges);
     // scatter offsets back to profile order
-    for (int64_t i = lane; i < V; i += 32) offs[pl.order[pl.lr[cb][i]]] = pl.ls[cb][i];
+    for (int64_t i = lane; i < V; i += 32) offs[pl.order[lr[i]]] = ls[i];
     if (lane == 0) sh.edges = edges;
   } else {
     // ---- AutoSwap on warps 1..: candidates, load_min, SWDOA greedy ----
     const WarpGroup sg{1, SW_WARPS - 1, 1};
     const int gi = sg.idx(), gn = sg.size();
     for (int64_t v = gi; v < V; v += gn)
-      sw.flag[v] = cand_item(v, v, p, peak_index, pa.size, pa.flags, pa.acc_off, pa.acc_index, pa.acc_next,
-                             ta.op_times, dur, prm.threshold, prm.bw, prm.lat, sw.tmp);
-    for (int64_t r = gi; r < p; r += gn) gr.op_times[r] = ta.op_times[r];
-    sg.sync();
-    k = grp_excl_scan(sg, sw.flag, sw.pos, V, sh.gsm);
-    for (int64_t v = gi; v < V; v += gn) {
-      if (!sw.flag[v]) continue;
-      int64_t q = sw.pos[v];
-      sw.c.var[q] = sw.tmp.var[v]; sw.c.out_index[q] = sw.tmp.out_index[v]; sw.c.in_index[q] = sw.tmp.in_index[v];
-      sw.c.size[q] = sw.tmp.size[v]; sw.c.out_t[q] = sw.tmp.out_t[v]; sw.c.out_ready[q] = sw.tmp.out_ready[v];
-      sw.c.in_t[q] = sw.tmp.in_t[v]; sw.c.dout[q] = sw.tmp.dout[v]; sw.c.din[q] = sw.tmp.din[v];
-      sw.c.spans[q] = sw.tmp.spans[v];
+      ss.flag[v] = cand_item(v, v, p, peak_index, pa.size, pa.flags, pa.acc_off, pa.acc_index, pa.acc_next,
+                             ta.op_times, dur, prm.threshold, prm.bw, prm.lat, ss.tmp);
+    for (int64_t r = gi; r < p; r += gn) {
+      kp.tau[r] = ta.op_times[r];
+      kp.delta[r] = 0;
     }
     sg.sync();
-    // candidate name ranks: final names, "base#alloc" for renamed instances
+    k = grp_excl_scan(sg, ss.flag, ss.pos, V, sh.gsm);
+    CandOut &cc = kp.c;
+    for (int64_t v = gi; v < V; v += gn) {
+      if (!ss.flag[v]) continue;
+      int64_t q = ss.pos[v];
+      cc.var[q] = ss.tmp.var[v]; cc.out_index[q] = ss.tmp.out_index[v]; cc.in_index[q] = ss.tmp.in_index[v];
+      cc.size[q] = ss.tmp.size[v]; cc.out_t[q] = ss.tmp.out_t[v]; cc.out_ready[q] = ss.tmp.out_ready[v];
+      cc.in_t[q] = ss.tmp.in_t[v]; cc.dout[q] = ss.tmp.dout[v]; cc.din[q] = ss.tmp.din[v];
+      cc.spans[q] = ss.tmp.spans[v];
+      // the candidate's final name: base id, "#alloc" suffix when renamed
+      ss.cbase[q] = pa.base[v];
+      ss.cralloc[q] = (pa.flags[v] & MP_F_RENAMED) ? pa.alloc[v] : -1;
+    }
+    sg.sync();
     NameTable names{a.blob, a.name_off + a.var_off[t]};
     for (int64_t i = gi; i < k; i += gn) {
-      int32_t vi = sw.c.var[i];
-      int32_t bi = pa.base[vi], ri = (pa.flags[vi] & MP_F_RENAMED) ? pa.alloc[vi] : -1;
+      const int32_t bi = ss.cbase[i], ri = ss.cralloc[i];
       int32_t rank = 0;
-      for (int64_t j = 0; j < k; j++) {
-        int32_t vj = sw.c.var[j];
-        int32_t bj = pa.base[vj], rj = (pa.flags[vj] & MP_F_RENAMED) ? pa.alloc[vj] : -1;
-        rank += name_cmp(names, bj, rj, bi, ri) < 0;
-      }
-      sw.name_rank[i] = rank;
+      for (int64_t j = 0; j < k; j++) rank += name_cmp(names, ss.cbase[j], ss.cralloc[j], bi, ri) < 0;
+      kp.name_rank[i] = rank;
     }
     sg.sync();
-    const CandView cv{k, sw.c.size, sw.c.out_index, sw.c.in_index, sw.name_rank, sw.c.out_t, sw.c.out_ready,
-                      sw.c.in_t, sw.c.dout, sw.c.din, sw.c.spans};
-    // compute_load_min (swapsim.py:398-405): every candidate absent
+    const CandView cv{k, cc.size, cc.out_index, cc.in_index, kp.name_rank, cc.out_t, cc.out_ready,
+                      cc.in_t, cc.dout, cc.din, cc.spans};
+    // compute_load_min (swapsim.py:398-405): every candidate absent.  While
+    // every load and size sum is an integer below 2^53 the reference's float
+    // subtractions are exact, so a difference array over the absence ranges
+    // gives the same values; otherwise the slot-parallel fold runs.
+    long long szsum = 0;
+    bool short_gaps = true;
+    for (int64_t q = gi; q < k; q += gn) {
+      szsum += cv.size[q];
+      short_gaps &= cv.in_index[q] + (cv.spans[q] ? p : 0) - cv.out_index[q] - 1 <= p;
+    }
+    for (int64_t r = gi; r <= p; r += gn) ss.lmdiff[r] = 0;
+    szsum = grp_sum(sg, szsum, sh.gsm);
+    const bool lm_fast = sg.sync_and(short_gaps) && (double)peak < EXACT_2_53 && (double)szsum < EXACT_2_53;
     double lm = -INF_D;
-    bool have = false;
-    for (int64_t r = gi; r < p; r += gn) {
-      double cur = (double)loads[r];
-      for (int64_t q = 0; q < k; q++) {
-        int64_t lo = cv.out_index[q], hi = cv.in_index[q] + (cv.spans[q] ? p : 0);
-        int h = absence_hits(r, lo, hi, p);
-        for (int z = 0; z < h; z++) cur -= (double)cv.size[q];
+    if (lm_fast) {
+      for (int64_t q = gi; q < k; q += gn) {
+        int64_t lo = cv.out_index[q] + 1, hi = cv.in_index[q] + (cv.spans[q] ? p : 0);  // slots [lo, hi)
+        unsigned long long neg = (unsigned long long)(-cv.size[q]), pos = (unsigned long long)cv.size[q];
+        if (lo >= hi) continue;
+        if (hi <= p) {
+          atomicAdd((unsigned long long *)&ss.lmdiff[lo], neg);
+          atomicAdd((unsigned long long *)&ss.lmdiff[hi], pos);
+        } else {
+          if (lo < p) {
+            atomicAdd((unsigned long long *)&ss.lmdiff[lo], neg);
+            atomicAdd((unsigned long long *)&ss.lmdiff[p], pos);
+            lo = p;
+          }
+          atomicAdd((unsigned long long *)&ss.lmdiff[lo - p], neg);
+          atomicAdd((unsigned long long *)&ss.lmdiff[hi - p], pos);
+        }
       }
-      lm = have ? pymax(lm, cur) : cur;
-      have = true;
+      sg.sync();
+      grp_excl_scan(sg, ss.lmdiff, ss.lmdiff, p + 1, sh.gsm);
+      // diff[r+1] after the exclusive scan = sum of diff[0..r]
+      for (int64_t r = gi; r < p; r += gn) {
+        double cur = (double)(loads[r] + ss.lmdiff[r + 1]);
+        lm = r == gi ? cur : pymax(lm, cur);
+      }
+    } else {
+      for (int64_t r = gi; r < p; r += gn) {
+        double cur = (double)loads[r];
+        for (int64_t q = 0; q < k; q++) {
+          int64_t lo = cv.out_index[q], hi = cv.in_index[q] + (cv.spans[q] ? p : 0);
+          int h = absence_hits(r, lo, hi, p);
+          for (int z = 0; z < h; z++) cur -= (double)cv.size[q];
+        }
+        lm = r == gi ? cur : pymax(lm, cur);
+      }
     }
     load_min = (int64_t)block_max(sg, lm, sh.red);
-    if (gi == 0 && a.prof) a.prof[t * 8 + 3] = clock64();
-    swdoa_greedy_block(sg, L, cv, gr.cur, gr.taken, nullptr, nullptr, nullptr, nullptr, sw.order, sw.peaks, gr.W,
-                       gr.jx, sh.red, sh.keys, sh.gsm);
-    if (gi == 0 && a.prof) a.prof[t * 8 + 4] = clock64();
-    for (int64_t q = gi; q < k; q += gn) corder[q] = sw.c.var[sw.order[q]];
+    if (gi == 0 && a.prof) a.prof[t * 16 + 3] = clock64();
+    swdoa_greedy_block(sg, L, cv, gr.cur, gr.taken, nullptr, nullptr, nullptr, nullptr, kp.order, kp.peaks, gr.W,
+                       gr.jx, sh.keys, sh.gsm);
+    if (gi == 0 && a.prof) a.prof[t * 16 + 4] = clock64();
+    for (int64_t q = gi; q < k; q += gn) corder[q] = cc.var[kp.order[q]];
     // ---- simulate prerequisites: _op_deltas and the sorted op events ----
-    for (int64_t r = gi; r < p; r += gn) sw.delta[r] = 0;
-    sg.sync();
     long long l0 = 0;
     for (int64_t i = gi; i < V; i += gn)
       for (int q = 0; q < pa.nseg[i]; q++) {
         int64_t lo = pa.seg[4 * i + 2 * q], hi = pa.seg[4 * i + 2 * q + 1];
         if (lo == 0) l0 += pa.size[i];
-        else atomicAdd((unsigned long long *)&sw.delta[lo], (unsigned long long)pa.size[i]);
-        if (hi < p) atomicAdd((unsigned long long *)&sw.delta[hi], (unsigned long long)(-pa.size[i]));
+        else atomicAdd((unsigned long long *)&kp.delta[lo], (unsigned long long)pa.size[i]);
+        if (hi < p) atomicAdd((unsigned long long *)&kp.delta[hi], (unsigned long long)(-pa.size[i]));
       }
     live0 = grp_sum(sg, l0, sh.gsm);
-    // _overlay_curve's op events (t, delta != 0) in (t, delta) order
-    if (gi == 0) {
-      na = sim_op_events(P, sw.delta, sw.ev_t, sw.ev_d);
-      sh.na = na;
-    }
+    // _overlay_curve's op events (t, delta != 0), swapsim.py:184-193: compacted
+    // in op order, which is (t, delta) order unless equal times run backwards
+    for (int64_t r = gi; r < p; r += gn) ss.evpos[r] = kp.delta[r] != 0;
     sg.sync();
-    na = sh.na;
-    if (gi == 0 && a.prof) a.prof[t * 8 + 5] = clock64();
+    na = grp_excl_scan(sg, ss.evpos, ss.evpos, p, sh.gsm);
+    for (int64_t r = gi; r < p; r += gn)
+      if (kp.delta[r] != 0) {
+        kp.ev_t[ss.evpos[r]] = kp.tau[r];
+        kp.ev_d[ss.evpos[r]] = kp.delta[r];
+      }
+    sg.sync();
+    bool sorted = true;
+    for (int64_t q = gi; q + 1 < na; q += gn) sorted &= !td_less(kp.ev_t[q + 1], kp.ev_d[q + 1], kp.ev_t[q], kp.ev_d[q]);
+    if (!sg.sync_and(sorted) && gi == 0) sim_op_events(P, kp.delta, kp.ev_t, kp.ev_d);
+    if (gi == 0) sh.na = na;
+    sg.sync();
+    if (gi == 0 && a.prof) a.prof[t * 16 + 5] = clock64();
   }
   __syncthreads();
   R.edges = sh.edges;
@@ -751,12 +863,12 @@ __device__ void sweep_one(const SweepArgs &a, int64_t t, char *slab, char *fast,
   }
   const int64_t foot = grp_max(cta, fe, sh.sm);
   R.footprint_bytes = V ? foot : 0;
-  const CandView cv{k, sw.c.size, sw.c.out_index, sw.c.in_index, sw.name_rank, sw.c.out_t, sw.c.out_ready,
-                    sw.c.in_t, sw.c.dout, sw.c.din, sw.c.spans};
+  const CandView cv{k, kp.c.size, kp.c.out_index, kp.c.in_index, kp.name_rank, kp.c.out_t, kp.c.out_ready,
+                    kp.c.in_t, kp.c.dout, kp.c.din, kp.c.spans};
 
   // ---- per budget: SwapPlanner(limit, score="swdoa").fit, one warp each ----
   SW_MARK(6);
-  ar.phase();
+  ar.fast.top = keep_top;
   BudgetArrays ba[MP_SWEEP_MAX_BUDGETS];
   for (int b = 0; b < prm.nbudget; b++) ba[b].take(ar, p, k);
   if (bump.over) return sweep_fail(a, t, MP_E_NOMEM, 0, 0, R);
@@ -773,15 +885,15 @@ __device__ void sweep_one(const SweepArgs &a, int64_t t, char *slab, char *fast,
       // select_by_swdoa: the greedy stops at the first planned peak <= limit
       int64_t m = -1;
       for (int64_t j = 0; j <= k; j++)
-        if (f_le_i(sw.peaks[j], limit)) { m = j; break; }
+        if (f_le_i(kp.peaks[j], limit)) { m = j; break; }
       if (m < 0) {
         rb.status = MP_E_LIMIT_UNREACHABLE;  // autoswap.py:222-224
-        rb.err_aux = (int64_t)sw.peaks[k];
+        rb.err_aux = (int64_t)kp.peaks[k];
       } else {
         SimScratch S = ba[b].S;
-        S.delta = sw.delta;
+        S.delta = kp.delta;
         const SimTimes &T = ba[b].T;
-        const int32_t *sel = sw.order;
+        const int32_t *sel = kp.order;
         long long bytes = 0;
         for (int64_t q = lane; q < m; q += 32) {
           S.ready[q] = cv.out_ready[sel[q]];   // build_schedule, swapsim.py:111-116
@@ -792,7 +904,7 @@ __device__ void sweep_one(const SweepArgs &a, int64_t t, char *slab, char *fast,
         __syncwarp();
         make_schedule(cv, sel, m, S.ready, S.deadline, T.t_so, T.t_eo, T.t_si, T.t_ei, T.eord, S);
         PeakCurve lp{};
-        sim_overlay(P, cv, sel, m, live0, T.t_eo, T.t_si, T.eord, sw.ev_t, sw.ev_d, na, S, lp);
+        sim_overlay(P, cv, sel, m, live0, T.t_eo, T.t_si, T.eord, kp.ev_t, kp.ev_d, na, S, lp);
         Replay<PeakCurve> rep{};
         SimResult res = sim_fixed_point<false>(P, cv, sel, m, limit, 1, prm.max_rounds, live0, S, T, rep);
         rb.status = res.status;
@@ -974,14 +1086,14 @@ extern "C" int mp_sweep_download(mp_ctx *ctx, mp_dsweep *s, mp_sweep_trace *trac
 
 extern "C" int mp_sweep_set_profile(mp_ctx *ctx, mp_dsweep *s, int on, mp_err *err) {
   if (!on) { s->prof.release(); return MP_OK; }
-  CUDA_TRY(s->prof.alloc(s->T * 8 > 0 ? s->T * 8 : 1, ctx->stream));
-  CUDA_TRY(cudaMemsetAsync(s->prof.p, 0, (s->T * 8 > 0 ? s->T * 8 : 1) * 8, ctx->stream));
+  CUDA_TRY(s->prof.alloc(s->T * 16 > 0 ? s->T * 16 : 1, ctx->stream));
+  CUDA_TRY(cudaMemsetAsync(s->prof.p, 0, (s->T * 16 > 0 ? s->T * 16 : 1) * 8, ctx->stream));
   return MP_OK;
 }
 
 extern "C" int mp_sweep_profile_download(mp_ctx *ctx, mp_dsweep *s, long long *out, mp_err *err) {
   if (!s->prof.p) { mp_set_err(err, MP_E_VALUE, 0, 0, 0, "profiling is off"); return MP_E_VALUE; }
-  CUDA_TRY(cudaMemcpyAsync(out, s->prof.p, s->T * 8 * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaMemcpyAsync(out, s->prof.p, s->T * 16 * 8, cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   return MP_OK;
 }

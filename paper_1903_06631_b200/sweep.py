@@ -263,10 +263,11 @@ class DeviceSweep:
         extract, plan, candidates, greedy, simulate prep, budgets."""
         L = _lib()
         L.mp_sweep_profile_download.restype = C.c_int
-        out = np.zeros((max(self.batch.ntraces, 1), 8), np.int64)
+        out = np.zeros((max(self.batch.ntraces, 1), 16), np.int64)
         err = MpErr()
         raise_for(L.mp_sweep_profile_download(N.ctx(), self._h, ptr(out), C.byref(err)), err)
-        return np.diff(out[:self.batch.ntraces], axis=1)
+        self.profile_extra = out[:self.batch.ntraces, 8:]
+        return np.diff(out[:self.batch.ntraces, :8], axis=1)
 
     def close(self):
         if self._h:

@@ -75,6 +75,9 @@ def main():
     print("phase cycles: median over traces / the 5 slowest traces")
     for j, nm in enumerate(names):
         print(f"  {nm:24s} med {int(np.median(prof[:, j])):>9d}  " + " ".join(f"{int(prof[t, j]):>9d}" for t in top))
+    ex = ds.profile_extra
+    print("  placement loop cycles (5 slowest):", [int(ex[t, 1] - ex[t, 0]) for t in top],
+          "scan", [int(ex[t, 2]) for t in top], "insert", [int(ex[t, 3]) for t in top])
     print("  slowest traces:", [(int(t), batch.events_of(int(t)), int(res.traces['nvars'][t]), int(res.traces['ncand'][t])) for t in top])
     t0 = time.perf_counter()
     recs, brecs, offs, orders = orc.sweep(batch, prm)
