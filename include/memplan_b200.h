@@ -375,6 +375,25 @@ int mp_sweep_set_profile(mp_ctx *ctx, mp_dsweep *s, int on, mp_err *err);
 int mp_sweep_profile_download(mp_ctx *ctx, mp_dsweep *s, long long *out /* [ntraces * 16]: 8 marks + 8 counters */,
                               mp_err *err);
 
+/* ---------------------------------------------------------------------- */
+/* Native trace reader (host, threads): trace.py:87-151 for the canonical   */
+/* record forms serialize_trace writes.  format 0 = JSONL, 1 = CSV.         */
+/* Lines outside the canonical grammar are not decoded here: their 1-based  */
+/* numbers come back as "slow lines" for the reference decoder, so every    */
+/* MalformedRecord keeps its line and reason.  MP_E_UNSUPPORTED: the whole  */
+/* buffer needs the reference reader (line separators other than \n/\r\n, */
+/* CSV quoting, a missing or different CSV header).  Var ids are            */
+/* lexicographic ranks of the names.  threads <= 0: all host cores.        */
+
+typedef struct mp_reader mp_reader;
+
+int mp_read_trace(const char *data, int64_t nbytes, int32_t format, int32_t threads, mp_reader **out,
+                  mp_err *err);
+int mp_reader_dims(mp_reader *r, int64_t *n, int64_t *nvars, int64_t *name_bytes, int64_t *nslow);
+int mp_reader_copy(mp_reader *r, uint8_t *kind, int32_t *var, int64_t *size, int64_t *t_us, int64_t *index,
+                   int64_t *line, uint8_t *name_blob, int64_t *name_off, int64_t *slow_lines);
+int mp_reader_free(mp_reader *r);
+
 #ifdef __cplusplus
 }
 #endif

@@ -79,7 +79,7 @@ class TraceArrays:
     input), so the validator can report the reference's first error.
     """
 
-    __slots__ = ("kind", "var", "size", "t_us", "index", "names",
+    __slots__ = ("kind", "var", "size", "t_us", "index", "_names",
                  "name_blob", "name_off", "_meta", "_dev")
 
     def __init__(self, kind, var, size, t_us, names: Sequence[str],
@@ -89,8 +89,8 @@ class TraceArrays:
         self.size = np.ascontiguousarray(size, dtype=np.int64)
         self.t_us = np.ascontiguousarray(t_us, dtype=np.int64)
         self.index = None if index is None else np.ascontiguousarray(index, dtype=np.int64)
-        self.names = list(names)
-        blobs = [s.encode("utf-8") for s in self.names]
+        self._names = list(names)
+        blobs = [s.encode("utf-8") for s in self._names]
         off = np.zeros(len(blobs) + 1, dtype=np.int64)
         if blobs:
             off[1:] = np.cumsum([len(b) for b in blobs])
@@ -99,12 +99,38 @@ class TraceArrays:
         self._meta = None
         self._dev = None
 
+    @classmethod
+    def from_blob(cls, kind, var, size, t_us, name_blob, name_off, index=None) -> "TraceArrays":
+        """Columns plus names already packed (UTF-8 blob + offsets, sorted);
+        the Python strings are decoded only if someone asks for them."""
+        self = cls.__new__(cls)
+        self.kind = np.ascontiguousarray(kind, dtype=np.uint8)
+        self.var = np.ascontiguousarray(var, dtype=np.int32)
+        self.size = np.ascontiguousarray(size, dtype=np.int64)
+        self.t_us = np.ascontiguousarray(t_us, dtype=np.int64)
+        self.index = None if index is None else np.ascontiguousarray(index, dtype=np.int64)
+        self._names = None
+        self.name_blob = np.ascontiguousarray(name_blob, dtype=np.uint8)
+        self.name_off = np.ascontiguousarray(name_off, dtype=np.int64)
+        if self.name_blob.size == 0:
+            self.name_blob = np.zeros(1, np.uint8)
+        self._meta = None
+        self._dev = None
+        return self
+
+    @property
+    def names(self) -> list[str]:
+        if self._names is None:
+            b, off = self.name_blob.tobytes(), self.name_off.tolist()
+            self._names = [b[off[i]:off[i + 1]].decode("utf-8") for i in range(len(off) - 1)]
+        return self._names
+
     def __len__(self) -> int:
         return int(self.kind.shape[0])
 
     @property
     def nvars(self) -> int:
-        return len(self.names)
+        return int(self.name_off.shape[0] - 1)
 
     @classmethod
     def from_columns(cls, kind, var_names, size, t_us, index=None) -> "TraceArrays":
@@ -222,17 +248,121 @@ def _read_csv(text: str) -> list[TraceEvent]:
     return out
 
 
+def _native_reader():
+    """The device library's host-side reader entry points (None when the
+    library is absent: text decoding is host plumbing, the Python reader is
+    the reference semantics)."""
+    try:
+        from . import _native
+        L = _native.lib()
+    except Exception:  # noqa: BLE001
+        return None
+    import ctypes as C
+    for name in ("mp_read_trace", "mp_reader_dims", "mp_reader_copy", "mp_reader_free"):
+        getattr(L, name).restype = C.c_int
+    return L
+
+
+def _slow_line(fmt: str, line_no: int, line: str):
+    """Decode one line with the reference semantics: None for a skipped line,
+    else the event; MalformedRecord as the reference raises it."""
+    if fmt == "jsonl":
+        if not line.strip():
+            return None
+        return _read_jsonl_line(line_no, line)
+    row = next(csv.reader([line]), [])
+    if not row:
+        return None
+    if len(row) != 5:
+        raise MalformedRecord(line_no, f"expected 5 fields, got {len(row)}")
+    return _record(line_no, *row)
+
+
+def _read_jsonl_line(line_no: int, line: str) -> TraceEvent:
+    try:
+        rec = json.loads(line)
+    except json.JSONDecodeError as exc:
+        raise MalformedRecord(line_no, f"bad JSON: {exc.msg}")
+    want = set(JSONL_KEYS)
+    if not isinstance(rec, dict) or set(rec) != want:
+        raise MalformedRecord(line_no, f"keys must be exactly {want}")
+    return _record(line_no, *(rec[k] for k in JSONL_KEYS))
+
+
+def read_trace_arrays(data: bytes | str, format: str = "jsonl", threads: int = 0) -> TraceArrays:
+    """Decode JSONL/CSV text straight into columns, without validation.
+
+    The canonical records (what serialize_trace writes) are decoded by the
+    native multi-threaded reader (csrc/reader.cpp); any other line is decoded
+    by the reference semantics (trace.py:87-137), so a MalformedRecord carries
+    the reference's line and reason.  Var ids are lexicographic name ranks.
+    """
+    if format not in ("jsonl", "csv"):
+        raise ValueError(f"unknown format {format!r}")
+    if isinstance(data, str):
+        text, raw = data, data.encode("utf-8")
+    else:
+        raw = bytes(data)
+        text = raw.decode("utf-8")  # UnicodeDecodeError exactly as the reference's decode
+    L = _native_reader()
+    if L is None:
+        return as_arrays(_read_jsonl(text) if format == "jsonl" else _read_csv(text))
+    import ctypes as C
+
+    from ._abi import MP_E_UNSUPPORTED, MP_OK, MpErr, raise_for
+    h = C.c_void_p()
+    err = MpErr()
+    rc = L.mp_read_trace(C.c_char_p(raw), C.c_int64(len(raw)), C.c_int32(0 if format == "jsonl" else 1),
+                         C.c_int32(threads), C.byref(h), C.byref(err))
+    if rc == MP_E_UNSUPPORTED:
+        return as_arrays(_read_jsonl(text) if format == "jsonl" else _read_csv(text))
+    raise_for(rc, err)
+    try:
+        n, nv, nb, ns = (C.c_int64() for _ in range(4))
+        L.mp_reader_dims(h, C.byref(n), C.byref(nv), C.byref(nb), C.byref(ns))
+        n, nv, nb, ns = n.value, nv.value, nb.value, ns.value
+        kind = np.empty(n, np.uint8)
+        var = np.empty(n, np.int32)
+        size = np.empty(n, np.int64)
+        t_us = np.empty(n, np.int64)
+        index = np.empty(n, np.int64)
+        line = np.empty(n, np.int64)
+        blob = np.empty(max(nb, 1), np.uint8)
+        off = np.empty(nv + 1, np.int64)
+        slow = np.empty(max(ns, 1), np.int64)
+        p = lambda a: C.c_void_p(a.ctypes.data)  # noqa: E731
+        L.mp_reader_copy(h, p(kind), p(var), p(size), p(t_us), p(index), p(line), p(blob), p(off), p(slow))
+    finally:
+        L.mp_reader_free(h)
+    if ns:
+        lines = text.split("\n")
+        extra = False
+        for ln in slow[:ns].tolist():
+            s = lines[ln - 1]
+            if s.endswith("\r"):
+                s = s[:-1]
+            if _slow_line(format, ln, s) is not None:
+                extra = True  # a valid non-canonical record: decode the file the reference way
+        if extra:
+            return as_arrays(_read_jsonl(text) if format == "jsonl" else _read_csv(text))
+    contiguous = n == 0 or bool(np.array_equal(index, np.arange(n, dtype=np.int64)))
+    return TraceArrays.from_blob(kind, var, size, t_us, blob[:max(nb, 1)], off, None if contiguous else index)
+
+
+def load_trace_arrays(path, format: str | None = None, threads: int = 0) -> TraceArrays:
+    """load_trace without materializing events: a file straight to columns."""
+    path = str(path)
+    with open(path, "rb") as fh:
+        return read_trace_arrays(fh.read(), format=_fmt_of(path, format), threads=threads)
+
+
 def parse_trace(data: bytes | str, format: str = "jsonl") -> Trace:
     """Decode JSONL/CSV text and validate it (trace.py:140-151)."""
-    if isinstance(data, bytes):
-        data = data.decode("utf-8")
-    if format == "jsonl":
-        events = _read_jsonl(data)
-    elif format == "csv":
-        events = _read_csv(data)
-    else:
+    if format not in ("jsonl", "csv"):
         raise ValueError(f"unknown format {format!r}")
-    trace = Trace(events=events)
+    arrays = read_trace_arrays(data, format)
+    trace = arrays.to_trace()
+    trace.__dict__["_mp_arrays"] = ((id(trace.events), len(trace.events)), arrays)
     validate_trace(trace)
     return trace
 
