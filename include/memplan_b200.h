@@ -286,6 +286,17 @@ typedef struct mp_sim_io {
 int mp_swap_simulate(mp_ctx *ctx, mp_dprofile *p, const mp_cands_io *c, const int32_t *sel, int64_t n,
                      int64_t limit, int32_t has_limit, int32_t max_rounds, mp_sim_io *io, mp_err *err);
 
+/* Batched BO objective (SwapPlanner score="bo", estimators.py:114-120):
+ * for each of m weight vectors (aoa, doa, wdoa, swdoa) the combined-score
+ * selection (autoswap.py:269-317) + build_schedule + simulate at `limit`,
+ * one warp per vector.  z = the candidates' standardized scores [4][k]
+ * (mp_standardize, SCORE_NAMES order).  Per vector: status (MP_OK,
+ * MP_E_LIMIT_UNREACHABLE with aux = int(peak), MP_E_SWAP_DEADLOCK with
+ * aux = index, MP_E_SIM_INDEXERROR), overhead_us, nsel. */
+int mp_swap_eval_weights(mp_ctx *ctx, mp_dprofile *p, const mp_cands_io *c, const double *z,
+                         const double *weights, int64_t m, int64_t limit, int32_t max_rounds, int32_t *status,
+                         double *overhead, int64_t *nsel, int64_t *aux, mp_err *err);
+
 /* CPython-3.12 compatible standardize (autoswap.py:228-238): Neumaier
  * sum() and libm pow — host code, since device pow differs from glibc's */
 int mp_standardize(const double *x, int64_t n, double *out);

@@ -398,6 +398,23 @@ def swap_simulate(dp: DProfile, period: int, c: Cands, sel, sched, limit, max_ro
                 rounds=int(io.rounds))
 
 
+def swap_eval_weights(dp: DProfile, c: Cands, z, weights, limit: int, max_rounds: int = 100):
+    """Batched BO objective (mp_swap_eval_weights): per weight vector
+    (status, overhead_us, nsel, aux)."""
+    w = np.ascontiguousarray(weights, np.float64).reshape(-1, 4)
+    m = w.shape[0]
+    zz = np.ascontiguousarray(z, np.float64).reshape(4, -1) if c.k else np.zeros((4, 1))
+    st = np.zeros(max(m, 1), np.int32)
+    ov = np.zeros(max(m, 1))
+    ns = np.zeros(max(m, 1), np.int64)
+    ax = np.zeros(max(m, 1), np.int64)
+    err = MpErr()
+    rc = lib().mp_swap_eval_weights(ctx(), dp.h, C.byref(c.io()), ptr(zz), ptr(w), C.c_int64(m), C.c_int64(limit),
+                                    C.c_int32(max_rounds), ptr(st), ptr(ov), ptr(ns), ptr(ax), C.byref(err))
+    raise_for(rc, err)
+    return st[:m], ov[:m], ns[:m], ax[:m]
+
+
 def standardize(x) -> np.ndarray:
     x = np.ascontiguousarray(x, np.float64)
     out = np.zeros(max(x.shape[0], 1))

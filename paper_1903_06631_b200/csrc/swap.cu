@@ -535,3 +535,212 @@ extern "C" int mp_swap_simulate(mp_ctx *ctx, mp_dprofile *P, const mp_cands_io *
   CUDA_TRY(cudaStreamSynchronize(st));
   return MP_OK;
 }
+
+// ---------------------------------------------------------------------------
+// batched BO evaluator: the SwapPlanner(score="bo") objective for m weight
+// vectors at once (estimators.py:114-120 -> _select_and_simulate with
+// score="combined"), one warp per vector:
+//   combined_scores  autoswap.py:269-282  sum over SCORE_NAMES of w * z (the
+//                                         z-scores are weight-free: host C)
+//   select_by_score  autoswap.py:303-317  static order (-score, -size, name),
+//                                         insert until max(cur) <= limit
+//   build_schedule + simulate             the warp-collective replay above
+// Only the overhead (and failures) come back: the winning weights are
+// re-run through the regular path by the caller.
+
+struct EvalArgs {
+  LoadView L;
+  ProfView P;
+  CandView c;
+  const double *z;   // [4][k]: standardized aoa, doa, wdoa, swdoa
+  const double *w;   // [m][4]
+  int64_t m, limit;
+  int max_rounds;
+  const unsigned long long *live0;
+  const int64_t *delta;
+  const double *ev_t;
+  const int64_t *ev_d;
+  const int64_t *na;
+  char *scratch;
+  size_t per_warp;
+  int32_t *status, *rounds;
+  double *overhead;
+  int64_t *nsel, *aux;
+};
+
+struct EvalScratch {
+  double *comb, *cur;
+  int32_t *ord, *sel;
+  SimScratch S;
+  SimTimes T;
+};
+
+template <class A>
+__host__ __device__ void eval_take(A &b, EvalScratch &x, int64_t p, int64_t k) {
+  x.comb = b.template take<double>(k); x.cur = b.template take<double>(p);
+  x.ord = b.template take<int32_t>(k); x.sel = b.template take<int32_t>(k);
+  SimScratch &S = x.S;
+  S.ord = b.template take<int32_t>(k); S.desired = b.template take<double>(k);
+  S.in_order = b.template take<int32_t>(k); S.plan_in = b.template take<double>(k);
+  S.in_done = b.template take<double>(k); S.in_has = b.template take<uint8_t>(k);
+  S.comp_t = b.template take<double>(k); S.comp_sz = b.template take<int64_t>(k);
+  S.out_trigger = b.template take<int32_t>(p); S.in_wait = b.template take<int32_t>(p);
+  S.busy_op = b.template take<uint32_t>((p + 31) / 32);
+  S.actual = b.template take<double>(p);
+  S.ready = b.template take<double>(k); S.deadline = b.template take<double>(k);
+  S.ev2_t = b.template take<double>(2 * k); S.ev2_d = b.template take<int64_t>(2 * k);
+  S.ev2_ord = b.template take<int32_t>(2 * k);
+  x.T.t_so = b.template take<double>(k); x.T.t_eo = b.template take<double>(k);
+  x.T.t_si = b.template take<double>(k); x.T.t_ei = b.template take<double>(k);
+  x.T.eord = b.template take<int32_t>(k);
+}
+
+struct LinearAlloc {  // bump allocation over one warp's scratch (count-only when base is null)
+  char *base;
+  size_t top;
+  template <typename T>
+  __host__ __device__ T *take(int64_t n) {
+    size_t a = (top + 15) & ~(size_t)15;
+    top = a + (size_t)(n > 0 ? n : 1) * sizeof(T);
+    return base ? reinterpret_cast<T *>(base + a) : nullptr;
+  }
+};
+
+__device__ __forceinline__ double warp_pymax_cur(const double *cur, int64_t p) {
+  const int lane = threadIdx.x & 31;
+  double m = -INF_D;
+  for (int64_t r = lane; r < p; r += 32) m = r == lane ? cur[r] : pymax(m, cur[r]);
+  // lanes hold interleaved slots: the maximum value is the same whichever
+  // copy is kept (a tie is the same double)
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = pymax(m, __shfl_xor_sync(FULL_MASK, m, o));
+  return m;
+}
+
+__global__ void k_op_events(ProfView P, const int64_t *delta, double *ev_t, int64_t *ev_d, int64_t *na) {
+  if (blockIdx.x || threadIdx.x) return;
+  *na = sim_op_events(P, delta, ev_t, ev_d);
+}
+
+__global__ void __launch_bounds__(128) k_swap_eval_weights(EvalArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t p = a.L.p, k = a.c.k;
+  const CandView &c = a.c;
+  LinearAlloc al{a.scratch + (size_t)gw * a.per_warp, 0};
+  EvalScratch x;
+  eval_take(al, x, p, k);
+  x.S.delta = const_cast<int64_t *>(a.delta);
+  const int64_t live0 = (int64_t)*a.live0, na = *a.na;
+  for (int64_t e = gw; e < a.m; e += nw) {
+    const double *w = a.w + 4 * e;
+    for (int64_t i = lane; i < k; i += 32) {
+      double s = 0.0;
+      for (int q = 0; q < 4; q++) s = s + w[q] * a.z[q * k + i];
+      x.comb[i] = s;
+    }
+    __syncwarp();
+    warp_rank_sort(x.ord, k, [&](int64_t y, int64_t q) {
+      double ry = -x.comb[y], rq = -x.comb[q];
+      if (ry != rq) return ry < rq;
+      if (c.size[y] != c.size[q]) return -c.size[y] < -c.size[q];
+      return c.name_rank[y] < c.name_rank[q];
+    });
+    for (int64_t r = lane; r < p; r += 32) x.cur[r] = (double)a.L.loads[r];
+    __syncwarp();
+    int64_t n = 0;
+    double mx = warp_pymax_cur(x.cur, p);
+    for (int64_t q = 0; q < k; q++) {
+      if (f_le_i(mx, a.limit)) break;
+      const int32_t i = x.ord[q];
+      const int64_t lo = c.out_index[i], hi = c.in_index[i] + (c.spans[i] ? p : 0);
+      const double sz = (double)c.size[i];
+      if (hi - lo - 1 <= p) {
+        for (int64_t s = lo + 1 + lane; s < hi; s += 32) x.cur[s % p] -= sz;
+      } else {
+        for (int64_t r = lane; r < p; r += 32) {
+          int h = absence_hits(r, lo, hi, p);
+          for (int z = 0; z < h; z++) x.cur[r] -= sz;
+        }
+      }
+      if (lane == 0) x.sel[n] = i;
+      n++;
+      __syncwarp();
+      mx = warp_pymax_cur(x.cur, p);
+    }
+    int status = MP_OK, rounds = 0;
+    double overhead = 0.0;
+    int64_t aux = 0;
+    if (!f_le_i(mx, a.limit)) {
+      status = MP_E_LIMIT_UNREACHABLE;  // autoswap.py:315-316
+      aux = (int64_t)mx;
+    } else {
+      for (int64_t q = lane; q < n; q += 32) {
+        x.S.ready[q] = c.out_ready[x.sel[q]];
+        x.S.deadline[q] = c.in_t[x.sel[q]];
+      }
+      __syncwarp();
+      make_schedule(c, x.sel, n, x.S.ready, x.S.deadline, x.T.t_so, x.T.t_eo, x.T.t_si, x.T.t_ei, x.T.eord, x.S);
+      // the overlay curve is not part of the objective; only the replay is
+      Replay<PeakCurve> rep{};
+      SimResult res = sim_fixed_point<false>(a.P, c, x.sel, n, a.limit, 1, a.max_rounds, live0, x.S, x.T, rep);
+      status = res.status;
+      rounds = (int)res.rounds;
+      overhead = res.delay;
+      aux = res.status == MP_E_SWAP_DEADLOCK ? res.eidx : 0;
+      (void)na;
+    }
+    if (lane == 0) {
+      a.status[e] = status;
+      a.rounds[e] = rounds;
+      a.overhead[e] = overhead;
+      a.nsel[e] = n;
+      a.aux[e] = aux;
+    }
+    __syncwarp();
+  }
+}
+
+extern "C" int mp_swap_eval_weights(mp_ctx *ctx, mp_dprofile *P, const mp_cands_io *c, const double *z,
+                                    const double *weights, int64_t m, int64_t limit, int32_t max_rounds,
+                                    int32_t *status, double *overhead, int64_t *nsel, int64_t *aux, mp_err *err) {
+  StageTimer tm(ctx, MP_ST_SWAP);
+  cudaStream_t st = ctx->stream;
+  if (m <= 0) return MP_OK;
+  CandDev d;
+  CandView cv;
+  int rc = upload_cands(ctx, c, d, cv, err);
+  if (rc) return rc;
+  const int64_t p = P->d.period, k = c->k;
+  DBuf<double> dz, dw, ev_t, ov;
+  DBuf<int64_t> delta, ev_d, dn, dnsel, daux;
+  DBuf<int32_t> dst, drounds;
+  DBuf<char> scratch;
+  CUDA_TRY(dz.alloc(4 * k, st)); CUDA_TRY(dw.alloc(4 * m, st)); CUDA_TRY(ev_t.alloc(p, st));
+  CUDA_TRY(ov.alloc(m, st)); CUDA_TRY(delta.alloc(p, st)); CUDA_TRY(ev_d.alloc(p, st)); CUDA_TRY(dn.alloc(2, st));
+  CUDA_TRY(dnsel.alloc(m, st)); CUDA_TRY(daux.alloc(m, st)); CUDA_TRY(dst.alloc(m, st)); CUDA_TRY(drounds.alloc(m, st));
+  if (k) CUDA_TRY(cudaMemcpyAsync(dz.p, z, 4 * k * 8, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(dw.p, weights, 4 * m * 8, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemsetAsync(delta.p, 0, p * 8, st));
+  CUDA_TRY(cudaMemsetAsync(dn.p, 0, 16, st));
+  ProfView pv{p, P->d.nvars, P->window0, P->d.duration_us, P->op_times.p, P->nseg.p, P->seg.p, P->size.p};
+  unsigned long long *d_live0 = (unsigned long long *)(dn.p + 1);
+  LAUNCH(ctx, k_op_deltas, grid_for(P->d.nvars, 256), 256, 0, pv, delta.p, d_live0);
+  LAUNCH(ctx, k_op_events, 1, 32, 0, pv, delta.p, ev_t.p, ev_d.p, dn.p);
+  LinearAlloc cnt{nullptr, 0};
+  EvalScratch xs;
+  eval_take(cnt, xs, p, k);
+  const size_t per = (cnt.top + 255) & ~(size_t)255;
+  int64_t warps = m < (int64_t)ctx->num_sms * 16 ? m : (int64_t)ctx->num_sms * 16;
+  CUDA_TRY(scratch.alloc((int64_t)(per * (size_t)warps), st));
+  EvalArgs a{load_view(P), pv, cv, dz.p, dw.p, m, limit, max_rounds, d_live0, delta.p, ev_t.p, ev_d.p, dn.p,
+             scratch.p, per, dst.p, drounds.p, ov.p, dnsel.p, daux.p};
+  LAUNCH(ctx, k_swap_eval_weights, (unsigned)((warps + 3) / 4), 128, 0, a);
+  CUDA_TRY(cudaMemcpyAsync(status, dst.p, m * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(overhead, ov.p, m * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(nsel, dnsel.p, m * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(aux, daux.p, m * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return MP_OK;
+}
