@@ -351,6 +351,8 @@ typedef struct mp_sweep_trace {
   int64_t edges;     /* undirected conflict edges (ConflictGraph.adj) */
   int64_t ncand;     /* filter_candidates */
   int64_t load_min;  /* compute_load_min */
+  int64_t norder;    /* SWDOA greedy picks computed (and stored in cand_order): up
+                        to the smallest budget limit SwapPlanner.fit selects for */
 } mp_sweep_trace;
 
 /* per (trace, budget) result of SwapPlanner.fit; status MP_OK,
@@ -376,8 +378,9 @@ int mp_sweep_free(mp_dsweep *s);
 int mp_sweep_run(mp_ctx *ctx, mp_dsweep *s, const mp_sweep_params *prm, mp_err *err);
 /* copy results out: traces[ntraces], budgets[ntraces * nbudget];
  * offsets / cand_order are laid out like the events (trace t's rows start
- * at ev_off[t]): plan_pool offsets in profile variable order, and the SWDOA
- * greedy order as profile variable indices.  Any pointer may be NULL. */
+ * at ev_off[t]): plan_pool offsets in profile variable order, and the first
+ * norder picks of the SWDOA greedy as profile variable indices (every
+ * budget's selection is a prefix of them).  Any pointer may be NULL. */
 int mp_sweep_download(mp_ctx *ctx, mp_dsweep *s, mp_sweep_trace *traces, mp_sweep_budget *budgets,
                       int64_t *offsets, int32_t *cand_order, mp_err *err);
 /* diagnostics: per-trace clock64() at 8 phase marks of the sweep kernel

@@ -1258,7 +1258,27 @@ int orc_sweep_unit(const mp_trace_in *t, const mp_sweep_params *prm, mp_sweep_tr
   for (int i = 0; i < 4; i++) sc[i] = malloc((size_t)(k + 1) * 8);
   int32_t *order = malloc((size_t)(k + 1) * 4);
   orc_scores(L, &C, names, sc[0], sc[1], sc[2], sc[3], order);
-  for (int64_t q = 0; q < k; q++) cand_order[q] = C.var[order[q]];
+  /* the greedy prefix the budgets select from: up to the smallest limit that
+   * passes SwapPlanner.fit's precheck (the device stops there too) */
+  {
+    int64_t stop = INT64_MAX;
+    int need = 0;
+    for (int b = 0; b < prm->nbudget; b++) {
+      int64_t limit = (int64_t)((double)d.peak_bytes * prm->budget_frac[b]);
+      if (limit <= 0 || (limit < d.peak_bytes && limit < load_min)) continue;
+      need = 1;
+      if (limit < stop) stop = limit;
+    }
+    int64_t norder = 0;
+    if (need) {
+      double *cur = malloc((size_t)(p + 1) * 8);
+      for (int64_t r = 0; r < p; r++) cur[r] = (double)P->loads[r];
+      while (norder < k && !f_le_i(vmax(cur, p), stop)) absence(p, &C, order[norder++], cur);
+      free(cur);
+    }
+    rec->norder = norder;
+    for (int64_t q = 0; q < norder; q++) cand_order[q] = C.var[order[q]];
+  }
   /* per budget: SwapPlanner.fit */
   int32_t *sel = malloc((size_t)(k + 1) * 4);
   int64_t cap = 1 + p + 2 * k + 2;

@@ -278,7 +278,7 @@ def sweep_unit(arrays, params):
     order = np.zeros(max(n, 1), np.int32)
     L.orc_sweep_unit(C.byref(trace_in(arrays)), C.byref(prm), ptr(rec), ptr(brec), ptr(offs), ptr(order))
     r = rec[0]
-    return r, brec[:nb], offs[:int(r["nvars"])], order[:int(r["ncand"])]
+    return r, brec[:nb], offs[:int(r["nvars"])], order[:int(r["norder"])]
 
 
 def sweep(batch, params, indices=None):

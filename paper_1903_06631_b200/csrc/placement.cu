@@ -124,6 +124,12 @@ __device__ int64_t place_mem(const PlaceArgs &a, P buf, int64_t rb, int m, int64
   return h.found ? h.best_off : h.top;
 }
 
+__device__ __forceinline__ int atom_sub_acq_rel(int32_t *p) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], -1;" : "=r"(old) : "l"(p) : "memory");
+  return old;
+}
+
 constexpr int PLACE_THREADS = 256;
 constexpr int PLACE_MIN_BLOCKS = 5;  // <= 48 registers: 40 resident warps per SM
 
@@ -207,7 +213,6 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_MIN_BLOCKS) k_place_async
       a.level[v] = lvl;
       if (o + need > fp) fp = o + need;
       if (lvl > dmax) dmax = lvl;
-      __threadfence();  // offsets visible before any successor counter drops
     }
     local_done++;
     __syncwarp();
@@ -216,8 +221,10 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_MIN_BLOCKS) k_place_async
       int32_t j = 0;
       if (k < re) {
         j = a.col[k];
-        ready = atomicSub(&a.remaining[j], 1) == 1;
-        if (ready) __threadfence();  // acquire the other predecessors' offsets
+        // acq_rel: releases this variable's offset (written by lane 0 before
+        // the __syncwarp above; release is cumulative) and, for the last
+        // predecessor, acquires every other predecessor's
+        ready = atom_sub_acq_rel(&a.remaining[j]) == 1;
       }
       unsigned bal = __ballot_sync(FULL_MASK, ready);
       if (bal && next < 0) {

@@ -63,54 +63,19 @@ __device__ T block_excl_scan(T v, T *total) {
   return r;
 }
 
+// Single-pass scan with decoupled look-back: tiles take ids in launch order
+// from a counter, publish their aggregate, then resolve their exclusive
+// prefix from predecessors (aggregate or inclusive prefix, whichever is
+// posted first) and post their own inclusive prefix.
 template <typename T>
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan_partials(const T *in, int64_t n, T *part) {
-  int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
-  T s = 0;
-#pragma unroll
-  for (int i = 0; i < SCAN_ITEMS; i++) {
-    int64_t j = base + (int64_t)i * SCAN_THREADS + threadIdx.x;
-    if (j < n) s += in[j];
-  }
-  __shared__ T tot;
-  block_excl_scan(s, &tot);
-  if (threadIdx.x == 0) part[blockIdx.x] = tot;
-}
-
-template <typename T>
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan_single(T *a, int64_t n, T *total) {
-  // one block scans n partials in place (n up to ~ millions, looped)
-  __shared__ T carry_s, tot;
-  if (threadIdx.x == 0) carry_s = 0;
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_onepass(const T *in, T *out, int64_t n, int32_t *flags,
+                                                               T *agg, T *incl, int32_t *tile_ctr, T *total) {
+  __shared__ int32_t s_tile;
+  __shared__ T s_excl, s_tot;
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1);
   __syncthreads();
-  for (int64_t base = 0; base < n; base += SCAN_TILE) {
-    T v[SCAN_ITEMS];
-    T s = 0;
-#pragma unroll
-    for (int i = 0; i < SCAN_ITEMS; i++) {
-      int64_t j = base + (int64_t)threadIdx.x * SCAN_ITEMS + i;
-      v[i] = j < n ? a[j] : T(0);
-      s += v[i];
-    }
-    T pre = block_excl_scan(s, &tot);
-    T c = carry_s;
-    T run = c + pre;
-#pragma unroll
-    for (int i = 0; i < SCAN_ITEMS; i++) {
-      int64_t j = base + (int64_t)threadIdx.x * SCAN_ITEMS + i;
-      if (j < n) a[j] = run;
-      run += v[i];
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) carry_s = c + tot;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0 && total) *total = carry_s;
-}
-
-template <typename T>
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan_apply(const T *in, T *out, int64_t n, const T *part) {
-  int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
+  const int64_t tile = s_tile;
+  const int64_t base = tile * SCAN_TILE;
   T v[SCAN_ITEMS];
   T s = 0;
 #pragma unroll
@@ -119,8 +84,51 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_apply(const T *in, T *out
     v[i] = j < n ? in[j] : T(0);
     s += v[i];
   }
-  __shared__ T tot;
-  T run = part[blockIdx.x] + block_excl_scan(s, &tot);
+  T pre = block_excl_scan(s, &s_tot);
+  if (threadIdx.x < 32) {
+    // warp 0 posts the tile, then looks back 32 predecessors at a time: sum
+    // aggregates up to the nearest posted inclusive prefix
+    const int lane = threadIdx.x;
+    const T sum = s_tot;
+    T excl = 0;
+    if (tile == 0) {
+      if (lane == 0) {
+        incl[0] = sum;
+        __threadfence();
+        atomicExch(&flags[0], 2);
+      }
+    } else {
+      if (lane == 0) {
+        agg[tile] = sum;
+        __threadfence();
+        atomicExch(&flags[tile], 1);
+      }
+      for (int64_t p = tile - 1;; p -= 32) {
+        int64_t q = p - lane;
+        int f = q >= 0 ? *(volatile int32_t *)&flags[q] : 2;
+        while (__any_sync(FULL_MASK, f == 0))
+          if (f == 0) f = *(volatile int32_t *)&flags[q];
+        __threadfence();
+        unsigned pfx = __ballot_sync(FULL_MASK, f == 2);
+        int stop = pfx ? __ffs(pfx) - 1 : 31;
+        T val = 0;
+        if (lane <= stop && q >= 0) val = f == 2 ? *(volatile T *)&incl[q] : *(volatile T *)&agg[q];
+        excl += warp_sum(val);
+        if (pfx) break;
+      }
+      if (lane == 0) {
+        incl[tile] = excl + sum;
+        __threadfence();
+        atomicExch(&flags[tile], 2);
+      }
+    }
+    if (lane == 0) {
+      s_excl = excl;
+      if (total && base + SCAN_TILE >= n) *total = excl + sum;
+    }
+  }
+  __syncthreads();
+  T run = s_excl + pre;
 #pragma unroll
   for (int i = 0; i < SCAN_ITEMS; i++) {
     int64_t j = base + (int64_t)threadIdx.x * SCAN_ITEMS + i;
@@ -136,16 +144,14 @@ int dev_exclusive_scan(mp_ctx *ctx, const T *in, T *out, int64_t n, T *total, mp
     return MP_OK;
   }
   int64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
-  if (nb == 1) {
-    if (out != in) CUDA_TRY(cudaMemcpyAsync(out, in, n * sizeof(T), cudaMemcpyDeviceToDevice, ctx->stream));
-    LAUNCH(ctx, k_scan_single<T>, 1, SCAN_THREADS, 0, out, n, total);
-    return MP_OK;
-  }
-  DBuf<T> part;
-  CUDA_TRY(part.alloc(nb, ctx->stream));
-  LAUNCH(ctx, k_scan_partials<T>, (unsigned)nb, SCAN_THREADS, 0, in, n, part.p);
-  LAUNCH(ctx, k_scan_single<T>, 1, SCAN_THREADS, 0, part.p, nb, total);
-  LAUNCH(ctx, k_scan_apply<T>, (unsigned)nb, SCAN_THREADS, 0, in, out, n, part.p);
+  // flags + tile counter in one zeroed block, per-tile values after it
+  DBuf<unsigned char> st;
+  size_t fbytes = ((size_t)(nb + 1) * 4 + 15) & ~(size_t)15;
+  CUDA_TRY(st.alloc((int64_t)(fbytes + 2 * (size_t)nb * sizeof(T)), ctx->stream));
+  CUDA_TRY(cudaMemsetAsync(st.p, 0, fbytes, ctx->stream));
+  int32_t *flags = (int32_t *)st.p;
+  T *agg = (T *)(st.p + fbytes), *incl = agg + nb;
+  LAUNCH(ctx, k_scan_onepass<T>, (unsigned)nb, SCAN_THREADS, 0, in, out, n, flags, agg, incl, flags + nb, total);
   return MP_OK;
 }
 
@@ -159,28 +165,50 @@ constexpr int RS_THREADS = 256;
 constexpr int RS_WARPS = RS_THREADS / 32;
 constexpr int RS_BINS = 256;
 
-template <typename K, int ITEMS>
-__global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const K *keys, int64_t n, int shift,
-                                                         int64_t ntiles, int32_t *counts) {
-  __shared__ int32_t h[RS_BINS];
-  h[threadIdx.x] = 0;
+// One-sweep LSD radix sort (8-bit digits): one kernel computes every pass's
+// global digit histogram up front, then each pass is a single kernel whose
+// tiles (ids in launch order) rank their keys per warp (match_any), post
+// their digit counts, resolve each digit's exclusive prefix by decoupled
+// look-back over earlier tiles (32-bit flag|count words), and scatter
+// through shared memory so global writes stay coalesced per digit run.
+
+constexpr uint32_t OS_AGG = 1u << 30, OS_PFX = 2u << 30, OS_MASK = (1u << 30) - 1;
+constexpr int OS_MAX_PASSES = 8;
+
+template <typename K>
+__global__ void __launch_bounds__(RS_THREADS) k_os_hist(const K *keys, int64_t n, int passes, int32_t *ghist) {
+  __shared__ int32_t h[OS_MAX_PASSES][RS_BINS];
+  for (int i = threadIdx.x; i < passes * RS_BINS; i += RS_THREADS) h[i / RS_BINS][i % RS_BINS] = 0;
   __syncthreads();
-  const int64_t tile = blockIdx.x;
-  const int64_t base = tile * (int64_t)(RS_THREADS * ITEMS);
-#pragma unroll
-  for (int i = 0; i < ITEMS; i++) {
-    int64_t j = base + (int64_t)i * RS_THREADS + threadIdx.x;
-    if (j < n) atomicAdd(&h[(unsigned)((keys[j] >> shift) & 0xff)], 1);
+  for (int64_t j = blockIdx.x * (int64_t)RS_THREADS + threadIdx.x; j < n; j += (int64_t)gridDim.x * RS_THREADS) {
+    K k = keys[j];
+    for (int p = 0; p < passes; p++) atomicAdd(&h[p][(unsigned)((k >> (8 * p)) & 0xff)], 1);
   }
   __syncthreads();
-  counts[(int64_t)threadIdx.x * ntiles + tile] = h[threadIdx.x];
+  for (int i = threadIdx.x; i < passes * RS_BINS; i += RS_THREADS) {
+    int32_t c = h[i / RS_BINS][i % RS_BINS];
+    if (c) atomicAdd(&ghist[i], c);
+  }
+}
+
+// per pass: exclusive prefix of the 256 digit counts (one warp per pass)
+__global__ void k_os_prefix(int32_t *ghist, int passes) {
+  const int lane = threadIdx.x & 31, p = threadIdx.x >> 5;
+  if (p >= passes) return;
+  int32_t c = 0;
+  for (int chunk = 0; chunk < RS_BINS; chunk += 32) {
+    int32_t x = ghist[p * RS_BINS + chunk + lane];
+    int32_t xi = warp_incl_scan_add(x);
+    ghist[p * RS_BINS + chunk + lane] = c + xi - x;
+    c += __shfl_sync(FULL_MASK, xi, 31);
+  }
 }
 
 template <typename K, int ITEMS>
-__global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K *keys, const uint32_t *vals,
-                                                            K *okeys, uint32_t *ovals, int64_t n,
-                                                            int shift, int64_t ntiles,
-                                                            const int32_t *offsets) {
+__global__ void __launch_bounds__(RS_THREADS) k_os_pass(const K *keys, const uint32_t *vals, K *okeys,
+                                                         uint32_t *ovals, int64_t n, int shift,
+                                                         const int32_t *gstart, uint32_t *look,
+                                                         int32_t *tile_ctr) {
   constexpr int TILE = RS_THREADS * ITEMS;
   constexpr int PER_WARP = 32 * ITEMS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -189,13 +217,14 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K *keys, const 
   __shared__ int32_t whist[RS_WARPS][RS_BINS];
   __shared__ int32_t dprefix[RS_BINS];
   __shared__ int32_t gbase[RS_BINS];
+  __shared__ int32_t s_tile;
 
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t tile = blockIdx.x;
-  const int64_t base = tile * (int64_t)TILE;
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1);
   for (int d = lane; d < RS_BINS; d += 32) whist[w][d] = 0;
-  if (threadIdx.x < RS_BINS) gbase[threadIdx.x] = offsets[(int64_t)threadIdx.x * ntiles + tile];
-  __syncwarp();
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int64_t base = tile * (int64_t)TILE;
 
   K k[ITEMS];
   uint32_t v[ITEMS];
@@ -223,9 +252,10 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K *keys, const 
     __syncwarp();
   }
   __syncthreads();
-  // per digit: exclusive prefix over warps; tile totals
   {
-    int d = threadIdx.x;  // RS_THREADS == RS_BINS
+    // per digit: exclusive prefix over warps, the tile's count, its posting
+    // and the look-back for its global position
+    const int d = threadIdx.x;  // RS_THREADS == RS_BINS
     int32_t run = 0;
 #pragma unroll
     for (int ww = 0; ww < RS_WARPS; ww++) {
@@ -234,9 +264,26 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K *keys, const 
       run += t;
     }
     dprefix[d] = run;
+    uint32_t *mine = look + tile * RS_BINS + d;
+    if (tile == 0) {
+      atomicExch(mine, OS_PFX | (uint32_t)run);
+      gbase[d] = gstart[d];
+    } else {
+      atomicExch(mine, OS_AGG | (uint32_t)run);
+      uint32_t excl = 0;
+      for (int64_t p = tile - 1;;) {
+        uint32_t x = *(volatile uint32_t *)(look + p * RS_BINS + d);
+        if (!(x & ~OS_MASK)) continue;
+        excl += x & OS_MASK;
+        if (x & OS_PFX) break;
+        p--;
+      }
+      atomicExch(mine, OS_PFX | (excl + (uint32_t)run));
+      gbase[d] = gstart[d] + (int32_t)excl;
+    }
   }
   __syncthreads();
-  // exclusive scan of tile digit totals (256 values, one warp)
+  // exclusive scan of the tile digit counts (256 values, one warp)
   if (w == 0) {
     int32_t c = 0;
     for (int chunk = 0; chunk < RS_BINS; chunk += 32) {
@@ -270,35 +317,56 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K *keys, const 
 template <typename K, int ITEMS>
 static int radix_sort_impl(mp_ctx *ctx, K *keys, uint32_t *vals, int64_t n, int bits, mp_err *err) {
   if (n <= 1 || bits <= 0) return MP_OK;
+  if (n > (int64_t)OS_MASK) {
+    mp_set_err(err, MP_E_UNSUPPORTED, 0, n, 0, "radix sort of more than 2^30 keys");
+    return MP_E_UNSUPPORTED;
+  }
   constexpr int TILE = RS_THREADS * ITEMS;
-  int64_t ntiles = (n + TILE - 1) / TILE;
+  const int64_t ntiles = (n + TILE - 1) / TILE;
+  const int passes = (bits + 7) / 8;
+  cudaStream_t st = ctx->stream;
   DBuf<K> k2;
   DBuf<uint32_t> v2;
-  DBuf<int32_t> counts;
-  CUDA_TRY(k2.alloc(n, ctx->stream));
-  CUDA_TRY(v2.alloc(n, ctx->stream));
-  CUDA_TRY(counts.alloc(ntiles * RS_BINS, ctx->stream));
+  DBuf<int32_t> meta;  // [passes][256] digit starts, then per pass a tile counter
+  DBuf<uint32_t> look;
+  CUDA_TRY(k2.alloc(n, st));
+  CUDA_TRY(v2.alloc(n, st));
+  CUDA_TRY(meta.alloc(passes * RS_BINS + passes, st));
+  CUDA_TRY(look.alloc(ntiles * RS_BINS * passes, st));
+  CUDA_TRY(cudaMemsetAsync(meta.p, 0, (passes * RS_BINS + passes) * sizeof(int32_t), st));
+  CUDA_TRY(cudaMemsetAsync(look.p, 0, ntiles * RS_BINS * passes * sizeof(uint32_t), st));
   size_t smem = (size_t)TILE * (sizeof(K) + sizeof(uint32_t));
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_rs_scatter<K, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_os_pass<K, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr_set = true;
   }
-  K *src_k = keys, *dst_k = k2.p;
-  uint32_t *src_v = vals, *dst_v = v2.p;
-  int passes = 0;
-  for (int shift = 0; shift < bits; shift += 8, passes++) {
-    LAUNCH(ctx, (k_rs_hist<K, ITEMS>), (unsigned)ntiles, RS_THREADS, 0, src_k, n, shift, ntiles, counts.p);
-    int rc = dev_exclusive_scan<int32_t>(ctx, counts.p, counts.p, ntiles * RS_BINS, nullptr, err);
-    if (rc) return rc;
-    LAUNCH(ctx, (k_rs_scatter<K, ITEMS>), (unsigned)ntiles, RS_THREADS, smem, src_k, src_v, dst_k, dst_v,
-           n, shift, ntiles, counts.p);
-    K *tk = src_k; src_k = dst_k; dst_k = tk;
-    uint32_t *tv = src_v; src_v = dst_v; dst_v = tv;
+  unsigned hgrid = grid_for(n, RS_THREADS, (int64_t)ctx->num_sms * 8);
+  LAUNCH(ctx, k_os_hist<K>, hgrid, RS_THREADS, 0, keys, n, passes, meta.p);
+  LAUNCH(ctx, k_os_prefix, 1, 32 * passes, 0, meta.p, passes);
+  // buffers: the caller's (0) and scratch (1, 2); the last pass always writes
+  // the caller's, odd pass counts route through the third buffer
+  DBuf<K> k3;
+  DBuf<uint32_t> v3;
+  if ((passes & 1) && passes > 1) {
+    CUDA_TRY(k3.alloc(n, st));
+    CUDA_TRY(v3.alloc(n, st));
   }
-  if (passes & 1) {
-    CUDA_TRY(cudaMemcpyAsync(keys, src_k, n * sizeof(K), cudaMemcpyDeviceToDevice, ctx->stream));
-    CUDA_TRY(cudaMemcpyAsync(vals, src_v, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, ctx->stream));
+  K *bk[3] = {keys, k2.p, k3.p};
+  uint32_t *bv[3] = {vals, v2.p, v3.p};
+  int src = 0;
+  for (int p = 0; p < passes; p++) {
+    int dst;
+    if (p == passes - 1) dst = passes == 1 ? 1 : 0;
+    else if (passes & 1) dst = src == 1 ? 2 : 1;
+    else dst = src ^ 1;
+    LAUNCH(ctx, (k_os_pass<K, ITEMS>), (unsigned)ntiles, RS_THREADS, smem, bk[src], bv[src], bk[dst], bv[dst], n,
+           8 * p, meta.p + p * RS_BINS, look.p + (int64_t)p * ntiles * RS_BINS, meta.p + passes * RS_BINS + p);
+    src = dst;
+  }
+  if (src != 0) {  // a single pass
+    CUDA_TRY(cudaMemcpyAsync(keys, bk[src], n * sizeof(K), cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(vals, bv[src], n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
   }
   return MP_OK;
 }

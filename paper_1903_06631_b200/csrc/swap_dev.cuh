@@ -339,15 +339,18 @@ __device__ double prefix_max_block(const G &g, const LoadView &L, const double *
   return mx;
 }
 
-// scores + the unbudgeted SWDOA greedy (autoswap.py:132-215), group-wide.
-// peaks[j] = max(cur) after j picks, so a budgeted select_by_swdoa is the
-// prefix order[0..m) with m the first j where peaks[j] <= limit.  Any of
+// scores + the SWDOA greedy (autoswap.py:132-215), group-wide.  peaks[j] =
+// max(cur) after j picks, so a budgeted select_by_swdoa is the prefix
+// order[0..m) with m the first j where peaks[j] <= limit.  With `stop` >= 0
+// the greedy ends at the first planned peak <= stop (every budget at or
+// above it is then decided); returns the number of picks made.  Any of
 // doa/aoa/wdoa/swdoa may be null.  Scratch: W[p + 1], jx[2k]; shared
 // memory keys >= 33 SwKey, sm >= PM_SMEM long longs.
 template <class G>
-__device__ void swdoa_greedy_block(const G &g, const LoadView &L, const CandView &c, double *cur, uint8_t *taken,
-                                   double *doa, double *aoa, double *wdoa, double *swdoa, int32_t *order,
-                                   double *peaks, int64_t *W, int32_t *jx, SwKey *keys, long long *sm) {
+__device__ int64_t swdoa_greedy_block(const G &g, const LoadView &L, const CandView &c, double *cur,
+                                      uint8_t *taken, double *doa, double *aoa, double *wdoa, double *swdoa,
+                                      int32_t *order, double *peaks, int64_t *W, int32_t *jx, SwKey *keys,
+                                      long long *sm, int64_t stop = -1) {
   const int64_t p = L.p, k = c.k;
   const int tid = g.idx(), nt = g.size();
   bool times_ok = int_valued(L.duration);
@@ -373,7 +376,7 @@ __device__ void swdoa_greedy_block(const G &g, const LoadView &L, const CandView
     bool exact = times_ok;
     const double pk = prefix_max_block(g, L, cur, W, sm, exact);
     if (tid == 0) peaks[round] = pk;
-    if (round == k) break;
+    if (round == k || (stop >= 0 && f_le_i(pk, stop))) return round;
     SwKey best{-1, 0, 0.0, 0};
     for (int64_t i = tid; i < k; i += nt) {
       if (taken[i]) continue;

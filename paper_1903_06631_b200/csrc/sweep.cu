@@ -371,7 +371,8 @@ struct SweepShared {
   int bad, unsorted;
   double red[33];
   SwKey keys[33];
-  int lm_ok, ev_ok;
+  int next_budget, swap_ready, nomem;
+  BudgetArrays ba[MP_SWEEP_MAX_BUDGETS];
 };
 
 __device__ void sweep_fail(const SweepArgs &a, int64_t t, int status, int code, int64_t index,
@@ -566,9 +567,11 @@ __device__ void sweep_one(const SweepArgs &a, int64_t t, char *slab, char *fast,
   ar.phase();
   SwapKeep kp;
   kp.take(ar, p, V);
-  const size_t keep_top = ar.fast.top;  // the budget phase refills the arena from here
   PlaceArrays pl;
   pl.take(ar, V);
+  // the budgets refill the arena from here once the greedy's arrays are dead
+  const size_t keep_top = ar.fast.top;
+  const size_t keep_slow = ar.slow.top;
   GreedyArrays gr;
   gr.take(ar, p, V);
   SwapScratch ss;
@@ -619,11 +622,81 @@ __device__ void sweep_one(const SweepArgs &a, int64_t t, char *slab, char *fast,
     }
     pl.adj[idx] = bits;
   }
+  if (tid == 0) {
+    sh.next_budget = 0;
+    sh.swap_ready = 0;
+    sh.nomem = 0;
+  }
   __syncthreads();
 
-  int64_t k = 0, load_min = 0, live0 = 0, na = 0;
   const LoadView L{p, loads, kp.tau, dur};
   const ProfView P{p, V, start, dur, kp.tau, pa.nseg, pa.seg, pa.size};
+  // SwapPlanner(limit, score="swdoa").fit for budgets pulled from a shared
+  // counter, one warp each; the swap path's scalars come through shared
+  // memory (published before swap_ready)
+  auto run_budgets = [&]() {
+    const int64_t k_ = sh.gsm[0], lmin = sh.gsm[1], l0 = sh.gsm[2], nord = sh.gsm[3], nevt = sh.gsm[4];
+    const CandView cv{k_, kp.c.size, kp.c.out_index, kp.c.in_index, kp.name_rank, kp.c.out_t, kp.c.out_ready,
+                      kp.c.in_t, kp.c.dout, kp.c.din, kp.c.spans};
+    for (;;) {
+      int b = 0;
+      if (lane == 0) b = atomicAdd(&sh.next_budget, 1);
+      b = __shfl_sync(FULL_MASK, b, 0);
+      if (b >= prm.nbudget) break;
+      mp_sweep_budget rb{};
+      const int64_t limit = (int64_t)((double)peak * prm.budget_frac[b]);
+      rb.limit_bytes = limit;
+      if (limit <= 0) {
+        rb.status = MP_E_VALUE;  // check_positive, validation.py:32-34
+      } else if (limit < peak && limit < lmin) {
+        rb.status = MP_E_LIMIT_UNREACHABLE;  // estimators.py:98-100
+        rb.err_aux = lmin;
+      } else {
+        // select_by_swdoa: the greedy stops at the first planned peak <= limit
+        int64_t m = -1;
+        for (int64_t j = 0; j <= nord; j++)
+          if (f_le_i(kp.peaks[j], limit)) { m = j; break; }
+        if (m < 0) {  // only when the greedy ran through every candidate
+          rb.status = MP_E_LIMIT_UNREACHABLE;  // autoswap.py:222-224
+          rb.err_aux = (int64_t)kp.peaks[nord];
+        } else {
+          SimScratch S = sh.ba[b].S;
+          S.delta = kp.delta;
+          const SimTimes T = sh.ba[b].T;
+          const int32_t *sel = kp.order;
+          long long bytes = 0;
+          for (int64_t q = lane; q < m; q += 32) {
+            S.ready[q] = cv.out_ready[sel[q]];   // build_schedule, swapsim.py:111-116
+            S.deadline[q] = cv.in_t[sel[q]];
+            bytes += cv.size[sel[q]];
+          }
+          bytes = warp_sum(bytes);
+          __syncwarp();
+          make_schedule(cv, sel, m, S.ready, S.deadline, T.t_so, T.t_eo, T.t_si, T.t_ei, T.eord, S);
+          PeakCurve lp{};
+          sim_overlay(P, cv, sel, m, l0, T.t_eo, T.t_si, T.eord, kp.ev_t, kp.ev_d, nevt, S, lp);
+          Replay<PeakCurve> rep{};
+          SimResult res = sim_fixed_point<false>(P, cv, sel, m, limit, 1, prm.max_rounds, l0, S, T, rep);
+          rb.status = res.status;
+          rb.nsel = m;
+          rb.selected_bytes = bytes;
+          if (res.status == MP_OK) {
+            rb.rounds = (int32_t)res.rounds;
+            rb.overhead_us = res.delay;
+            rb.achieved_peak_bytes = rep.cv.peak;
+            rb.planned_peak_bytes = lp.peak;
+          } else if (res.status == MP_E_SWAP_DEADLOCK) {
+            rb.err_index = res.eidx;
+            rb.err_aux = res.eaux1;
+          }
+        }
+      }
+      if (lane == 0) a.brec[t * prm.nbudget + b] = rb;
+      __syncwarp();
+    }
+  };
+
+  int64_t k = 0, load_min = 0, live0 = 0, na = 0, norder = 0;
   if (warp == 0) {
     // ---- plan_pool (smartpool.py:122-144), concurrently with the swap path ----
     // One warp walks the order.  All placed ranges are kept in one list
@@ -721,6 +794,12 @@ __device__ void sweep_one(const SweepArgs &a, int64_t t, char *slab, char *fast,
     // scatter offsets back to profile order
     for (int64_t i = lane; i < V; i += 32) offs[pl.order[lr[i]]] = ls[i];
     if (lane == 0) sh.edges = edges;
+    // then help with the budgets the swap path has not claimed yet
+    if (lane == 0)
+      while (!*(volatile int *)&sh.swap_ready) __nanosleep(64);
+    __syncwarp();
+    __threadfence_block();
+    if (!*(volatile int *)&sh.nomem) run_budgets();
   } else {
     // ---- AutoSwap on warps 1..: candidates, load_min, SWDOA greedy ----
     const WarpGroup sg{1, SW_WARPS - 1, 1};
@@ -808,11 +887,24 @@ __device__ void sweep_one(const SweepArgs &a, int64_t t, char *slab, char *fast,
       }
     }
     load_min = (int64_t)block_max(sg, lm, sh.red);
+    // the smallest limit the greedy must reach: a budget below load_min (and
+    // below the peak) is rejected by SwapPlanner.fit before selecting
+    // (estimators.py:98-100), so every other budget is decided by the
+    // greedy prefix up to it
+    int64_t stop = INT64_MAX;
+    bool need = false;
+    for (int b = 0; b < prm.nbudget; b++) {
+      const int64_t limit = (int64_t)((double)peak * prm.budget_frac[b]);
+      if (limit <= 0 || (limit < peak && limit < load_min)) continue;
+      need = true;
+      stop = limit < stop ? limit : stop;
+    }
     if (gi == 0 && a.prof) a.prof[t * 16 + 3] = clock64();
-    swdoa_greedy_block(sg, L, cv, gr.cur, gr.taken, nullptr, nullptr, nullptr, nullptr, kp.order, kp.peaks, gr.W,
-                       gr.jx, sh.keys, sh.gsm);
+    norder = need ? swdoa_greedy_block(sg, L, cv, gr.cur, gr.taken, nullptr, nullptr, nullptr, nullptr, kp.order,
+                                       kp.peaks, gr.W, gr.jx, sh.keys, sh.gsm, stop)
+                  : 0;
     if (gi == 0 && a.prof) a.prof[t * 16 + 4] = clock64();
-    for (int64_t q = gi; q < k; q += gn) corder[q] = cc.var[kp.order[q]];
+    for (int64_t q = gi; q < norder; q += gn) corder[q] = cc.var[kp.order[q]];
     // ---- simulate prerequisites: _op_deltas and the sorted op events ----
     long long l0 = 0;
     for (int64_t i = gi; i < V; i += gn)
@@ -837,25 +929,40 @@ __device__ void sweep_one(const SweepArgs &a, int64_t t, char *slab, char *fast,
     bool sorted = true;
     for (int64_t q = gi; q + 1 < na; q += gn) sorted &= !td_less(kp.ev_t[q + 1], kp.ev_d[q + 1], kp.ev_t[q], kp.ev_d[q]);
     if (!sg.sync_and(sorted) && gi == 0) sim_op_events(P, kp.delta, kp.ev_t, kp.ev_d);
-    if (gi == 0) sh.na = na;
+    // publish the scalars, lay out each budget's scratch (sized by its
+    // selection) over the now-dead greedy arrays, then start the budgets
+    if (gi == 0) {
+      sh.gsm[0] = k;
+      sh.gsm[1] = load_min;
+      sh.gsm[2] = live0;
+      sh.gsm[3] = norder;
+      sh.gsm[4] = na;
+      Arena bar = ar;
+      bar.fast.top = keep_top;
+      bar.slow.top = keep_slow;
+      for (int b = 0; b < prm.nbudget; b++) {
+        const int64_t limit = (int64_t)((double)peak * prm.budget_frac[b]);
+        int64_t m = 0;
+        if (limit > 0 && !(limit < peak && limit < load_min))
+          while (m < norder && !f_le_i(kp.peaks[m], limit)) m++;
+        sh.ba[b].take(bar, p, m);
+      }
+      sh.nomem = bar.slow.over;
+      if (a.prof) a.prof[t * 16 + 5] = clock64();
+    }
     sg.sync();
-    if (gi == 0 && a.prof) a.prof[t * 16 + 5] = clock64();
+    if (gi == 0) {
+      __threadfence_block();
+      *(volatile int *)&sh.swap_ready = 1;
+    }
+    if (!sh.nomem) run_budgets();
   }
   __syncthreads();
+  if (sh.nomem) return sweep_fail(a, t, MP_E_NOMEM, 0, 0, R);
   R.edges = sh.edges;
-  // the swap group's scalars
-  if (warp == 1 && lane == 0) {
-    sh.gsm[0] = k;
-    sh.gsm[1] = load_min;
-    sh.gsm[2] = live0;
-  }
-  __syncthreads();
-  k = sh.gsm[0];
-  load_min = sh.gsm[1];
-  live0 = sh.gsm[2];
-  na = sh.na;
-  R.ncand = k;
-  R.load_min = load_min;
+  R.ncand = sh.gsm[0];
+  R.load_min = sh.gsm[1];
+  R.norder = sh.gsm[3];
   long long fe = LLONG_MIN;
   for (int64_t i = tid; i < V; i += SW_THREADS) {
     long long e = offs[i] + pa.size[i];
@@ -863,66 +970,7 @@ __device__ void sweep_one(const SweepArgs &a, int64_t t, char *slab, char *fast,
   }
   const int64_t foot = grp_max(cta, fe, sh.sm);
   R.footprint_bytes = V ? foot : 0;
-  const CandView cv{k, kp.c.size, kp.c.out_index, kp.c.in_index, kp.name_rank, kp.c.out_t, kp.c.out_ready,
-                    kp.c.in_t, kp.c.dout, kp.c.din, kp.c.spans};
-
-  // ---- per budget: SwapPlanner(limit, score="swdoa").fit, one warp each ----
   SW_MARK(6);
-  ar.fast.top = keep_top;
-  BudgetArrays ba[MP_SWEEP_MAX_BUDGETS];
-  for (int b = 0; b < prm.nbudget; b++) ba[b].take(ar, p, k);
-  if (bump.over) return sweep_fail(a, t, MP_E_NOMEM, 0, 0, R);
-  for (int b = warp; b < prm.nbudget; b += SW_WARPS) {  // warp-collective
-    mp_sweep_budget rb{};
-    const int64_t limit = (int64_t)((double)peak * prm.budget_frac[b]);
-    rb.limit_bytes = limit;
-    if (limit <= 0) {
-      rb.status = MP_E_VALUE;  // check_positive, validation.py:32-34
-    } else if (limit < peak && limit < load_min) {
-      rb.status = MP_E_LIMIT_UNREACHABLE;  // estimators.py:98-100
-      rb.err_aux = load_min;
-    } else {
-      // select_by_swdoa: the greedy stops at the first planned peak <= limit
-      int64_t m = -1;
-      for (int64_t j = 0; j <= k; j++)
-        if (f_le_i(kp.peaks[j], limit)) { m = j; break; }
-      if (m < 0) {
-        rb.status = MP_E_LIMIT_UNREACHABLE;  // autoswap.py:222-224
-        rb.err_aux = (int64_t)kp.peaks[k];
-      } else {
-        SimScratch S = ba[b].S;
-        S.delta = kp.delta;
-        const SimTimes &T = ba[b].T;
-        const int32_t *sel = kp.order;
-        long long bytes = 0;
-        for (int64_t q = lane; q < m; q += 32) {
-          S.ready[q] = cv.out_ready[sel[q]];   // build_schedule, swapsim.py:111-116
-          S.deadline[q] = cv.in_t[sel[q]];
-          bytes += cv.size[sel[q]];
-        }
-        bytes = warp_sum(bytes);
-        __syncwarp();
-        make_schedule(cv, sel, m, S.ready, S.deadline, T.t_so, T.t_eo, T.t_si, T.t_ei, T.eord, S);
-        PeakCurve lp{};
-        sim_overlay(P, cv, sel, m, live0, T.t_eo, T.t_si, T.eord, kp.ev_t, kp.ev_d, na, S, lp);
-        Replay<PeakCurve> rep{};
-        SimResult res = sim_fixed_point<false>(P, cv, sel, m, limit, 1, prm.max_rounds, live0, S, T, rep);
-        rb.status = res.status;
-        rb.nsel = m;
-        rb.selected_bytes = bytes;
-        if (res.status == MP_OK) {
-          rb.rounds = (int32_t)res.rounds;
-          rb.overhead_us = res.delay;
-          rb.achieved_peak_bytes = rep.cv.peak;
-          rb.planned_peak_bytes = lp.peak;
-        } else if (res.status == MP_E_SWAP_DEADLOCK) {
-          rb.err_index = res.eidx;
-          rb.err_aux = res.eaux1;
-        }
-      }
-    }
-    if (lane == 0) a.brec[t * prm.nbudget + b] = rb;
-  }
   __syncwarp();
   __syncthreads();
   SW_MARK(7);

@@ -37,6 +37,7 @@ TRACE_DTYPE = np.dtype([
     ("period", np.int64), ("nvars", np.int64), ("ncarry", np.int64), ("naccess", np.int64),
     ("peak_bytes", np.int64), ("peak_index", np.int64), ("duration_us", np.float64),
     ("footprint_bytes", np.int64), ("edges", np.int64), ("ncand", np.int64), ("load_min", np.int64),
+    ("norder", np.int64),
 ], align=True)
 
 BUDGET_DTYPE = np.dtype([
@@ -57,7 +58,7 @@ class MpSweepIn(C.Structure):
         "ev_off", "kind", "var", "size", "t_us", "var_off", "name_blob", "name_off")]
 
 
-assert TRACE_DTYPE.itemsize == 104 and BUDGET_DTYPE.itemsize == 72
+assert TRACE_DTYPE.itemsize == 112 and BUDGET_DTYPE.itemsize == 72
 
 
 @dataclass
@@ -169,8 +170,9 @@ class SweepResult:
         return self.offsets[e0:e0 + int(self.traces["nvars"][t])]
 
     def order_of(self, t: int) -> np.ndarray:
+        """The SWDOA greedy picks the budgets needed (a prefix of the full order)."""
         e0 = int(self.ev_off[t])
-        return self.cand_order[e0:e0 + int(self.traces["ncand"][t])]
+        return self.cand_order[e0:e0 + int(self.traces["norder"][t])]
 
     def selection_of(self, t: int, b: int) -> np.ndarray:
         return self.order_of(t)[:int(self.budgets["nsel"][t, b])]

@@ -138,9 +138,12 @@ def check_sweep_unit(rec, brec, offsets, order, gold: dict) -> None:
            "peak_index": int(rec["peak_index"]), "duration": fhex(rec["duration_us"]),
            "footprint": int(rec["footprint_bytes"]), "edges": int(rec["edges"]),
            "ncand": int(rec["ncand"]), "load_min": int(rec["load_min"]),
-           "offsets": [int(x) for x in offsets], "order": [int(x) for x in order]}
+           "offsets": [int(x) for x in offsets]}
     want = {k: gold[k] for k in got}
     assert got == want
+    # the greedy prefix the budgets need (the reference's full order cut)
+    assert int(rec["norder"]) == len(order) <= len(gold["order"])
+    assert [int(x) for x in order] == gold["order"][:len(order)]
     assert len(brec) == len(gold["budgets"])
     code = {"ValueError": 6, "LimitUnreachable": 3, "SwapDeadlock": 4, "IndexError": 5}
     for b, g in zip(brec, gold["budgets"]):
@@ -154,6 +157,7 @@ def check_sweep_unit(rec, brec, offsets, order, gold: dict) -> None:
                 assert int(b["err_index"]) == e[1], (b, g)
             continue
         nsel = int(b["nsel"])
+        assert nsel <= len(order)
         got_b = {"selection": [int(x) for x in order[:nsel]], "selected_bytes": int(b["selected_bytes"]),
                  "rounds": int(b["rounds"]), "overhead_us": fhex(b["overhead_us"]),
                  "achieved": int(b["achieved_peak_bytes"]), "planned": int(b["planned_peak_bytes"])}

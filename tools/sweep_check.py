@@ -69,7 +69,7 @@ def main():
     ds.set_profile(True)
     ds.run(prm)
     prof = ds.profile()
-    names = ("group+validate+detect", "extract+loads", "prep+cand+loadmin", "greedy", "sim prep", "join(place)", "budgets")
+    names = ("group+validate+detect", "extract+loads", "prep+cand+loadmin", "greedy", "sim prep+publish", "to join", "tail")
     tot = prof.sum(axis=1)
     top = np.argsort(-tot)[:5]
     print("phase cycles: median over traces / the 5 slowest traces")
