@@ -150,9 +150,9 @@ struct PlaceArrays {
   int4 *rseg;
   int64_t *rsize;
   uint32_t *adj;
-  // every placed range, sorted by start (double-buffered): start, end, rank
-  int64_t *ls[2], *le[2];
-  int32_t *lr[2];
+  // every placed range, sorted by start: start, end, rank
+  int64_t *ls, *le;
+  int32_t *lr;
   int64_t n2, words;
   template <class A>
   __host__ __device__ void take(A &b, int64_t V) {
@@ -164,11 +164,9 @@ struct PlaceArrays {
     kbase = b.template take<int32_t>(V);
     rseg = b.template take<int4>(V);
     rsize = b.template take<int64_t>(V);
-    for (int i = 0; i < 2; i++) {
-      ls[i] = b.template take<int64_t>(V);
-      le[i] = b.template take<int64_t>(V);
-      lr[i] = b.template take<int32_t>(V);
-    }
+    ls = b.template take<int64_t>(V);
+    le = b.template take<int64_t>(V);
+    lr = b.template take<int32_t>(V);
     adj = b.template take<uint32_t>(V * words);
   }
 };
@@ -390,6 +388,82 @@ __device__ void sweep_fail(const SweepArgs &a, int64_t t, int status, int code, 
     a.brec[t * a.prm.nbudget + b] = rb;
   }
   __syncthreads();
+}
+
+// SwapPlanner(limit, score="swdoa").fit (estimators.py:85-130) for budgets
+// pulled from the shared counter, one warp each.
+static __device__ __forceinline__ void sweep_budgets(SweepShared *shp, const SwapKeep kp, const ProfView P,
+                                                  const int64_t peak, const double *fracs, const int nbudget,
+                                                  const int max_rounds, mp_sweep_budget *brec, long long *prof) {
+  SweepShared &sh = *shp;
+  const int lane = threadIdx.x & 31;
+  const int64_t k_ = sh.gsm[0], lmin = sh.gsm[1], l0 = sh.gsm[2], nord = sh.gsm[3], nevt = sh.gsm[4];
+  const CandView cv{k_, kp.c.size, kp.c.out_index, kp.c.in_index, kp.name_rank, kp.c.out_t, kp.c.out_ready,
+                    kp.c.in_t, kp.c.dout, kp.c.din, kp.c.spans};
+  for (;;) {
+    int b = 0;
+    if (lane == 0) b = atomicAdd(&sh.next_budget, 1);
+    b = __shfl_sync(FULL_MASK, b, 0);
+    if (b >= nbudget) break;
+    mp_sweep_budget rb{};
+    const int64_t limit = (int64_t)((double)peak * fracs[b]);
+    rb.limit_bytes = limit;
+    if (limit <= 0) {
+      rb.status = MP_E_VALUE;  // check_positive, validation.py:32-34
+    } else if (limit < peak && limit < lmin) {
+      rb.status = MP_E_LIMIT_UNREACHABLE;  // estimators.py:98-100
+      rb.err_aux = lmin;
+    } else {
+      // select_by_swdoa: the greedy stops at the first planned peak <= limit
+      int64_t m = -1;
+      for (int64_t j = 0; j <= nord; j++)
+        if (f_le_i(kp.peaks[j], limit)) { m = j; break; }
+      if (m < 0) {  // only when the greedy ran through every candidate
+        rb.status = MP_E_LIMIT_UNREACHABLE;  // autoswap.py:222-224
+        rb.err_aux = (int64_t)kp.peaks[nord];
+      } else {
+        SimScratch S = sh.ba[b].S;
+        S.delta = kp.delta;
+        const SimTimes T = sh.ba[b].T;
+        const int32_t *sel = kp.order;
+        long long bytes = 0;
+        for (int64_t q = lane; q < m; q += 32) {
+          S.ready[q] = cv.out_ready[sel[q]];   // build_schedule, swapsim.py:111-116
+          S.deadline[q] = cv.in_t[sel[q]];
+          bytes += cv.size[sel[q]];
+        }
+        bytes = warp_sum(bytes);
+        __syncwarp();
+        long long c0 = clock64();
+        make_schedule(cv, sel, m, S.ready, S.deadline, T.t_so, T.t_eo, T.t_si, T.t_ei, T.eord, S);
+        PeakCurve lp{};
+        sim_overlay(P, cv, sel, m, l0, T.t_eo, T.t_si, T.eord, kp.ev_t, kp.ev_d, nevt, S, lp);
+        long long c1 = clock64();
+        Replay<PeakCurve> rep{};
+        SimResult res = sim_fixed_point<false>(P, cv, sel, m, limit, 1, max_rounds, l0, S, T, rep);
+        if (b == 0 && lane == 0 && prof) {
+          prof[12] = c1 - c0;
+          prof[13] = clock64() - c1;
+          prof[14] = res.rounds;
+          prof[15] = m;
+        }
+        rb.status = res.status;
+        rb.nsel = m;
+        rb.selected_bytes = bytes;
+        if (res.status == MP_OK) {
+          rb.rounds = (int32_t)res.rounds;
+          rb.overhead_us = res.delay;
+          rb.achieved_peak_bytes = rep.cv.peak;
+          rb.planned_peak_bytes = lp.peak;
+        } else if (res.status == MP_E_SWAP_DEADLOCK) {
+          rb.err_index = res.eidx;
+          rb.err_aux = res.eaux1;
+        }
+      }
+    }
+    if (lane == 0) brec[b] = rb;
+    __syncwarp();
+  }
 }
 
 __device__ void sweep_one(const SweepArgs &a, int64_t t, char *slab, char *fast, size_t fast_bytes,
@@ -632,68 +706,10 @@ __device__ void sweep_one(const SweepArgs &a, int64_t t, char *slab, char *fast,
   const LoadView L{p, loads, kp.tau, dur};
   const ProfView P{p, V, start, dur, kp.tau, pa.nseg, pa.seg, pa.size};
   // SwapPlanner(limit, score="swdoa").fit for budgets pulled from a shared
-  // counter, one warp each; the swap path's scalars come through shared
-  // memory (published before swap_ready)
+  // counter, one warp each
   auto run_budgets = [&]() {
-    const int64_t k_ = sh.gsm[0], lmin = sh.gsm[1], l0 = sh.gsm[2], nord = sh.gsm[3], nevt = sh.gsm[4];
-    const CandView cv{k_, kp.c.size, kp.c.out_index, kp.c.in_index, kp.name_rank, kp.c.out_t, kp.c.out_ready,
-                      kp.c.in_t, kp.c.dout, kp.c.din, kp.c.spans};
-    for (;;) {
-      int b = 0;
-      if (lane == 0) b = atomicAdd(&sh.next_budget, 1);
-      b = __shfl_sync(FULL_MASK, b, 0);
-      if (b >= prm.nbudget) break;
-      mp_sweep_budget rb{};
-      const int64_t limit = (int64_t)((double)peak * prm.budget_frac[b]);
-      rb.limit_bytes = limit;
-      if (limit <= 0) {
-        rb.status = MP_E_VALUE;  // check_positive, validation.py:32-34
-      } else if (limit < peak && limit < lmin) {
-        rb.status = MP_E_LIMIT_UNREACHABLE;  // estimators.py:98-100
-        rb.err_aux = lmin;
-      } else {
-        // select_by_swdoa: the greedy stops at the first planned peak <= limit
-        int64_t m = -1;
-        for (int64_t j = 0; j <= nord; j++)
-          if (f_le_i(kp.peaks[j], limit)) { m = j; break; }
-        if (m < 0) {  // only when the greedy ran through every candidate
-          rb.status = MP_E_LIMIT_UNREACHABLE;  // autoswap.py:222-224
-          rb.err_aux = (int64_t)kp.peaks[nord];
-        } else {
-          SimScratch S = sh.ba[b].S;
-          S.delta = kp.delta;
-          const SimTimes T = sh.ba[b].T;
-          const int32_t *sel = kp.order;
-          long long bytes = 0;
-          for (int64_t q = lane; q < m; q += 32) {
-            S.ready[q] = cv.out_ready[sel[q]];   // build_schedule, swapsim.py:111-116
-            S.deadline[q] = cv.in_t[sel[q]];
-            bytes += cv.size[sel[q]];
-          }
-          bytes = warp_sum(bytes);
-          __syncwarp();
-          make_schedule(cv, sel, m, S.ready, S.deadline, T.t_so, T.t_eo, T.t_si, T.t_ei, T.eord, S);
-          PeakCurve lp{};
-          sim_overlay(P, cv, sel, m, l0, T.t_eo, T.t_si, T.eord, kp.ev_t, kp.ev_d, nevt, S, lp);
-          Replay<PeakCurve> rep{};
-          SimResult res = sim_fixed_point<false>(P, cv, sel, m, limit, 1, prm.max_rounds, l0, S, T, rep);
-          rb.status = res.status;
-          rb.nsel = m;
-          rb.selected_bytes = bytes;
-          if (res.status == MP_OK) {
-            rb.rounds = (int32_t)res.rounds;
-            rb.overhead_us = res.delay;
-            rb.achieved_peak_bytes = rep.cv.peak;
-            rb.planned_peak_bytes = lp.peak;
-          } else if (res.status == MP_E_SWAP_DEADLOCK) {
-            rb.err_index = res.eidx;
-            rb.err_aux = res.eaux1;
-          }
-        }
-      }
-      if (lane == 0) a.brec[t * prm.nbudget + b] = rb;
-      __syncwarp();
-    }
+    sweep_budgets(&sh, kp, P, peak, a.prm.budget_frac, prm.nbudget, prm.max_rounds, a.brec + t * prm.nbudget,
+                  a.prof ? a.prof + t * 16 : nullptr);
   };
 
   int64_t k = 0, load_min = 0, live0 = 0, na = 0, norder = 0;
@@ -705,9 +721,8 @@ __device__ void sweep_one(const SweepArgs &a, int64_t t, char *slab, char *fast,
     // (smartpool.py:101-119) is one pass over it — then the new range
     // is inserted in order.
     int64_t edges = 0;
-    // the two list buffers, swapped each step (kept in registers)
-    int64_t *ls = pl.ls[0], *le = pl.le[0], *ds = pl.ls[1], *de = pl.le[1];
-    int32_t *lr = pl.lr[0], *dr = pl.lr[1];
+    int64_t *const ls = pl.ls, *const le = pl.le;
+    int32_t *const lr = pl.lr;
     long long c_scan = 0, c_ins = 0, c_t0 = clock64();
     for (int64_t q = 0; q < V; q++) {
       const uint32_t *row = pl.adj + q * pl.words;
@@ -780,12 +795,18 @@ __device__ void sweep_one(const SweepArgs &a, int64_t t, char *slab, char *fast,
         int64_t i = c0 + lane;
         pos += __popc(__ballot_sync(FULL_MASK, i < q && ls[i] < off));
       }
-      for (int64_t i = lane; i <= q; i += 32) {
-        if (i < pos) { ds[i] = ls[i]; de[i] = le[i]; dr[i] = lr[i]; }
-        else if (i == pos) { ds[i] = off; de[i] = off + need; dr[i] = (int32_t)q; }
-        else { ds[i] = ls[i - 1]; de[i] = le[i - 1]; dr[i] = lr[i - 1]; }
+      // shift [pos, q) up by one in place, highest chunk first
+      for (int64_t c1 = q; c1 > pos; c1 -= 32) {
+        const int64_t i = c1 - 32 + lane;
+        const bool mv = i >= pos;
+        int64_t vs = 0, ve = 0;
+        int32_t vr = 0;
+        if (mv) { vs = ls[i]; ve = le[i]; vr = lr[i]; }
+        __syncwarp();
+        if (mv) { ls[i + 1] = vs; le[i + 1] = ve; lr[i + 1] = vr; }
+        __syncwarp();
       }
-      { int64_t *x = ls; ls = ds; ds = x; x = le; le = de; de = x; int32_t *y = lr; lr = dr; dr = y; }
+      if (lane == 0) { ls[pos] = off; le[pos] = off + need; lr[pos] = (int32_t)q; }
       __syncwarp();
       c_ins += clock64() - c_b;
     }

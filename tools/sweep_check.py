@@ -78,6 +78,8 @@ def main():
     ex = ds.profile_extra
     print("  placement loop cycles (5 slowest):", [int(ex[t, 1] - ex[t, 0]) for t in top],
           "scan", [int(ex[t, 2]) for t in top], "insert", [int(ex[t, 3]) for t in top])
+    print("  budget 0 (5 slowest): sched+overlay", [int(ex[t, 4]) for t in top], "replay", [int(ex[t, 5]) for t in top],
+          "rounds", [int(ex[t, 6]) for t in top], "nsel", [int(ex[t, 7]) for t in top])
     print("  slowest traces:", [(int(t), batch.events_of(int(t)), int(res.traces['nvars'][t]), int(res.traces['ncand'][t])) for t in top])
     t0 = time.perf_counter()
     recs, brecs, offs, orders = orc.sweep(batch, prm)
