@@ -190,6 +190,10 @@ struct SwapKeep {
     peaks = b.template take<double>(V + 1);
     tau = b.template take<double>(p);
     delta = b.template take<int64_t>(p);
+  }
+  // the overlay's op events are read once per budget: global scratch
+  template <class A>
+  __host__ __device__ void take_events(A &b, int64_t p) {
     ev_t = b.template take<double>(p);
     ev_d = b.template take<int64_t>(p);
   }
@@ -263,7 +267,7 @@ static size_t slab_bound(int64_t n, int64_t nv, int nb) {
   TimeArrays ta; ta.take(b, p);
   ProfileArrays pa; pa.take(b, p, V);
   PlaceArrays pl; pl.take(b, V);
-  SwapKeep kp; kp.take(b, p, V);
+  SwapKeep kp; kp.take(b, p, V); kp.take_events(b, p);
   SwapScratch ss; ss.take(b, p, V);
   GreedyArrays gr; gr.take(b, p, V);
   for (int i = 0; i < nb; i++) { BudgetArrays ba; ba.take(b, p, V); }
@@ -641,6 +645,7 @@ __device__ void sweep_one(const SweepArgs &a, int64_t t, char *slab, char *fast,
   ar.phase();
   SwapKeep kp;
   kp.take(ar, p, V);
+  kp.take_events(bump, p);
   PlaceArrays pl;
   pl.take(ar, V);
   // the budgets refill the arena from here once the greedy's arrays are dead
