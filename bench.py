@@ -57,56 +57,69 @@ def hbm_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def _nvml_sampler(index, period, stop, conn):
+    """Child process: NVML SM clock + clock-event reasons every `period` s
+    until `stop` is set (a separate process, so sampling never holds the
+    benchmark's GIL)."""
+    names = ClockSampler.NAMES
+    samples = []
+    try:
+        import pynvml as nv
+        nv.nvmlInit()
+        h = nv.nvmlDeviceGetHandleByIndex(index)
+        bits = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
+        mx = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+        while not stop.is_set():
+            sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            samples.append((sm, mx, tuple(n for n, b in zip(names, bits) if r & b)))
+            stop.wait(period)
+    except Exception:  # noqa: BLE001
+        fields = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                  "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                  "clocks_event_reasons.sw_power_cap")
+        while not stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(index), f"--query-gpu={fields}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                f = [x.strip() for x in out.split(",")]
+                samples.append((float(f[0]), float(f[1]),
+                                tuple(n for i, n in enumerate(names) if f[2 + i].lower().startswith("active"))))
+            except Exception:  # noqa: BLE001
+                pass
+            stop.wait(0.05)
+    conn.send(samples)
+    conn.close()
+
+
 class ClockSampler:
     """SM clocks and clock-event (throttle) reasons sampled through NVML every
-    2 ms while the timed region runs (nvidia-smi as the fallback)."""
+    2 ms while the timed region runs, in a child process."""
 
     NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, index: int, period_s: float = 0.002):
-        self.index = index
-        self.period = period_s
-        self.samples = []  # (sm_mhz, max_mhz, reasons tuple)
-        self._stop = threading.Event()
-        self._t = threading.Thread(target=self._run, daemon=True)
-
-    def _run(self):
-        try:
-            import pynvml as nv
-            nv.nvmlInit()
-            h = nv.nvmlDeviceGetHandleByIndex(self.index)
-            bits = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
-                    nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
-            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-            while not self._stop.is_set():
-                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.samples.append((float(sm), float(mx), tuple(n for n, b in zip(self.NAMES, bits) if r & b)))
-                self._stop.wait(self.period)
-            return
-        except Exception:  # noqa: BLE001
-            pass
-        fields = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={fields}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                f = [x.strip() for x in out.split(",")]
-                self.samples.append((float(f[0]), float(f[1]),
-                                     tuple(n for i, n in enumerate(self.NAMES) if f[2 + i].lower().startswith("active"))))
-            except Exception:  # noqa: BLE001
-                pass
-            self._stop.wait(0.05)
+        import multiprocessing as mp
+        ctx = mp.get_context("fork")
+        self._stop = ctx.Event()
+        self._recv, send = ctx.Pipe(duplex=False)
+        self._p = ctx.Process(target=_nvml_sampler, args=(index, period_s, self._stop, send), daemon=True)
+        self.samples = []
 
     def __enter__(self):
-        self._t.start()
+        self._p.start()
+        time.sleep(0.05)  # the child's first samples precede the timed region
         return self
 
     def __exit__(self, *exc):
         self._stop.set()
-        self._t.join(timeout=10)
+        try:
+            if self._recv.poll(10):
+                self.samples = self._recv.recv()
+        finally:
+            self._p.join(timeout=10)
 
     def summary(self):
         if not self.samples:
@@ -298,9 +311,23 @@ def run_sweep_bench(args, rank, world, local_rank):
     launches = (N.launches() - l0) / max(args.steps, 1)
     res = ds.download()
     ds.close()
+    # e2e: the public call from pinned host buffers (inputs and records)
+    keep = []
+
+    def pinned(nbytes):
+        t = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+        keep.append(t)
+        return t.numpy()
+
+    hb = mine.copy_to(pinned)
+    nev = max(int(mine.ev_off[-1]), 1)
+    hout = sweep.SweepResult(pinned(res.traces.nbytes).view(sweep.TRACE_DTYPE),
+                             pinned(max(res.budgets.nbytes, 1)).view(sweep.BUDGET_DTYPE)[:res.budgets.size]
+                             .reshape(res.budgets.shape),
+                             pinned(nev * 8).view(np.int64), pinned(nev * 4).view(np.int32), hb.ev_off, params, hb)
     e2e_ms = []
     for i in range(args.warmup + args.steps):
-        ms, out = timed(lambda: sweep.run_sweep(mine, params))
+        ms, out = timed(lambda: sweep.run_sweep(hb, params, out=hout))
         if i >= args.warmup:
             e2e_ms.append(ms)
     step_ms, e2e_step = float(np.mean(res_ms)), float(np.mean(e2e_ms))

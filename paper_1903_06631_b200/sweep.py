@@ -88,6 +88,19 @@ class SweepBatch:
     """Traces concatenated column-wise (host numpy); trace t's events are
     rows ev_off[t]:ev_off[t+1], its names ids var_off[t]:var_off[t+1]."""
 
+    COLUMNS = ("kind", "var", "size", "t_us", "ev_off", "var_off", "name_blob", "name_off")
+
+    def copy_to(self, alloc) -> "SweepBatch":
+        """The same batch in buffers from ``alloc(nbytes) -> uint8 array`` (e.g.
+        pinned host memory, so uploads are asynchronous DMA)."""
+        cols = {}
+        for c in self.COLUMNS:
+            a = getattr(self, c)
+            buf = alloc(max(a.nbytes, 1)).view(a.dtype)[:a.size]
+            buf[...] = a
+            cols[c] = buf
+        return SweepBatch(**cols)
+
     def __init__(self, kind, var, size, t_us, ev_off, var_off, name_blob, name_off):
         self.kind = np.ascontiguousarray(kind, np.uint8)
         self.var = np.ascontiguousarray(var, np.int32)
@@ -283,15 +296,18 @@ class DeviceSweep:
             pass
 
 
-def run_sweep(traces, params: SweepParams | None = None) -> SweepResult:
+def run_sweep(traces, params: SweepParams | None = None, out: SweepResult | None = None) -> SweepResult:
     """Plan every trace of a batch (a SweepBatch or a list of traces) on the
-    device: upload, one sweep launch, download."""
+    device: upload, one sweep launch, download.  ``out`` (e.g. pinned
+    buffers from ``SweepResult.empty_like``) receives the records."""
     batch = traces if isinstance(traces, SweepBatch) else SweepBatch.from_traces(traces)
     params = params or SweepParams()
     ds = DeviceSweep(batch)
     try:
         ds.run(params)
-        return ds.download()
+        if out is None:
+            return ds.download()
+        return ds.download(out.traces, out.budgets, out.offsets, out.cand_order)
     finally:
         ds.close()
 
