@@ -83,3 +83,27 @@ def test_device_arcs_match_reference(name):
         offs, foot, _ = N.plan_pool(g, code, n)
         assert pack(offs.tolist()) == sc["plans"][pol]["offsets"], pol
         assert foot == sc["plans"][pol]["footprint"]
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_plan_arrays_paths_match_oracle(seed):
+    """plan_arrays through the one-CTA path (small traces) and the grid path
+    give the oracle's plan (pipeline.py)."""
+    import oracle as orc
+    from paper_1903_06631_b200 import workloads
+    from paper_1903_06631_b200.pipeline import plan_arrays
+    from paper_1903_06631_b200.trace import as_arrays
+    tr = workloads.random_periodic_trace(seed, slots=40, nvars=12, iterations=5)
+    arrays = as_arrays(tr)
+    for policy, code in (("best_fit", 1), ("first_fit", 0)):
+        rc, p = orc.detect(arrays)
+        rc, fp = orc.extract(arrays, len(arrays) - p, len(arrays))
+        off, lo, hi = orc.profile_segments(fp)
+        h, _r, _c = orc.conflict(off, lo, hi)
+        rc, offs, foot = orc.plan(h, fp.size, fp.alloc.astype(np.int64), fp.base, fp.name_ralloc(), fp.name_blob,
+                                  fp.name_off, code)
+        orc.graph_free(h)
+        for path in ("cta", "grid"):
+            plan = plan_arrays(arrays, policy=policy, path=path)
+            assert np.array_equal(plan.offsets, offs), (path, policy)
+            assert plan.footprint_bytes == foot and plan.peak_bytes == fp.peak_bytes and plan.period == p
