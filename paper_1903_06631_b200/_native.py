@@ -17,7 +17,8 @@ from ._abi import (MP_OK, FlatProfile, MpErr, MpProfileDims, MpProfileOut, ptr,
                    raise_for, trace_in)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmemplan_b200.so")
+# MEMPLAN_LIB: an alternative build of the same library (A/B kernel experiments, tools/ab_place.sh)
+LIB_PATH = os.environ.get("MEMPLAN_LIB") or os.path.join(HERE, "libmemplan_b200.so")
 
 _lib = None
 _ctx = None

@@ -121,6 +121,15 @@ __device__ __forceinline__ int warp_max_i32(int v) {
   return v;
 }
 
+// One compare-exchange step of a bitonic network on a 64-bit key: one
+// 64-bit compare and one select (the keys are unique up to equal padding,
+// so "take the partner" is a single predicate: the lane keeps the minimum
+// iff it sits low in an ascending block, and the partner is the minimum
+// iff it compares below).
+__device__ __forceinline__ uint64_t cx_key(uint64_t x, uint64_t o, bool keep_min) {
+  return ((o < x) == keep_min) ? o : x;
+}
+
 // bitonic sort of 32*K unsigned keys held as element i = r*32 + lane
 template <int K>
 __device__ __forceinline__ void warp_bitonic_keys(uint64_t (&x)[K]) {
@@ -136,9 +145,10 @@ __device__ __forceinline__ void warp_bitonic_keys(uint64_t (&x)[K]) {
           if ((r & jr) == 0) {
             const int r2 = r | jr;
             const bool up = ((r * 32) & k) == 0;
-            uint64_t lo = min(x[r], x[r2]), hi = max(x[r], x[r2]);
-            x[r] = up ? lo : hi;
-            x[r2] = up ? hi : lo;
+            bool sw = (x[r2] < x[r]) == up;
+            uint64_t a = sw ? x[r2] : x[r], b = sw ? x[r] : x[r2];
+            x[r] = a;
+            x[r2] = b;
           }
         }
       } else {
@@ -147,7 +157,51 @@ __device__ __forceinline__ void warp_bitonic_keys(uint64_t (&x)[K]) {
           uint64_t o = __shfl_xor_sync(FULL_MASK, x[r], j);
           const bool up = ((r * 32 + lane) & k) == 0;
           const bool lower = (lane & j) == 0;
-          x[r] = (lower == up) ? min(x[r], o) : max(x[r], o);
+          x[r] = cx_key(x[r], o, lower == up);
+        }
+      }
+    }
+  }
+}
+
+// The same network with the stage loops rolled (runtime k, j): a fraction
+// of the code of the unrolled form, for the rarer long rows, so the hot
+// loop stays inside the instruction cache.
+template <int K>
+__device__ __forceinline__ void warp_bitonic_keys_rolled(uint64_t (&x)[K]) {
+  static_assert(K == 2 || K == 4, "rolled network is for 64 or 128 keys");
+  const int lane = threadIdx.x & 31;
+#pragma unroll 1
+  for (int k = 2; k <= 32 * K; k <<= 1) {
+#pragma unroll 1
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+        if (K == 4 && j == 64) {
+#pragma unroll
+          for (int r = 0; r < 2; r++) {
+            const bool up = ((r * 32) & k) == 0;
+            bool sw = (x[r + 2] < x[r]) == up;
+            uint64_t a = sw ? x[r + 2] : x[r], b = sw ? x[r] : x[r + 2];
+            x[r] = a;
+            x[r + 2] = b;
+          }
+        } else {
+#pragma unroll
+          for (int r = 0; r < K; r += 2) {
+            const bool up = ((r * 32) & k) == 0;
+            bool sw = (x[r + 1] < x[r]) == up;
+            uint64_t a = sw ? x[r + 1] : x[r], b = sw ? x[r] : x[r + 1];
+            x[r] = a;
+            x[r + 1] = b;
+          }
+        }
+      } else {
+        const bool lower = (lane & j) == 0;
+#pragma unroll
+        for (int r = 0; r < K; r++) {
+          uint64_t o = __shfl_xor_sync(FULL_MASK, x[r], j);
+          const bool up = ((r * 32 + lane) & k) == 0;
+          x[r] = cx_key(x[r], o, lower == up);
         }
       }
     }

@@ -21,9 +21,39 @@
 // waiting for a whole wavefront.  The CSR rows arrive partitioned into
 // predecessors and successors by the conflict build (conflict.cu).
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 #include "handles.cuh"
 #include "place_dev.cuh"
+
+// PLACE_TRACE=1 builds (tools/place_trace.py) record per-variable
+// %globaltimer stamps: placed, claimed, made ready, gathered, sorted.
+#ifndef PLACE_TRACE
+#define PLACE_TRACE 0
+#endif
+// experiment switches (tools/ab_place.sh)
+#ifndef PLACE_SUCC_PIPE
+#define PLACE_SUCC_PIPE 2  // 1: batched relaxed successor decrements between two fences; 2: that for rows with > 32 successors, one acq_rel atomic per successor otherwise; 0: never
+#endif
+#ifndef PLACE_FIRST_ACQ
+#define PLACE_FIRST_ACQ 1  // first queue probe with acquire
+#endif
+#ifndef PLACE_BACKOFF
+#define PLACE_BACKOFF 1    // exponential idle backoff
+#endif
+#ifndef PLACE_K4_ROLLED
+#define PLACE_K4_ROLLED 1  // rolled stage loops for 65..128 predecessors
+#endif
+#define PT_STAMP(slot, v)                                                 \
+  do {                                                                    \
+    if (PLACE_TRACE && a.tdone) {                                         \
+      unsigned long long t_;                                              \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)::"memory");    \
+      a.tdone[(slot) * a.V + (v)] = t_;                                   \
+    }                                                                     \
+  } while (0)
 
 struct PlaceArgs {
   int64_t V;
@@ -43,6 +73,8 @@ struct PlaceArgs {
   unsigned long long *arena_top;
   long long *footprint;
   int32_t *depth;
+  int32_t dbg_v;
+  unsigned long long *tdone;  // debug (MP_PLACE_TRACE): %globaltimer when each variable was placed
 };
 
 // Gather the predecessors' ranges, sort them by start and replay
@@ -75,7 +107,10 @@ __device__ __forceinline__ int64_t place_reg(const PlaceArgs &a, int64_t rb, int
   ok = !__any_sync(FULL_MASK, big);
   if (!ok) return 0;
   lvl = warp_max_i32(lv) + 1;
-  warp_bitonic_keys<K>(x);
+  if (lane == 0) PT_STAMP(3, a.dbg_v);
+  if constexpr (K <= 2 || !PLACE_K4_ROLLED) warp_bitonic_keys<K>(x);
+  else warp_bitonic_keys_rolled<K>(x);
+  if (lane == 0) PT_STAMP(4, a.dbg_v);
   HoleState h{0, 0, 0, false};
 #pragma unroll
   for (int r = 0; r < K; r++) {
@@ -124,11 +159,22 @@ __device__ int64_t place_mem(const PlaceArgs &a, P buf, int64_t rb, int m, int64
   return h.found ? h.best_off : h.top;
 }
 
+__device__ __forceinline__ int atom_dec_relaxed(int32_t *p) {
+  int old;
+  asm volatile("atom.relaxed.gpu.global.add.s32 %0, [%1], -1;" : "=r"(old) : "l"(p) : "memory");
+  return old;
+}
+
 __device__ __forceinline__ int atom_sub_acq_rel(int32_t *p) {
   int old;
   asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], -1;" : "=r"(old) : "l"(p) : "memory");
   return old;
 }
+
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+constexpr int SUCC_BATCH = 4;                // successor rows of 32 decremented per round trip
+constexpr unsigned PLACE_MAX_SLEEP = 256;    // ns, idle-warp poll backoff cap
 
 constexpr int PLACE_THREADS = 256;
 constexpr int PLACE_MIN_BLOCKS = 5;  // <= 48 registers: 40 resident warps per SM
@@ -192,30 +238,100 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_MIN_BLOCKS) k_place_async
         // was published; continuation means not every variable passes
         // through the queue, so an empty slot ends the warp once all are placed
         const int32_t *q = a.queue + (i < a.V ? i : 0);
-        for (;;) {
-          if (i < a.V) asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v1) : "l"(q) : "memory");
-          if (v1) break;
-          if (*(volatile int *)a.done >= a.V) { v1 = -1; break; }
-          __nanosleep(20);
+        // idle warps back off exponentially and look at the done count only
+        // now and then: thousands of pollers on one line slow the L2 slice
+        // the working warps' atomics go through
+        unsigned ns = 32;
+        // first probe with acquire (in a busy phase the slot is usually
+        // filled already); later probes relaxed (an acquire load
+        // invalidates L1 on every probe), acquiring once the slot is filled
+        if (PLACE_FIRST_ACQ && i < a.V) asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v1) : "l"(q) : "memory");
+        for (int spin = 0; !v1; spin++) {
+          if (i < a.V) asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v1) : "l"(q) : "memory");
+          if (v1) {
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v1) : "l"(q) : "memory");
+            break;
+          }
+          if ((!PLACE_BACKOFF || (spin & 7) == 7) && *(volatile int *)a.done >= a.V) { v1 = -1; break; }
+          __nanosleep(PLACE_BACKOFF ? ns : 20);
+          if (ns < PLACE_MAX_SLEEP) ns <<= 1;
         }
       }
       v1 = __shfl_sync(FULL_MASK, v1, 0);
       if (v1 < 0) break;
       v = v1 - 1;
     }
+    if (lane == 0) PT_STAMP(1, v);
     int64_t rb = a.row_off[v], re = a.row_off[v + 1];
     int m = a.pcnt[v];
     int64_t need = a.size[v];
     int lvl;
+#if PLACE_TRACE
+    PlaceArgs ad = a;
+    ad.dbg_v = v;
+    int64_t o = place_var(ad, v, gwarp, rb, m, need, lvl);
+#else
     int64_t o = place_var(a, v, gwarp, rb, m, need, lvl);
+#endif
     if (lane == 0) {
       a.off[v] = o;
       a.level[v] = lvl;
       if (o + need > fp) fp = o + need;
       if (lvl > dmax) dmax = lvl;
+      PT_STAMP(0, v);
     }
     local_done++;
     __syncwarp();
+    if (PLACE_SUCC_PIPE && re - (rb + m) > (PLACE_SUCC_PIPE == 2 ? 32 : 0)) {
+      // release this variable's offset (stored by lane 0; the fence is
+      // cumulative over the warp barrier above), then decrement every
+      // successor's counter with relaxed atomics, SUCC_BATCH rows of 32 in
+      // flight at once instead of one acq_rel round trip per 32
+      fence_acq_rel_gpu();
+      for (int64_t base = rb + m; base < re; base += 32 * SUCC_BATCH) {
+        int32_t jj[SUCC_BATCH];
+        int rem[SUCC_BATCH];
+#pragma unroll
+        for (int c = 0; c < SUCC_BATCH; c++) {
+          int64_t k = base + c * 32 + lane;
+          jj[c] = k < re ? a.col[k] : -1;
+        }
+#pragma unroll
+        for (int c = 0; c < SUCC_BATCH; c++) rem[c] = jj[c] >= 0 ? atom_dec_relaxed(&a.remaining[jj[c]]) : 0;
+        bool any = false;
+#pragma unroll
+        for (int c = 0; c < SUCC_BATCH; c++) any |= rem[c] == 1;
+        if (!__any_sync(FULL_MASK, any)) continue;
+        // acquire the other predecessors' offsets for the successors this
+        // warp completed, and release them to whoever claims a published one
+        fence_acq_rel_gpu();
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < SUCC_BATCH; c++) {
+          bool ready = rem[c] == 1;
+          int32_t j = jj[c];
+          if (ready) PT_STAMP(2, j);
+          unsigned bal = __ballot_sync(FULL_MASK, ready);
+          if (bal && next < 0) {
+            // keep the first newly ready successor; publish the rest
+            int keep = __ffs(bal) - 1;
+            next = __shfl_sync(FULL_MASK, j, keep);
+            bal &= bal - 1;
+            if (lane == keep) ready = false;
+          }
+          if (bal) {
+            int qb = 0;
+            if (lane == __ffs(bal) - 1) qb = atomicAdd(a.tail, __popc(bal));
+            qb = __shfl_sync(FULL_MASK, qb, __ffs(bal) - 1);
+            if (ready) {
+              int32_t *q = a.queue + qb + __popc(bal & lanemask_lt());
+              asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(q), "r"(j + 1) : "memory");
+            }
+          }
+        }
+      }
+    }
+    if (!PLACE_SUCC_PIPE || (PLACE_SUCC_PIPE == 2 && re - (rb + m) <= 32)) {
     for (int64_t k = rb + m + lane; k - lane < re; k += 32) {
       bool ready = false;
       int32_t j = 0;
@@ -226,23 +342,24 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_MIN_BLOCKS) k_place_async
         // predecessor, acquires every other predecessor's
         ready = atom_sub_acq_rel(&a.remaining[j]) == 1;
       }
+      if (ready) PT_STAMP(2, j);
       unsigned bal = __ballot_sync(FULL_MASK, ready);
       if (bal && next < 0) {
-        // keep the first newly ready successor; publish the rest
         int keep = __ffs(bal) - 1;
         next = __shfl_sync(FULL_MASK, j, keep);
         bal &= bal - 1;
         if (lane == keep) ready = false;
       }
       if (bal) {
-        int base = 0;
-        if (lane == __ffs(bal) - 1) base = atomicAdd(a.tail, __popc(bal));
-        base = __shfl_sync(FULL_MASK, base, __ffs(bal) - 1);
+        int qb = 0;
+        if (lane == __ffs(bal) - 1) qb = atomicAdd(a.tail, __popc(bal));
+        qb = __shfl_sync(FULL_MASK, qb, __ffs(bal) - 1);
         if (ready) {
-          int32_t *q = a.queue + base + __popc(bal & lanemask_lt());
+          int32_t *q = a.queue + qb + __popc(bal & lanemask_lt());
           asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(q), "r"(j + 1) : "memory");
         }
       }
+    }
     }
   }
   if (lane == 0) {
@@ -428,22 +545,13 @@ extern "C" int mp_plan_pool(mp_ctx *ctx, mp_dgraph *g, int32_t policy, int64_t *
     return MP_OK;
   }
   DBuf<int32_t> remaining, queue, level, ctr;
-  StageTimer *tm = new StageTimer(ctx, MP_ST_PLACE_SPLIT);
   CUDA_TRY(remaining.alloc(V, st)); CUDA_TRY(queue.alloc(V, st)); CUDA_TRY(level.alloc(V, st));
   CUDA_TRY(ctr.alloc(16, st));
-  CUDA_TRY(cudaMemsetAsync(queue.p, 0, V * 4, st));
-  CUDA_TRY(cudaMemsetAsync(ctr.p, 0, 64, st));
   // ctr: [0] head [1] tail [2] done [3] depth [4..5] footprint [6..7] arena need [8..9] arena top
   long long *d_fp = (long long *)(ctr.p + 4);
   unsigned long long *d_need = (unsigned long long *)(ctr.p + 6);
-  const long long lmin = LLONG_MIN;
-  CUDA_TRY(cudaMemcpyAsync(d_fp, &lmin, 8, cudaMemcpyHostToDevice, st));
-  LAUNCH(ctx, k_ready_init, grid_for(V, 256, 2048), 256, 0, V, g->pcnt.p, remaining.p, queue.p, ctr.p + 1,
-         d_need);
   // the conflict build bounded the long-row scratch by degree (no readback)
   uint64_t arena_need = (uint64_t)g->arena_need;
-  int rc = MP_OK;
-  delete tm;
   static int per_sm_cached = 0;
   DBuf<int64_t> &off = g->offsets;
   CUDA_TRY(off.alloc(V, st));
@@ -451,6 +559,7 @@ extern "C" int mp_plan_pool(mp_ctx *ctx, mp_dgraph *g, int32_t policy, int64_t *
   if (!per_sm_cached)
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_cached, k_place_async, PLACE_THREADS, smem));
   int per_sm = per_sm_cached < 1 ? 1 : per_sm_cached;
+  if (const char *e = getenv("MP_PLACE_BLOCKS_PER_SM")) per_sm = atoi(e) < per_sm ? atoi(e) : per_sm;  // experiments
   // all warps resident: spinning consumers must never starve producers
   int64_t warps_needed = V;
   int64_t nblocks = (int64_t)per_sm * ctx->num_sms;
@@ -462,14 +571,47 @@ extern "C" int mp_plan_pool(mp_ctx *ctx, mp_dgraph *g, int32_t policy, int64_t *
   CUDA_TRY(wscratch.alloc(128 * nblocks * (PLACE_THREADS / 32), st));
   CUDA_TRY(arena.alloc((int64_t)arena_need, st));
   PlaceArgs a{V, g->row_off.p, g->col.p, g->pcnt.p, g->size.p, off.p, level.p, remaining.p, queue.p,
-              ctr.p, ctr.p + 1, ctr.p + 2, policy, wscratch.p, arena.p, (unsigned long long *)(ctr.p + 8), d_fp, ctr.p + 3};
+              ctr.p, ctr.p + 1, ctr.p + 2, policy, wscratch.p, arena.p, (unsigned long long *)(ctr.p + 8), d_fp, ctr.p + 3,
+              0, nullptr};
+  const char *trace_path = PLACE_TRACE ? getenv("MP_PLACE_TRACE") : nullptr;
+  DBuf<unsigned long long> tdone;
+  if (trace_path) {
+    CUDA_TRY(tdone.alloc(5 * V, st));
+    CUDA_TRY(cudaMemsetAsync(tdone.p, 0, 5 * V * 8, st));
+    a.tdone = tdone.p;
+  }
   {
+    {
+      StageTimer tm(ctx, MP_ST_PLACE_SPLIT);
+      CUDA_TRY(cudaMemsetAsync(queue.p, 0, V * 4, st));
+      CUDA_TRY(cudaMemsetAsync(ctr.p, 0, 64, st));
+      const long long lmin = LLONG_MIN;
+      CUDA_TRY(cudaMemcpyAsync(d_fp, &lmin, 8, cudaMemcpyHostToDevice, st));
+      LAUNCH(ctx, k_ready_init, grid_for(V, 256, 2048), 256, 0, V, g->pcnt.p, remaining.p, queue.p, ctr.p + 1,
+             d_need);
+    }
     StageTimer ptm(ctx, MP_ST_PLACE);
     LAUNCH(ctx, k_place_async, (unsigned)nblocks, PLACE_THREADS, smem, a);
   }
   if (offsets) CUDA_TRY(cudaMemcpyAsync(offsets, off.p, V * 8, cudaMemcpyDeviceToHost, st));
+  if (trace_path) {
+    // debug dump: V, level[V] (int32), predecessor count[V] (int32), time
+    // placed[V], time claimed[V], time made ready[V] (ns, 0 = no predecessors)
+    std::vector<int32_t> hl(2 * V);
+    std::vector<unsigned long long> ht(5 * V);
+    CUDA_TRY(cudaMemcpyAsync(hl.data(), level.p, V * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(hl.data() + V, g->pcnt.p, V * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(ht.data(), tdone.p, 5 * V * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (FILE *f = fopen(trace_path, "wb")) {
+      fwrite(&V, 8, 1, f);
+      fwrite(hl.data(), 4, 2 * V, f);
+      fwrite(ht.data(), 8, 5 * V, f);
+      fclose(f);
+    }
+  }
   int32_t tail4[6];
-  rc = dev_read_n(ctx, ctr.p, tail4, 24, err);
+  int rc = dev_read_n(ctx, ctr.p, tail4, 24, err);
   if (rc) return rc;
   *footprint = *(int64_t *)(tail4 + 4);
   if (levels) *levels = tail4[3];
