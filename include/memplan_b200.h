@@ -164,6 +164,12 @@ int mp_ctx_timings(mp_ctx *ctx, double *ms, int64_t *count, mp_err *err);
  * memplan.trace.validate_trace; the first violation is reported exactly as
  * the sequential reference would. */
 int mp_trace_upload(mp_ctx *ctx, const mp_trace_in *in, mp_dtrace **out, mp_err *err);
+/* the same upload without a host wait: the columns go up on a copy stream
+ * (var, kind, size, index, t_us) and each stage waits only for the columns it
+ * reads, so grouping and period detection overlap the rest of the transfer.
+ * The input buffers stay borrowed until mp_trace_wait returns. */
+int mp_trace_upload_async(mp_ctx *ctx, const mp_trace_in *in, mp_dtrace **out, mp_err *err);
+int mp_trace_wait(mp_dtrace *t, mp_err *err);
 int mp_trace_free(mp_dtrace *t);
 /* drop cached derived state (event grouping) so the next stage recomputes it */
 int mp_trace_reset(mp_dtrace *t);

@@ -38,7 +38,8 @@ def lib():
         L = C.CDLL(LIB_PATH)
         L.mp_ctx_launches.restype = C.c_int64
         L.mp_ctx_stream.restype = C.c_void_p
-        for name in ("mp_validate", "mp_detect", "mp_extract", "mp_trace_upload", "mp_profile_download",
+        for name in ("mp_validate", "mp_detect", "mp_extract", "mp_trace_upload", "mp_trace_upload_async",
+                     "mp_trace_wait", "mp_profile_download",
                      "mp_profile_upload", "mp_conflict_from_profile", "mp_conflict_from_arcs",
                      "mp_graph_download", "mp_plan_pool", "mp_ctx_create"):
             getattr(L, name).restype = C.c_int
@@ -113,14 +114,17 @@ class DGraph(_Handle):
 # trace stages
 
 
-def device_trace(arrays) -> DTrace:
-    """Upload (once) and cache the trace on its TraceArrays."""
+def device_trace(arrays, asynchronous: bool = False) -> DTrace:
+    """Upload (once) and cache the trace on its TraceArrays.  With
+    ``asynchronous`` the copies overlap the first stages; the host arrays
+    must stay untouched until ``trace_wait``."""
     cached = getattr(arrays, "_dev", None)
     if cached is not None:
         return cached
     h = C.c_void_p()
     err = MpErr()
-    rc = lib().mp_trace_upload(ctx(), C.byref(trace_in(arrays)), C.byref(h), C.byref(err))
+    fn = lib().mp_trace_upload_async if asynchronous else lib().mp_trace_upload
+    rc = fn(ctx(), C.byref(trace_in(arrays)), C.byref(h), C.byref(err))
     raise_for(rc, err, arrays.names)
     d = DTrace(h)
     try:
@@ -128,6 +132,12 @@ def device_trace(arrays) -> DTrace:
     except AttributeError:
         pass
     return d
+
+
+def trace_wait(d: DTrace) -> None:
+    """Host wait until an asynchronous upload has read its host buffers."""
+    err = MpErr()
+    raise_for(lib().mp_trace_wait(d.h, C.byref(err)), err)
 
 
 def validate(arrays) -> None:

@@ -36,6 +36,10 @@ extern "C" int mp_ctx_destroy(mp_ctx *c) {
   cudaStreamSynchronize(c->stream);
   cudaFreeHost(c->h_small);
   cudaFree(c->d_small);
+  if (c->copy) {
+    cudaStreamSynchronize(c->copy);
+    cudaStreamDestroy(c->copy);
+  }
   cudaStreamDestroy(c->stream);
   delete c;
   return MP_OK;
@@ -76,7 +80,7 @@ extern "C" int mp_trace_reset(mp_dtrace *t) {
   return MP_OK;
 }
 
-extern "C" int mp_trace_upload(mp_ctx *ctx, const mp_trace_in *in, mp_dtrace **out, mp_err *err) {
+static int trace_upload(mp_ctx *ctx, const mp_trace_in *in, mp_dtrace **out, bool async, mp_err *err) {
   cudaStream_t st = ctx->stream;
   mp_dtrace *t = new mp_dtrace();
   t->ctx = ctx;
@@ -88,26 +92,67 @@ extern "C" int mp_trace_upload(mp_ctx *ctx, const mp_trace_in *in, mp_dtrace **o
   CUDA_TRY(t->var.alloc(n, st));
   CUDA_TRY(t->size.alloc(n, st));
   CUDA_TRY(t->t_us.alloc(n, st));
-  if (n) {
-    CUDA_TRY(cudaMemcpyAsync(t->kind.p, in->kind, n, cudaMemcpyHostToDevice, st));
-    CUDA_TRY(cudaMemcpyAsync(t->var.p, in->var, n * 4, cudaMemcpyHostToDevice, st));
-    CUDA_TRY(cudaMemcpyAsync(t->size.p, in->size, n * 8, cudaMemcpyHostToDevice, st));
-    CUDA_TRY(cudaMemcpyAsync(t->t_us.p, in->t_us, n * 8, cudaMemcpyHostToDevice, st));
-  }
-  if (in->index) {
-    CUDA_TRY(t->index.alloc(n, st));
-    CUDA_TRY(cudaMemcpyAsync(t->index.p, in->index, n * 8, cudaMemcpyHostToDevice, st));
-  }
+  if (in->index) CUDA_TRY(t->index.alloc(n, st));
   // Names stay on the host: ids are lexicographic ranks, so every device
   // tie-break is an id compare (renamed instances only ever tie on alloc,
   // which is unique), and candidate name ranks arrive with the candidates.
-  // inputs are borrowed for the duration of the call only
-  CUDA_TRY(cudaStreamSynchronize(st));
+  if (!async) {
+    if (n) {
+      CUDA_TRY(cudaMemcpyAsync(t->kind.p, in->kind, n, cudaMemcpyHostToDevice, st));
+      CUDA_TRY(cudaMemcpyAsync(t->var.p, in->var, n * 4, cudaMemcpyHostToDevice, st));
+      CUDA_TRY(cudaMemcpyAsync(t->size.p, in->size, n * 8, cudaMemcpyHostToDevice, st));
+      CUDA_TRY(cudaMemcpyAsync(t->t_us.p, in->t_us, n * 8, cudaMemcpyHostToDevice, st));
+      if (in->index) CUDA_TRY(cudaMemcpyAsync(t->index.p, in->index, n * 8, cudaMemcpyHostToDevice, st));
+    }
+    // inputs are borrowed for the duration of the call only
+    CUDA_TRY(cudaStreamSynchronize(st));
+    *out = t;
+    return MP_OK;
+  }
+  // The columns go up on the copy stream in the order the stages need them
+  // (var: grouping; kind, size: period detection; then the rest), each
+  // followed by an event the consuming stage waits on (trace_need), so the
+  // first stages run while the later columns are still in flight.
+  if (!ctx->copy) CUDA_TRY(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking));
+  cudaEvent_t start;
+  CUDA_TRY(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventRecord(start, st));  // after the allocations and earlier work
+  CUDA_TRY(cudaStreamWaitEvent(ctx->copy, start, 0));
+  CUDA_TRY(cudaEventDestroy(start));
+  struct Col { int bit; void *dst; const void *src; size_t bytes; };
+  const Col cols[5] = {{0, t->var.p, in->var, (size_t)n * 4}, {1, t->kind.p, in->kind, (size_t)n},
+                       {2, t->size.p, in->size, (size_t)n * 8}, {3, t->index.p, in->index, (size_t)n * 8},
+                       {4, t->t_us.p, in->t_us, (size_t)n * 8}};
+  for (const Col &c : cols) {
+    CUDA_TRY(cudaEventCreateWithFlags(&t->col_ev[c.bit], cudaEventDisableTiming));
+    if (n && c.src) CUDA_TRY(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyHostToDevice, ctx->copy));
+    CUDA_TRY(cudaEventRecord(t->col_ev[c.bit], ctx->copy));
+  }
+  t->pending = TC_ALL;
   *out = t;
   return MP_OK;
 }
 
+extern "C" int mp_trace_upload(mp_ctx *ctx, const mp_trace_in *in, mp_dtrace **out, mp_err *err) {
+  return trace_upload(ctx, in, out, false, err);
+}
+
+extern "C" int mp_trace_upload_async(mp_ctx *ctx, const mp_trace_in *in, mp_dtrace **out, mp_err *err) {
+  return trace_upload(ctx, in, out, true, err);
+}
+
+extern "C" int mp_trace_wait(mp_dtrace *t, mp_err *err) {
+  if (t->col_ev[4]) CUDA_TRY(cudaEventSynchronize(t->col_ev[4]));
+  return MP_OK;
+}
+
 extern "C" int mp_trace_free(mp_dtrace *t) {
+  if (t->col_ev[4]) {
+    // buffers are released stream-ordered on the context stream: after the copies
+    cudaStreamWaitEvent(t->ctx->stream, t->col_ev[4], 0);
+    for (cudaEvent_t &e : t->col_ev)
+      if (e) cudaEventDestroy(e);
+  }
   delete t;
   return MP_OK;
 }

@@ -27,6 +27,7 @@ struct mp_ctx {
   int device = 0;
   int num_sms = 148;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy = nullptr;  // asynchronous trace uploads (created on first use)
   long long launches = 0;
   // pinned host staging for small scalar readbacks
   int64_t *h_small = nullptr;

@@ -21,7 +21,23 @@ struct mp_dtrace {
   bool grouped = false;
   DBuf<uint32_t> perm;
   DBuf<int64_t> gstart;
+  // asynchronous upload (mp_trace_upload_async): one event per column on
+  // the copy stream; `pending` = columns the context stream has not yet
+  // waited for
+  cudaEvent_t col_ev[5] = {};
+  unsigned pending = 0;
 };
+
+enum { TC_VAR = 1, TC_KIND = 2, TC_SIZE = 4, TC_INDEX = 8, TC_TUS = 16, TC_ALL = 31 };
+
+// order the context stream after the upload of the columns in `mask`
+inline int trace_need(mp_ctx *ctx, mp_dtrace *t, unsigned mask, mp_err *err) {
+  unsigned m = mask & t->pending;
+  for (int b = 0; b < 5; b++)
+    if (m & (1u << b)) CUDA_TRY(cudaStreamWaitEvent(ctx->stream, t->col_ev[b], 0));
+  t->pending &= ~m;
+  return MP_OK;
+}
 
 struct mp_dprofile {
   mp_ctx *ctx = nullptr;

@@ -42,6 +42,8 @@ __global__ void k_group_bounds(const uint32_t *skeys, int64_t n, int32_t nvars, 
 
 int build_groups(mp_ctx *ctx, mp_dtrace *t, mp_err *err) {
   if (t->grouped) return MP_OK;
+  int rc0 = trace_need(ctx, t, TC_VAR, err);
+  if (rc0) return rc0;
   StageTimer tm(ctx, MP_ST_GROUP_SORT);
   int64_t n = t->n;
   DBuf<uint32_t> keys;
@@ -78,6 +80,8 @@ __global__ void k_validate_var(const uint8_t *kind, const uint32_t *perm, const 
 extern "C" int mp_validate(mp_ctx *ctx, mp_dtrace *t, mp_err *err) {
   if (t->n == 0) return MP_OK;
   int rc = build_groups(ctx, t, err);
+  if (rc) return rc;
+  rc = trace_need(ctx, t, TC_ALL, err);
   if (rc) return rc;
   StageTimer tm(ctx, MP_ST_VALIDATE);
   unsigned long long *d_first = (unsigned long long *)ctx->d_small;
@@ -259,6 +263,12 @@ extern "C" int mp_detect(mp_ctx *ctx, mp_dtrace *t, int64_t *period, mp_err *err
     mp_set_err(err, MP_E_PERIOD_NOT_FOUND, n, 0, 0, "no period");
     return MP_E_PERIOD_NOT_FOUND;
   }
+  // group the events first: it needs only the var column, which an
+  // asynchronous upload delivers before kind and size
+  int rc0 = build_groups(ctx, t, err);
+  if (rc0) return rc0;
+  rc0 = trace_need(ctx, t, TC_KIND | TC_SIZE, err);
+  if (rc0) return rc0;
   StageTimer tm(ctx, MP_ST_DETECT);
   int64_t ntiles = (n + DT_TILE - 1) / DT_TILE;
   DBuf<HPair> agg;
@@ -438,6 +448,8 @@ extern "C" int mp_extract(mp_ctx *ctx, mp_dtrace *t, int64_t start, int64_t end,
     return MP_E_VALUE;
   }
   int rc = build_groups(ctx, t, err);
+  if (rc) return rc;
+  rc = trace_need(ctx, t, TC_ALL, err);
   if (rc) return rc;
   cudaStream_t st = ctx->stream;
   int64_t p = end - start;

@@ -13,6 +13,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as N
+from .errors import MemplanError
 from .trace import TraceArrays
 
 # traces up to this many events are planned by one CTA (csrc/sweep.cu) — a
@@ -60,22 +61,37 @@ def plan_arrays(arrays: TraceArrays, window: tuple[int, int] | None = None,
         if not small:
             raise ValueError("the one-CTA path plans the detected window of an indexed, host-side plan")
         return _plan_cta(arrays, policy, validate, offsets_out)
-    dev = N.device_trace(arrays)
-    N.lib().mp_trace_reset(dev.h)
-    if validate:
-        N.validate(arrays)
-    if window is None:
-        p = N.detect(arrays)
-        window = (len(arrays) - p, len(arrays))
-    dp = N.extract(arrays, window[0], window[1])
-    dims = dp.dims()
-    g = N.conflict_from_profile(dp)
-    nv, nnz = N.graph_dims(g)
-    if keep_on_device:
-        fp, lv = N.plan_pool_device(g, POLICY_CODE[policy])
-        offs = None
-    else:
-        offs, fp, lv = N.plan_pool(g, POLICY_CODE[policy], nv, out=offsets_out)
+    # The upload is asynchronous, column by column (var, kind, size, then
+    # the rest): grouping and period detection run while the later columns
+    # are still in flight.  Validation still decides first: a detection
+    # failure on an invalid trace reports the invariant violation, as the
+    # reference (validate -> detect -> extract) would.
+    fresh = getattr(arrays, "_dev", None) is None
+    dev = N.device_trace(arrays, asynchronous=True)
+    try:
+        N.lib().mp_trace_reset(dev.h)
+        if window is None:
+            try:
+                p = N.detect(arrays)
+            except (MemplanError, ValueError):
+                if validate:
+                    N.validate(arrays)
+                raise
+            window = (len(arrays) - p, len(arrays))
+        if validate:
+            N.validate(arrays)
+        dp = N.extract(arrays, window[0], window[1])
+        dims = dp.dims()
+        g = N.conflict_from_profile(dp)
+        nv, nnz = N.graph_dims(g)
+        if keep_on_device:
+            fp, lv = N.plan_pool_device(g, POLICY_CODE[policy])
+            offs = None
+        else:
+            offs, fp, lv = N.plan_pool(g, POLICY_CODE[policy], nv, out=offsets_out)
+    finally:
+        if fresh:
+            N.trace_wait(dev)  # the host arrays are the caller's again
     return ArrayPlan(period=int(dims.period), window=tuple(window), nvars=int(dims.nvars),
                      peak_bytes=int(dims.peak_bytes), peak_index=int(dims.peak_index),
                      footprint_bytes=fp, offsets=offs, levels=lv, nnz=nnz)
