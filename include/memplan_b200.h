@@ -174,6 +174,13 @@ int mp_trace_free(mp_dtrace *t);
 /* drop cached derived state (event grouping) so the next stage recomputes it */
 int mp_trace_reset(mp_dtrace *t);
 int mp_validate(mp_ctx *ctx, mp_dtrace *t, mp_err *err);
+/* mp_validate in two passes, for a trace whose timestamps are still
+ * uploading: mp_validate_structure checks everything but the timestamps
+ * (on a violation it runs the full pass, so the error is the one
+ * mp_validate reports), mp_validate_times only the timestamps.  Both passing
+ * == mp_validate passing; the first failing pass names the first violation. */
+int mp_validate_structure(mp_ctx *ctx, mp_dtrace *t, mp_err *err);
+int mp_validate_times(mp_ctx *ctx, mp_dtrace *t, mp_err *err);
 
 /* detect_iteration (iteration.py:93-105): smallest p with the last 2p
  * (kind, size) fingerprints equal pairwise; window = (n - p, n). */

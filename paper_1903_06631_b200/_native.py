@@ -39,7 +39,7 @@ def lib():
         L.mp_ctx_launches.restype = C.c_int64
         L.mp_ctx_stream.restype = C.c_void_p
         for name in ("mp_validate", "mp_detect", "mp_extract", "mp_trace_upload", "mp_trace_upload_async",
-                     "mp_trace_wait", "mp_profile_download",
+                     "mp_trace_wait", "mp_validate_structure", "mp_validate_times", "mp_profile_download",
                      "mp_profile_upload", "mp_conflict_from_profile", "mp_conflict_from_arcs",
                      "mp_graph_download", "mp_plan_pool", "mp_ctx_create"):
             getattr(L, name).restype = C.c_int
@@ -140,10 +140,15 @@ def trace_wait(d: DTrace) -> None:
     raise_for(lib().mp_trace_wait(d.h, C.byref(err)), err)
 
 
-def validate(arrays) -> None:
+def validate(arrays, checks: str = "all") -> None:
+    """validate_trace on the device: ``checks`` "all", or the two halves of
+    an overlapped upload, "structure" (everything but timestamps; reports
+    what "all" would on a violation) and "times"."""
     t = device_trace(arrays)
     err = MpErr()
-    rc = lib().mp_validate(ctx(), t.h, C.byref(err))
+    fn = {"all": lib().mp_validate, "structure": lib().mp_validate_structure,
+          "times": lib().mp_validate_times}[checks]
+    rc = fn(ctx(), t.h, C.byref(err))
     raise_for(rc, err, arrays.names)
 
 

@@ -158,11 +158,18 @@ extern "C" int mp_trace_free(mp_dtrace *t) {
 }
 
 extern "C" int mp_profile_get_dims(mp_dprofile *p, mp_profile_dims *dims) {
+  mp_err e{};
+  int rc = profile_times(p->ctx, p, &e);
+  if (rc) return rc;
   *dims = p->d;
   return MP_OK;
 }
 
 extern "C" int mp_profile_download(mp_ctx *ctx, mp_dprofile *P, mp_profile_out *o, mp_err *err) {
+  {
+    int rc = profile_times(ctx, P, err);
+    if (rc) return rc;
+  }
   cudaStream_t st = ctx->stream;
   int64_t V = P->d.nvars, A = P->d.naccess, p = P->d.period;
 #define DL(dst, src, bytes) \
@@ -187,6 +194,11 @@ extern "C" int mp_profile_download(mp_ctx *ctx, mp_dprofile *P, mp_profile_out *
 }
 
 extern "C" int mp_profile_free(mp_dprofile *p) {
+  if (p->times_ev) {
+    // buffers are released stream-ordered on the context stream: after the op times
+    cudaStreamWaitEvent(p->ctx->stream, p->times_ev, 0);
+    cudaEventDestroy(p->times_ev);
+  }
   delete p;
   return MP_OK;
 }

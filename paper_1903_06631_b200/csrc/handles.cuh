@@ -50,7 +50,23 @@ struct mp_dprofile {
   DBuf<uint8_t> blob;
   DBuf<int64_t> name_off;
   int32_t nnames = 0;
+  // op times computed behind an asynchronous trace upload (mp_extract on a
+  // trace whose t_us column is still in flight): ready at times_ev
+  cudaEvent_t times_ev = nullptr;
+  bool times_pending = false;
+  DBuf<double> dur;
 };
+
+// wait for deferred op times (device order on the context stream, and the
+// period duration on the host)
+inline int profile_times(mp_ctx *ctx, mp_dprofile *P, mp_err *err) {
+  if (!P->times_pending) return MP_OK;
+  CUDA_TRY(cudaStreamWaitEvent(ctx->stream, P->times_ev, 0));
+  CUDA_TRY(cudaEventSynchronize(P->times_ev));
+  CUDA_TRY(cudaMemcpy(&P->d.duration_us, P->dur.p, 8, cudaMemcpyDeviceToHost));
+  P->times_pending = false;
+  return MP_OK;
+}
 
 struct mp_dgraph {
   mp_ctx *ctx = nullptr;

@@ -62,9 +62,9 @@ int build_groups(mp_ctx *ctx, mp_dtrace *t, mp_err *err) {
 // validate_trace
 
 __global__ void k_validate_elem(const uint8_t *kind, const int64_t *size, const int64_t *t_us,
-                                const int64_t *index, int64_t n, unsigned long long *first) {
+                                const int64_t *index, int64_t n, int checks, unsigned long long *first) {
   for (int64_t pos = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; pos < n; pos += (int64_t)gridDim.x * blockDim.x) {
-    int code = validate_elem_code(kind, size, t_us, index, pos);
+    int code = validate_elem_code(kind, size, t_us, index, pos, checks);
     if (code) atomicMin(first, ((unsigned long long)pos << 4) | (unsigned)code);
   }
 }
@@ -77,19 +77,26 @@ __global__ void k_validate_var(const uint8_t *kind, const uint32_t *perm, const 
   }
 }
 
-extern "C" int mp_validate(mp_ctx *ctx, mp_dtrace *t, mp_err *err) {
+// validate_trace (trace.py:55-84) restricted to `checks`: VC_STRUCT (index,
+// kind/size, live-set walk: no timestamps), VC_TIMES (timestamps only) or
+// VC_ALL.  Reports the first violation among the checks run.
+static int validate_checks(mp_ctx *ctx, mp_dtrace *t, int checks, mp_err *err) {
   if (t->n == 0) return MP_OK;
-  int rc = build_groups(ctx, t, err);
-  if (rc) return rc;
-  rc = trace_need(ctx, t, TC_ALL, err);
+  int rc = MP_OK;
+  if (checks & VC_STRUCT) {
+    rc = build_groups(ctx, t, err);
+    if (rc) return rc;
+  }
+  rc = trace_need(ctx, t, checks == VC_ALL ? TC_ALL : checks == VC_TIMES ? TC_TUS : TC_ALL & ~TC_TUS, err);
   if (rc) return rc;
   StageTimer tm(ctx, MP_ST_VALIDATE);
   unsigned long long *d_first = (unsigned long long *)ctx->d_small;
   CUDA_TRY(cudaMemsetAsync(d_first, 0xff, 8, ctx->stream));
   LAUNCH(ctx, k_validate_elem, grid_for(t->n, 256, 4096), 256, 0, t->kind.p, t->size.p, t->t_us.p,
-         t->index.p, t->n, d_first);
-  LAUNCH(ctx, k_validate_var, grid_for(t->nvars, 256), 256, 0, t->kind.p, t->perm.p, t->gstart.p,
-         t->nvars, d_first);
+         t->index.p, t->n, checks, d_first);
+  if (checks & VC_STRUCT)
+    LAUNCH(ctx, k_validate_var, grid_for(t->nvars, 256), 256, 0, t->kind.p, t->perm.p, t->gstart.p,
+           t->nvars, d_first);
   int64_t first;
   rc = dev_read_i64(ctx, (const int64_t *)d_first, &first, err);
   if (rc) return rc;
@@ -111,6 +118,20 @@ extern "C" int mp_validate(mp_ctx *ctx, mp_dtrace *t, mp_err *err) {
   if (rc) return rc;
   mp_set_err(err, MP_E_INVARIANT, pos, code, aux1, "invariant violation");
   return MP_E_INVARIANT;
+}
+
+extern "C" int mp_validate(mp_ctx *ctx, mp_dtrace *t, mp_err *err) { return validate_checks(ctx, t, VC_ALL, err); }
+
+extern "C" int mp_validate_structure(mp_ctx *ctx, mp_dtrace *t, mp_err *err) {
+  int rc = validate_checks(ctx, t, VC_STRUCT, err);
+  // a structural violation may still be preceded by a timestamp one: the
+  // full pass decides which comes first
+  if (rc == MP_E_INVARIANT) rc = validate_checks(ctx, t, VC_ALL, err);
+  return rc;
+}
+
+extern "C" int mp_validate_times(mp_ctx *ctx, mp_dtrace *t, mp_err *err) {
+  return validate_checks(ctx, t, VC_TIMES, err);
 }
 
 // ---------------------------------------------------------------------------
@@ -449,7 +470,10 @@ extern "C" int mp_extract(mp_ctx *ctx, mp_dtrace *t, int64_t start, int64_t end,
   }
   int rc = build_groups(ctx, t, err);
   if (rc) return rc;
-  rc = trace_need(ctx, t, TC_ALL, err);
+  // lifetimes need kind/var/size only; with the timestamps still uploading,
+  // the op times are computed on the copy stream behind them (times_ev)
+  const bool late_times = (t->pending & TC_TUS) && ctx->copy;
+  rc = trace_need(ctx, t, late_times ? TC_ALL & ~TC_TUS : TC_ALL, err);
   if (rc) return rc;
   cudaStream_t st = ctx->stream;
   int64_t p = end - start;
@@ -531,7 +555,22 @@ extern "C" int mp_extract(mp_ctx *ctx, mp_dtrace *t, int64_t start, int64_t end,
   LAUNCH(ctx, k_ex_access, grid_for(nv, 128), 128, 0, t->kind.p, t->perm.p, t->gstart.p, nv, start, end,
          ncarry, s, carry_ord.p, win_ord.p, o);
   double *d_dur = (double *)(ctx->d_small + 3);
-  LAUNCH(ctx, k_ex_times, grid_for(p, 256), 256, 0, t->t_us.p, start, end, P->op_times.p, d_dur);
+  if (late_times) {
+    CUDA_TRY(P->dur.alloc(1, st));
+    cudaEvent_t ready;
+    CUDA_TRY(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(ready, st));  // op_times / dur allocated
+    CUDA_TRY(cudaStreamWaitEvent(ctx->copy, ready, 0));
+    CUDA_TRY(cudaEventDestroy(ready));
+    ctx->launches++;
+    k_ex_times<<<grid_for(p, 256), 256, 0, ctx->copy>>>(t->t_us.p, start, end, P->op_times.p, P->dur.p);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaEventCreateWithFlags(&P->times_ev, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(P->times_ev, ctx->copy));
+    P->times_pending = true;
+  } else {
+    LAUNCH(ctx, k_ex_times, grid_for(p, 256), 256, 0, t->t_us.p, start, end, P->op_times.p, d_dur);
+  }
   delete tm;
   rc = profile_loads_async(ctx, P, err);
   if (rc) { delete P; return rc; }
@@ -542,7 +581,7 @@ extern "C" int mp_extract(mp_ctx *ctx, mp_dtrace *t, int64_t start, int64_t end,
   P->d.peak_bytes = p ? fin[0] : 0;
   P->d.peak_index = p ? fin[1] : 0;
   P->d.naccess = fin[2];
-  memcpy(&P->d.duration_us, &fin[3], 8);
+  if (!late_times) memcpy(&P->d.duration_us, &fin[3], 8);
   P->nnames = t->nvars;
   *out = P;
   return MP_OK;
@@ -556,6 +595,8 @@ extern "C" int mp_extract_times(mp_ctx *ctx, mp_dtrace *t, int64_t start, int64_
   int rc = mp_extract(ctx, t, start, end, out, err);
   if (rc) return rc;
   mp_dprofile *P = *out;
+  rc = profile_times(ctx, P, err);  // the caller's times replace the computed ones
+  if (rc) return rc;
   CUDA_TRY(cudaMemcpyAsync(P->op_times.p, op_times, (end - start) * 8, cudaMemcpyHostToDevice, ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   P->d.duration_us = duration;

@@ -52,11 +52,18 @@ struct ProfOut {
 // validate_trace, trace.py:55-84
 
 // element checks of position pos (trace.py:63-79); 0 = none
+// checks: VC_STRUCT = index + kind/size, VC_TIMES = timestamps.  The codes
+// are numbered in the reference's check order, so the minimum of
+// (pos << 4 | code) over separate passes is the first violation of one pass.
+enum { VC_STRUCT = 1, VC_TIMES = 2, VC_ALL = 3 };
 __device__ __forceinline__ int validate_elem_code(const uint8_t *kind, const int64_t *size, const int64_t *t_us,
-                                                  const int64_t *index, int64_t pos) {
-  if (index && index[pos] != pos) return MP_V_INDEX;
-  if (t_us[pos] < 0) return MP_V_NEG_T;
-  if (pos > 0 && t_us[pos] < t_us[pos - 1]) return MP_V_T_DEC;
+                                                  const int64_t *index, int64_t pos, int checks = VC_ALL) {
+  if ((checks & VC_STRUCT) && index && index[pos] != pos) return MP_V_INDEX;
+  if (checks & VC_TIMES) {
+    if (t_us[pos] < 0) return MP_V_NEG_T;
+    if (pos > 0 && t_us[pos] < t_us[pos - 1]) return MP_V_T_DEC;
+  }
+  if (!(checks & VC_STRUCT)) return 0;
   if (kind[pos] == MP_MALLOC) return size[pos] <= 0 ? MP_V_MALLOC_SIZE : 0;
   return size[pos] != 0 ? MP_V_SIZE_NONZERO : 0;
 }

@@ -73,6 +73,10 @@ __global__ void k_compact(int64_t V, const int32_t *flag, const int32_t *pos, co
 
 extern "C" int mp_swap_candidates(mp_ctx *ctx, mp_dprofile *P, int64_t threshold, double bw, double lat,
                                   mp_cands_io *out, mp_err *err) {
+  {
+    int rc_t = profile_times(ctx, P, err);
+    if (rc_t) return rc_t;
+  }
   StageTimer tm(ctx, MP_ST_SWAP);
   cudaStream_t st = ctx->stream;
   int64_t V = P->d.nvars;
@@ -146,6 +150,10 @@ static LoadView load_view(mp_dprofile *P) { return LoadView{P->d.period, P->load
 
 extern "C" int mp_swap_scores(mp_ctx *ctx, mp_dprofile *P, const mp_cands_io *c, double *doa, double *aoa,
                               double *wdoa, double *swdoa, int32_t *order, double *peaks, mp_err *err) {
+  {
+    int rc_t = profile_times(ctx, P, err);
+    if (rc_t) return rc_t;
+  }
   StageTimer tm(ctx, MP_ST_SWAP);
   cudaStream_t st = ctx->stream;
   CandDev d;
@@ -178,6 +186,10 @@ extern "C" int mp_swap_scores(mp_ctx *ctx, mp_dprofile *P, const mp_cands_io *c,
 
 extern "C" int mp_swap_gap_area(mp_ctx *ctx, mp_dprofile *P, const mp_cands_io *c, const double *loads,
                                 double *area, mp_err *err) {
+  {
+    int rc_t = profile_times(ctx, P, err);
+    if (rc_t) return rc_t;
+  }
   StageTimer tm(ctx, MP_ST_SWAP);
   cudaStream_t st = ctx->stream;
   CandDev d;
@@ -306,6 +318,10 @@ __global__ void k_planned_peak(LoadView L, CandView c, const int32_t *subset, in
 
 extern "C" int mp_swap_planned_peak(mp_ctx *ctx, mp_dprofile *P, const mp_cands_io *c, const int32_t *subset,
                                     int64_t nsub, double *peak, mp_err *err) {
+  {
+    int rc_t = profile_times(ctx, P, err);
+    if (rc_t) return rc_t;
+  }
   StageTimer tm(ctx, MP_ST_SWAP);
   cudaStream_t st = ctx->stream;
   CandDev d;
@@ -453,6 +469,10 @@ __global__ void k_sim_delays(ProfView P, const double *actual, double delay_tota
 
 extern "C" int mp_swap_simulate(mp_ctx *ctx, mp_dprofile *P, const mp_cands_io *c, const int32_t *sel, int64_t n,
                                 int64_t limit, int32_t has_limit, int32_t max_rounds, mp_sim_io *io, mp_err *err) {
+  {
+    int rc_t = profile_times(ctx, P, err);
+    if (rc_t) return rc_t;
+  }
   StageTimer tm(ctx, MP_ST_SWAP);
   cudaStream_t st = ctx->stream;
   CandDev d;
@@ -705,6 +725,10 @@ __global__ void __launch_bounds__(128) k_swap_eval_weights(EvalArgs a) {
 extern "C" int mp_swap_eval_weights(mp_ctx *ctx, mp_dprofile *P, const mp_cands_io *c, const double *z,
                                     const double *weights, int64_t m, int64_t limit, int32_t max_rounds,
                                     int32_t *status, double *overhead, int64_t *nsel, int64_t *aux, mp_err *err) {
+  {
+    int rc_t = profile_times(ctx, P, err);
+    if (rc_t) return rc_t;
+  }
   StageTimer tm(ctx, MP_ST_SWAP);
   cudaStream_t st = ctx->stream;
   if (m <= 0) return MP_OK;

@@ -66,6 +66,9 @@ def plan_arrays(arrays: TraceArrays, window: tuple[int, int] | None = None,
     # are still in flight.  Validation still decides first: a detection
     # failure on an invalid trace reports the invariant violation, as the
     # reference (validate -> detect -> extract) would.
+    # The timestamps (needed only for op times and their own checks) arrive
+    # last: structure is validated before extraction, timestamps after the
+    # plan, and any failure in between defers to the timestamp check first.
     fresh = getattr(arrays, "_dev", None) is None
     dev = N.device_trace(arrays, asynchronous=True)
     try:
@@ -79,16 +82,23 @@ def plan_arrays(arrays: TraceArrays, window: tuple[int, int] | None = None,
                 raise
             window = (len(arrays) - p, len(arrays))
         if validate:
-            N.validate(arrays)
-        dp = N.extract(arrays, window[0], window[1])
+            N.validate(arrays, "structure")
+        try:
+            dp = N.extract(arrays, window[0], window[1])
+            g = N.conflict_from_profile(dp)
+            nv, nnz = N.graph_dims(g)
+            if keep_on_device:
+                fp, lv = N.plan_pool_device(g, POLICY_CODE[policy])
+                offs = None
+            else:
+                offs, fp, lv = N.plan_pool(g, POLICY_CODE[policy], nv, out=offsets_out)
+        except (MemplanError, ValueError):
+            if validate:
+                N.validate(arrays, "times")
+            raise
+        if validate:
+            N.validate(arrays, "times")
         dims = dp.dims()
-        g = N.conflict_from_profile(dp)
-        nv, nnz = N.graph_dims(g)
-        if keep_on_device:
-            fp, lv = N.plan_pool_device(g, POLICY_CODE[policy])
-            offs = None
-        else:
-            offs, fp, lv = N.plan_pool(g, POLICY_CODE[policy], nv, out=offsets_out)
     finally:
         if fresh:
             N.trace_wait(dev)  # the host arrays are the caller's again
