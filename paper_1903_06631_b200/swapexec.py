@@ -117,6 +117,72 @@ def plan_actions(profile, selection, limit_bytes: int, points, slot_of) -> tuple
     return acts, skipped
 
 
+def select_window_fits(profile, cands, limit_bytes: int, points, slot_of, d2h_bytes_per_s: float,
+                       h2d_bytes_per_s: float, latency_us: float = 10.0, margin: float = 0.9,
+                       stall_budget_us: float = 0.0, order=None):
+    """An executor-aware selection (not the reference's): candidates largest
+    first, each kept only if, with the absences chosen so far, its copies fit
+    the windows ``plan_actions`` would give it — the D2H (queued behind
+    earlier ones on its stream) done before the first op that needs its
+    bytes, the H2D done before its in access — at ``margin`` x the measured
+    link rates on the traced op times.  Stops once the load is within the
+    limit; returns the selection or raises LimitUnreachable.  With
+    ``stall_budget_us`` a candidate may also stall the compute stream (copy
+    done after the op that waits for it) while the predicted stalls sum to
+    at most that budget.
+    """
+    from .errors import LimitUnreachable
+    t = np.asarray(profile.op_times_us, np.float64)
+    loads = np.asarray(profile.load.loads, np.int64).copy()
+    busy_out, busy_in = [], []  # (start, end) of accepted copies per stream
+    chosen = []
+    stall = 0.0
+
+    def queue_end(busy, start, dur):
+        # first start >= start that does not overlap an accepted copy
+        for s0, e0 in sorted(busy):
+            if start + dur <= s0:
+                break
+            if e0 > start:
+                start = e0
+        return start + dur
+
+    for c in sorted(cands, key=order or (lambda c: (-c.size, c.var))):
+        if loads.max() <= limit_bytes:
+            break
+        if c.spans_iterations or c.var not in slot_of:
+            continue
+        r1, r2 = int(c.out_index), int(c.in_index)
+        over = np.nonzero(loads[r1 + 1:r2] > limit_bytes)[0]
+        if over.size == 0:
+            continue
+        a = r1 + 1 + int(over[0])
+        b = r1 + 1 + int(over[-1]) + 1
+        while a < b and next_point(points[r1]) > points[a]:
+            a += 1
+        while b > a and next_point(points[b - 1]) > points[r2]:
+            b -= 1
+        if b <= a:
+            continue
+        d_out = c.size / (d2h_bytes_per_s * margin) * 1e6 + latency_us
+        d_in = c.size / (h2d_bytes_per_s * margin) * 1e6 + latency_us
+        out_start = t[r1 + 1]
+        out_end = queue_end(busy_out, out_start, d_out)
+        in_start = t[b] if b < len(t) else t[-1]
+        in_end = queue_end(busy_in, in_start, d_in)
+        st = max(0.0, out_end - t[a]) + max(0.0, in_end - t[r2])
+        if st > 0 and stall + st > stall_budget_us:
+            continue
+        stall += st
+        busy_out.append((out_end - d_out, out_end))
+        busy_in.append((in_end - d_in, in_end))
+        loads[a:b] -= c.size
+        chosen.append(c)
+    if loads.max() > limit_bytes:
+        raise LimitUnreachable(limit_bytes, int(loads.max()))
+    return chosen
+
+
 SWAP_LEAD = 512  # swapped blocks start this far into their arc (see split_arcs)
 
 

@@ -89,3 +89,55 @@ def test_split_arcs_and_served_offsets():
 def test_window_slots_follow_allocation_order():
     prof = profile([0] * 10, [var("b", 8, 5, 9), var("a", 8, 2, 9), var("~iteration", 1, 7, 8)])
     assert swapexec.window_slots(prof) == {"a": 0, "b": 1}
+
+
+# ---- select_window_fits: copies must fit the executor's windows ----
+
+def _wf_profile(loads, times):
+    return SimpleNamespace(load=SimpleNamespace(loads=list(loads)), op_times_us=list(times), period=len(loads))
+
+
+def test_window_fits_keeps_a_candidate_whose_copies_fit():
+    from paper_1903_06631_b200.errors import LimitUnreachable
+    loads = [10] * 20
+    for r in range(8, 13):
+        loads[r] = 30
+    times = [100.0 * r for r in range(20)]          # 100 us per op
+    points = np.arange(20) * 2
+    c = cand("x", 1000, 1, 18)                       # 1000 B at 1e8 B/s = 10 us each way
+    sel = swapexec.select_window_fits(_wf_profile(loads, times), [c], 20, points, {"x": 0}, 1e8, 1e8,
+                                      latency_us=0.0, margin=1.0)
+    assert [s.var for s in sel] == ["x"]
+    # a link too slow for the window: D2H (from t[2]=200) must end by t[8]=800
+    try:
+        swapexec.select_window_fits(_wf_profile(loads, times), [c], 20, points, {"x": 0}, 1e6, 1e8,
+                                    latency_us=0.0, margin=1.0)
+        raise AssertionError("expected LimitUnreachable")
+    except LimitUnreachable:
+        pass
+    # ... unless the stall budget covers the predicted wait (1000 us - 600 us)
+    sel = swapexec.select_window_fits(_wf_profile(loads, times), [c], 20, points, {"x": 0}, 1e6, 1e8,
+                                      latency_us=0.0, margin=1.0, stall_budget_us=400.0)
+    assert [s.var for s in sel] == ["x"]
+
+
+def test_window_fits_serializes_copies_on_one_stream():
+    from paper_1903_06631_b200.errors import LimitUnreachable
+    loads = [1000] * 20
+    for r in range(8, 13):
+        loads[r] = 2000
+    times = [100.0 * r for r in range(20)]
+    points = np.arange(20) * 2
+    # each needs 500 us of D2H after t[2] = 200: on one stream the second
+    # would end at 1200 > t[8] = 800
+    cs = [cand("x", 500, 1, 18), cand("y", 500, 1, 18)]
+    try:
+        swapexec.select_window_fits(_wf_profile(loads, times), cs, 1000, points, {"x": 0, "y": 1}, 1e6, 1e8,
+                                    latency_us=0.0, margin=1.0)
+        raise AssertionError("expected LimitUnreachable")
+    except LimitUnreachable:
+        pass
+    # one of them suffices for a looser limit
+    sel = swapexec.select_window_fits(_wf_profile(loads, times), cs, 1500, points, {"x": 0, "y": 1}, 1e6, 1e8,
+                                      latency_us=0.0, margin=1.0)
+    assert len(sel) == 1

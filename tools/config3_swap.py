@@ -11,10 +11,14 @@ CUDA allocation):
 2. Detects the iteration and extracts lifetimes + access gaps on the device.
 3. Measures the host link (pinned D2H / H2D) and uses it as the transfer
    model.
-4. For each memory limit (fraction of the traced peak load): SWDOA
-   selection among the executable candidates, schedule, simulation (predicted
-   overhead), mapping onto op-granular hook points, pool plan on the split
-   lifetimes, and a served + swapped run of ``--steps`` iterations.
+4. For each memory limit (fraction of the traced peak load) and selection
+   mode — the reference's SWDOA selection among the executable candidates;
+   the same restricted to candidates whose round trip fits their gap; and
+   ``swapexec.select_window_fits`` (ours: copies must fit the executor's
+   windows at the measured link rates, optionally with a 4 % stall budget) —
+   schedule, simulation (predicted overhead), mapping onto op-granular hook
+   points, pool plan on the split lifetimes, and a served + swapped run of
+   ``--steps`` iterations.
 5. Prints one JSON line: per limit the predicted and measured overhead vs
    the same hooked run without swaps, the pool footprint vs the no-swap pool,
    the bytes moved, and whether the losses equal the unswapped run bit for bit.
@@ -68,7 +72,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--batch", type=int, default=128)
     ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--fracs", default="0.98,0.95,0.92,0.9,0.85,0.8,0.7")
+    ap.add_argument("--fracs", default="0.98,0.95,0.93,0.92,0.9,0.88,0.85,0.8,0.7")
+    ap.add_argument("--modes", default="reference_selection,transfer_fits_gap,window_fits,window_fits_stall4pct")
     ap.add_argument("--threshold-mib", type=float, default=1.0)
     ap.add_argument("--sync-times", action="store_true",
                     help="time ops with a synchronize each (the paper's profiler) instead of device events")
@@ -172,12 +177,20 @@ def main():
     ms_hook2, _l, _x, _p, _s = run([], hooked=True)
     fit_cands = [c for c in exec_cands if c.gap_us >= c.delta_out_us + c.delta_in_us]
     rows = []
-    for mode, pool in (("reference_selection", exec_cands), ("transfer_fits_gap", fit_cands)):
+    pools = {"reference_selection": exec_cands, "transfer_fits_gap": fit_cands, "window_fits": exec_cands,
+             "window_fits_stall4pct": exec_cands}
+    for mode in [m for m in a.modes.split(",") if m]:
+        pool = pools[mode]
         for frac in [float(x) for x in a.fracs.split(",") if x]:
             limit = int(prof.peak_bytes * frac)
             row = {"mode": mode, "frac": frac, "limit_bytes": limit}
             try:
-                sel = autoswap.select_by_score(pool, prof, limit, "swdoa")
+                if mode.startswith("window_fits"):
+                    budget = 0.04 * prof.period_duration_us if mode.endswith("4pct") else 0.0
+                    sel = swapexec.select_window_fits(prof, pool, limit, points, slot_of, bw["d2h"], bw["h2d"],
+                                                      stall_budget_us=budget)
+                else:
+                    sel = autoswap.select_by_score(pool, prof, limit, "swdoa")
             except LimitUnreachable as exc:
                 row["error"] = type(exc).__name__
                 rows.append(row)
@@ -221,7 +234,13 @@ def main():
         "noswap_pool_bytes": plan0.footprint_bytes, "noswap_pool_arc_peak_bytes": plan0.arc_peak_bytes, "iter_ms_served_plain": ms_plain,
         "iter_ms_served_hooked": ms_hook, "iter_ms_served_hooked_repeat": ms_hook2,
         "hooked_losses_equal_plain": losses_hook == losses_plain, "noswap_allocator": st0,
-        "losses": losses_plain[:4], "limits": rows}))
+        "losses": losses_plain[:4], "limits": rows,
+        # enough of the profile to replay the selections offline
+        "replay": {"loads": [int(x) for x in prof.load.loads], "op_times_us": [float(x) for x in prof.op_times_us],
+                   "points": [int(x) for x in points], "slots": sorted(slot_of),
+                   "cands": [{"var": c.var, "size": int(c.size), "out_index": int(c.out_index),
+                              "in_index": int(c.in_index), "spans_iterations": bool(c.spans_iterations),
+                              "gap_us": float(c.gap_us), "delta_out_us": float(c.delta_out_us)} for c in exec_cands]}}))
 
 
 if __name__ == "__main__":
