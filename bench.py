@@ -23,6 +23,12 @@ budgets = 4096 units (csrc/sweep.cu, one CTA per trace) — resident and e2e
 units/s, sharded over ranks by LPT (strong scaling), its own parity check
 and the C oracle on every host core as its cpu_baseline.
 
+The line also carries "swap": BASELINE configs[2], the swap-iteration
+overhead on a VGG-16 b128 training iteration (tools/config3_swap.py in a
+subprocess on rank 0's GPU: traced, planned, executed with copy streams for
+10 iterations at 95 % of the traced peak, the reference's SWDOA selection and
+the executor-aware one; lower is better).
+
 --impl reference: the reference's CPU algorithm (the C oracle port — the
 Python reference cannot run on this box) on all host cores, one trace
 replica per process, same metric.
@@ -420,6 +426,34 @@ def run_reference(args, rank, world):
     return 0
 
 
+def run_swap_leg(local_rank: int, frac: float = 0.95) -> dict:
+    """BASELINE configs[2]: swap-iteration overhead % vs the same served,
+    hooked iteration without swaps (tools/config3_swap.py, own process: the
+    pluggable allocator must own the CUDA context from its first malloc)."""
+    cmd = [sys.executable, os.path.join(ROOT, "tools", "config3_swap.py"), "--fracs", str(frac),
+           "--modes", "reference_selection,window_fits", "--steps", "10"]
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES=os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",")[local_rank]
+               if os.environ.get("CUDA_VISIBLE_DEVICES") else str(local_rank))
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+        d = json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception as exc:  # noqa: BLE001  (the main line must still print)
+        return {"error": f"{type(exc).__name__}: {str(exc)[:200]}"}
+    rows = []
+    for l in d["limits"]:
+        rows.append({"mode": l["mode"], "limit_frac": l["frac"], "error": l.get("error"),
+                     "measured_overhead_pct": l.get("measured_overhead_pct"),
+                     "predicted_overhead_pct": l.get("predicted_overhead_pct"),
+                     "pool_reduction_vs_noswap": l.get("pool_reduction_vs_noswap"),
+                     "bytes_moved_per_iter": l.get("swap_bytes_per_iter"),
+                     "losses_equal_unswapped": l.get("losses_equal_unswapped")})
+    return {"workload": "VGG-16 b128 training iteration (BASELINE configs[2])",
+            "metric": "swap-iter overhead % vs no-swap", "unit": "%", "higher_is_better": False,
+            "data": "synthetic (random-init VGG-16, random batch)", "iter_ms_noswap": d["iter_ms_served_hooked"],
+            "traced_peak_bytes": d["traced_peak_bytes"], "link_bytes_per_s": d["link_bw_bytes_per_s"],
+            "rows": rows}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -429,6 +463,7 @@ def main():
     ap.add_argument("--accesses", action="store_true", help="config-4 variant with write/read per var")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="skip the config-5 batched sweep leg")
+    ap.add_argument("--no-swap", action="store_true", help="skip the config-3 swap-overhead leg")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -493,6 +528,8 @@ def main():
     }
     if r.get("sweep") is not None:
         line["sweep"] = r["sweep"]
+    if not args.no_swap:
+        line["swap"] = run_swap_leg(local_rank)
     if not args.no_cpu_baseline:
         cb = cpu_baseline(arrays)
         line["cpu_baseline"] = {"value": cb["value"], "unit": UNIT, "cores": 1, "kind": "port",
