@@ -76,9 +76,13 @@ __global__ void k_iv_keys(int64_t n, const int32_t *a, uint32_t *keys, uint32_t 
   }
 }
 
-// fwd/bwd counts per interval (indexed by interval id)
+// fwd/bwd counts per interval (indexed by interval id), plus per sorted
+// position the interval's variable, that variable's placement rank and the
+// forward count (the fill reads these contiguously instead of chasing
+// perm -> ivar -> rank)
 __global__ void k_iv_counts(int64_t n, const uint32_t *sstart, const uint32_t *perm, const uint32_t *send,
-                            const int32_t *eb, int64_t *cnt, int32_t *fwd) {
+                            const int32_t *eb, int64_t *cnt, const int32_t *ivar, const int32_t *rank,
+                            int32_t *sv) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
     uint32_t iid = perm[k];
     uint32_t a = sstart[k], b = (uint32_t)eb[iid] ^ 0x80000000u;
@@ -94,8 +98,11 @@ __global__ void k_iv_counts(int64_t n, const uint32_t *sstart, const uint32_t *p
       if (send[mid] <= a) lo = mid + 1; else hi = mid;
     }
     int64_t bw = k - lo;
-    fwd[iid] = (int32_t)f;
     cnt[iid] = f + bw;
+    int32_t v = ivar[iid];
+    sv[3 * k] = v;
+    sv[3 * k + 1] = rank[v];
+    sv[3 * k + 2] = (int32_t)f;
   }
 }
 
@@ -147,13 +154,17 @@ __global__ void k_iv_scatter(int64_t n, const int32_t *ea, int32_t base, const i
 
 // forward run = sorted positions (k, #starts < end); backward = k - #ends <= start
 __global__ void k_iv_counts_dense(int64_t n, const uint32_t *perm, const int32_t *ea, const int32_t *eb, int32_t base,
-                                  const int32_t *offs, const int32_t *cum_e, int64_t *cnt, int32_t *fwd) {
+                                  const int32_t *offs, const int32_t *cum_e, int64_t *cnt, const int32_t *ivar,
+                                  const int32_t *rank, int32_t *sv) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
     uint32_t iid = perm[k];
     int64_t f = (int64_t)offs[eb[iid] - base] - k - 1;
     int64_t bw = k - cum_e[ea[iid] - base + 1];
-    fwd[iid] = (int32_t)f;
     cnt[iid] = f + bw;
+    int32_t v = ivar[iid];
+    sv[3 * k] = v;
+    sv[3 * k + 1] = rank[v];
+    sv[3 * k + 2] = (int32_t)f;
   }
 }
 
@@ -165,23 +176,24 @@ __global__ void k_row_off(int64_t nv, const int64_t *eoff, const int64_t *sub_of
 // warp per sorted interval: the forward run and its mirror, written straight
 // into placement-partitioned rows (predecessors grow from the row start,
 // successors from the row end) so plan_pool needs no separate split pass
-__global__ void k_iv_fill(int64_t n, const uint32_t *perm, const int32_t *ivar, const int32_t *fwd,
-                          const int64_t *row_off, const int32_t *rank, int32_t *pc, int32_t *sc, int32_t *col) {
+__global__ void k_iv_fill(int64_t n, const int32_t *sv, const int64_t *row_off, int32_t *pc, int32_t *sc,
+                          int32_t *col) {
   const int lane = threadIdx.x & 31;
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const unsigned lt = lanemask_lt();
   for (int64_t k = warp; k < n; k += nwarps) {
-    uint32_t iid = perm[k];
-    int32_t u = ivar[iid];
-    int32_t f = fwd[iid];
-    int32_t ru = rank[u];
+    const int32_t u = sv[3 * k], ru = sv[3 * k + 1], f = sv[3 * k + 2];
     int64_t rbu = row_off[u], reu = row_off[u + 1];
     for (int32_t base = 0; base < f; base += 32) {
       int32_t jx = base + lane;
       bool valid = jx < f;
-      int32_t j = valid ? ivar[perm[k + 1 + jx]] : 0;
-      bool isp = valid && rank[j] < ru;  // j precedes u in placement order
+      int32_t j = 0, rj = 0;
+      if (valid) {
+        j = sv[3 * (k + 1 + jx)];
+        rj = sv[3 * (k + 1 + jx) + 1];
+      }
+      bool isp = valid && rj < ru;  // j precedes u in placement order
       unsigned bp = __ballot_sync(FULL_MASK, isp);
       unsigned bs = __ballot_sync(FULL_MASK, valid && !isp);
       int32_t p0 = 0, s0 = 0;
@@ -244,9 +256,9 @@ static int build_csr(mp_ctx *ctx, int64_t nv, const int64_t *seg_off_d, const in
     rc = placement_rank_sort(ctx, nv, g->size.p, g->tiekey.p, g->rank.p, (uint64_t)h[6], (uint64_t)h[7], err);
     if (rc) return rc;
   }
-  DBuf<int32_t> ea, eb, ivar, fwd, scur;
+  DBuf<int32_t> ea, eb, ivar, sv, scur;
   CUDA_TRY(ea.alloc(ni, st)); CUDA_TRY(eb.alloc(ni, st)); CUDA_TRY(ivar.alloc(ni, st));
-  CUDA_TRY(fwd.alloc(ni, st)); CUDA_TRY(scur.alloc(nv, st));
+  CUDA_TRY(sv.alloc(3 * ni, st)); CUDA_TRY(scur.alloc(nv, st));
   LAUNCH(ctx, k_norm_count, grid_for(nv, 128), 128, 0, nv, seg_off_d, lo_d, hi_d, ecnt.p, ea.p, eb.p,
          d_over, 1, eoff.p, ivar.p);
   // order intervals by start.  Interval bounds are op positions, so when
@@ -273,7 +285,7 @@ static int build_csr(mp_ctx *ctx, int64_t nv, const int64_t *seg_off_d, const in
     if (rc) return rc;
     LAUNCH(ctx, k_iv_scatter, grid_for(ni, 256), 256, 0, ni, ea.p, mm[0], offs_s.p, curs.p, perm.p);
     LAUNCH(ctx, k_iv_counts_dense, grid_for(ni, 256), 256, 0, ni, perm.p, ea.p, eb.p, mm[0], offs_s.p, cum_e.p,
-           cnt.p, fwd.p);
+           cnt.p, ivar.p, g->rank.p, sv.p);
   } else {
     DBuf<uint32_t> ekey, edummy;
     CUDA_TRY(ekey.alloc(ni, st)); CUDA_TRY(edummy.alloc(ni, st));
@@ -283,7 +295,8 @@ static int build_csr(mp_ctx *ctx, int64_t nv, const int64_t *seg_off_d, const in
     if (rc) return rc;
     rc = dev_radix_sort_u32(ctx, ekey.p, edummy.p, ni, 32, err);
     if (rc) return rc;
-    LAUNCH(ctx, k_iv_counts, grid_for(ni, 256), 256, 0, ni, skey.p, perm.p, ekey.p, eb.p, cnt.p, fwd.p);
+    LAUNCH(ctx, k_iv_counts, grid_for(ni, 256), 256, 0, ni, skey.p, perm.p, ekey.p, eb.p, cnt.p, ivar.p, g->rank.p,
+           sv.p);
   }
   rc = dev_exclusive_scan<int64_t>(ctx, cnt.p, sub_off.p, ni, d_tot, err);
   if (rc) return rc;
@@ -307,8 +320,8 @@ static int build_csr(mp_ctx *ctx, int64_t nv, const int64_t *seg_off_d, const in
   CUDA_TRY(cudaMemsetAsync(g->pcnt.p, 0, nv * 4, st));
   delete tm;
   StageTimer fill(ctx, MP_ST_CONFLICT_FILL);
-  LAUNCH(ctx, k_iv_fill, grid_for(ni * 32, 256, 148 * 64), 256, 0, ni, perm.p, ivar.p, fwd.p, g->row_off.p,
-         g->rank.p, g->pcnt.p, scur.p, g->col.p);
+  LAUNCH(ctx, k_iv_fill, grid_for(ni * 32, 256, 148 * 64), 256, 0, ni, sv.p, g->row_off.p, g->pcnt.p, scur.p,
+         g->col.p);
   return MP_OK;
 }
 
