@@ -475,10 +475,29 @@ int placement_rank_keys(mp_ctx *ctx, int64_t V, const int64_t *size, unsigned lo
 }
 
 // rank[v] = position in (-size, tiekey or vertex) order, size keys in [kmin, kmax]
+__global__ void k_size_keys32(int64_t V, const int64_t *size, uint64_t kmin, uint32_t *keys, uint32_t *vals) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
+    keys[v] = (uint32_t)(desc_size_key(size[v]) - kmin);
+    vals[v] = (uint32_t)v;
+  }
+}
+
 int placement_rank_sort(mp_ctx *ctx, int64_t V, const int64_t *size, const int64_t *tiekey, int32_t *rank,
                         uint64_t kmin, uint64_t kmax, mp_err *err) {
   StageTimer tm(ctx, MP_ST_PLACE_ORDER);
   cudaStream_t st = ctx->stream;
+  if (!tiekey && kmax - kmin <= 0xffffffffull) {
+    // vertex-order ties and a size range that fits 32 bits: one stable sort
+    // of 32-bit keys (a third less traffic per pass than the 64-bit path)
+    DBuf<uint32_t> k32, order;
+    CUDA_TRY(k32.alloc(V, st));
+    CUDA_TRY(order.alloc(V, st));
+    LAUNCH(ctx, k_size_keys32, grid_for(V, 256), 256, 0, V, size, kmin, k32.p, order.p);
+    int rc = dev_radix_sort_u32(ctx, k32.p, order.p, V, bits_for(kmax - kmin), err);
+    if (rc) return rc;
+    LAUNCH(ctx, k_rank, grid_for(V, 256), 256, 0, V, order.p, rank);
+    return MP_OK;
+  }
   DBuf<uint64_t> keys;
   DBuf<uint32_t> order;
   CUDA_TRY(keys.alloc(V, st));
