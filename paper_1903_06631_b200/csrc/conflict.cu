@@ -25,9 +25,44 @@ __global__ void k_norm_count(int64_t nv, const int64_t *seg_off, const int32_t *
   // counting pass (write == 0): eb doubles as the (min start, max end) cell
   int32_t lmin = INT32_MAX, lmax = INT32_MIN;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s0 = seg_off[v], s1 = seg_off[v + 1];
+    if (s1 - s0 <= 2) {
+      // profile variables (at most two segments): the same rule in registers
+      int32_t l0 = 0, h0 = 0, l1 = 0, h1 = 0;
+      int mm = 0;
+      for (int64_t s = s0; s < s1; s++) {
+        int32_t a = lo[s], b = hi[s];
+        if (b <= a) continue;
+        if (mm == 0) { l0 = a; h0 = b; }
+        else if (a < l0) { l1 = l0; h1 = h0; l0 = a; h0 = b; }
+        else { l1 = a; h1 = b; }
+        mm++;
+      }
+      int64_t out = write ? eoff[v] : 0, c = 0;
+      int32_t cur_end = INT32_MIN;
+      for (int k = 0; k < mm; k++) {
+        const int32_t lk = k ? l1 : l0;
+        if (lk < cur_end) continue;
+        int32_t ne = INT32_MAX;
+        if (h0 > lk && h0 < ne) ne = h0;
+        if (mm > 1 && h1 > lk && h1 < ne) ne = h1;
+        if (write) {
+          ea[out + c] = lk;
+          eb[out + c] = ne;
+          ivar[out + c] = (int32_t)v;
+        } else {
+          lmin = min(lmin, lk);
+          lmax = max(lmax, ne);
+        }
+        c++;
+        cur_end = ne;
+      }
+      if (!write) ecnt[v] = c;
+      continue;
+    }
     int32_t L[MAXSEG], H[MAXSEG];
     int m = 0;
-    for (int64_t s = seg_off[v]; s < seg_off[v + 1]; s++) {
+    for (int64_t s = s0; s < s1; s++) {
       if (hi[s] <= lo[s]) continue;  // empty segments never enter the sweep
       if (m == MAXSEG) { *overflow = 1; break; }
       // insertion sort by lo

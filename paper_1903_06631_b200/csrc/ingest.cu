@@ -29,14 +29,17 @@ __global__ void k_group_init(const int32_t *var, int64_t n, uint32_t *keys, uint
   }
 }
 
+// gstart[v] = lower_bound(v) in the sorted keys: each position where the
+// key changes writes the starts of the ids from the previous key + 1 up to
+// its own (ids without events get an empty run); the last position closes
+// the ids after the largest key.  n >= 1.
 __global__ void k_group_bounds(const uint32_t *skeys, int64_t n, int32_t nvars, int64_t *gstart) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v <= nvars; v += (int64_t)gridDim.x * blockDim.x) {
-    int64_t lo = 0, hi = n;  // lower_bound(v)
-    while (lo < hi) {
-      int64_t mid = (lo + hi) >> 1;
-      if (skeys[mid] < (uint32_t)v) lo = mid + 1; else hi = mid;
-    }
-    gstart[v] = lo;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t cur = skeys[i];
+    const int64_t prev = i ? (int64_t)skeys[i - 1] : -1;
+    for (int64_t v = prev + 1; v <= cur && v <= nvars; v++) gstart[v] = i;
+    if (i == n - 1)
+      for (int64_t v = cur + 1; v <= nvars; v++) gstart[v] = n;
   }
 }
 
@@ -53,7 +56,8 @@ int build_groups(mp_ctx *ctx, mp_dtrace *t, mp_err *err) {
   LAUNCH(ctx, k_group_init, grid_for(n, 256), 256, 0, t->var.p, n, keys.p, t->perm.p);
   int rc = dev_radix_sort_u32(ctx, keys.p, t->perm.p, n, bits_for((uint64_t)(t->nvars > 0 ? t->nvars - 1 : 0)), err);
   if (rc) return rc;
-  LAUNCH(ctx, k_group_bounds, grid_for((int64_t)t->nvars + 1, 256), 256, 0, keys.p, n, t->nvars, t->gstart.p);
+  if (n) LAUNCH(ctx, k_group_bounds, grid_for(n, 256), 256, 0, keys.p, n, t->nvars, t->gstart.p);
+  else CUDA_TRY(cudaMemsetAsync(t->gstart.p, 0, ((int64_t)t->nvars + 1) * 8, ctx->stream));
   t->grouped = true;
   return MP_OK;
 }
