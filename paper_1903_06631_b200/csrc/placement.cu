@@ -20,6 +20,14 @@
 // a variable starts as soon as its own predecessors are placed instead of
 // waiting for a whole wavefront.  The CSR rows arrive partitioned into
 // predecessors and successors by the conflict build (conflict.cu).
+//
+// Memory protocol (PLACE_SENTINEL): offsets and levels are written once,
+// from the sentinels -1 / 0, with relaxed stores; successor counters,
+// queue slots and polls are relaxed too.  A variable whose counter reached
+// zero reads its predecessors' offsets until none is a sentinel (a
+// non-sentinel value is final), so no release fence has to wait for the
+// offset store before the counters go down (3.5 % faster than acq_rel
+// counters + fences).
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
@@ -42,6 +50,9 @@
 #endif
 #ifndef PLACE_BACKOFF
 #define PLACE_BACKOFF 1    // exponential idle backoff
+#endif
+#ifndef PLACE_SENTINEL
+#define PLACE_SENTINEL 1   // write-once offsets with a sentinel instead of release/acquire fences
 #endif
 #ifndef PLACE_K4_ROLLED
 #define PLACE_K4_ROLLED 1  // rolled stage loops for 65..128 predecessors
@@ -77,6 +88,35 @@ struct PlaceArgs {
   unsigned long long *tdone;  // debug (MP_PLACE_TRACE): %globaltimer when each variable was placed
 };
 
+__device__ __forceinline__ int64_t ld_relaxed_s64(const int64_t *p) {
+  int64_t v;
+  asm volatile("ld.relaxed.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int32_t ld_relaxed_s32(const int32_t *p) {
+  int32_t v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Offset and level of placed predecessor j.  Sentinel mode: both are
+// written once (offset from -1, level from 0) with relaxed stores and the
+// counters carry no release/acquire, so a predecessor counted as placed may
+// not be visible yet — read until it is (a non-sentinel value is final).
+__device__ __forceinline__ void pred_off_level(const PlaceArgs &a, int32_t j, int64_t &s, int &l) {
+  if (PLACE_SENTINEL) {
+    for (;;) {
+      s = ld_relaxed_s64(&a.off[j]);
+      l = ld_relaxed_s32(&a.level[j]);
+      if (s >= 0 && l > 0) break;
+      __nanosleep(32);
+    }
+  } else {
+    s = __ldcg(&a.off[j]);
+    l = __ldcg(&a.level[j]);
+  }
+}
+
 // Gather the predecessors' ranges, sort them by start and replay
 // _pick_offset.  Ranges are sorted as one 64-bit key (start << IB | slot):
 // equal starts may come in any order (the hole scan only sees the running
@@ -97,9 +137,11 @@ __device__ __forceinline__ int64_t place_reg(const PlaceArgs &a, int64_t rb, int
     e[r] = INT64_MIN;
     if (i < m) {
       int32_t j = a.col[rb + i];
-      int64_t s = __ldcg(&a.off[j]);
+      int64_t s;
+      int l;
+      pred_off_level(a, j, s, l);
       e[r] = s + a.size[j];
-      lv = max(lv, __ldcg(&a.level[j]));
+      lv = max(lv, l);
       big |= (uint64_t)s >> (63 - IB) != 0;
       x[r] = ((uint64_t)s << IB) | (uint64_t)i;
     }
@@ -140,9 +182,10 @@ __device__ int64_t place_mem(const PlaceArgs &a, P buf, int64_t rb, int m, int64
     IV x{INT64_MAX, INT64_MAX};
     if (i < m) {
       int32_t j = a.col[rb + i];
-      x.s = __ldcg(&a.off[j]);
+      int l;
+      pred_off_level(a, j, x.s, l);
       x.e = x.s + a.size[j];
-      lv = max(lv, __ldcg(&a.level[j]));
+      lv = max(lv, l);
     }
     buf[i] = x;
   }
@@ -251,11 +294,12 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_MIN_BLOCKS) k_place_async
         // first probe with acquire (in a busy phase the slot is usually
         // filled already); later probes relaxed (an acquire load
         // invalidates L1 on every probe), acquiring once the slot is filled
-        if (PLACE_FIRST_ACQ && i < a.V) asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v1) : "l"(q) : "memory");
+        if (PLACE_FIRST_ACQ && !PLACE_SENTINEL && i < a.V)
+          asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v1) : "l"(q) : "memory");
         for (int spin = 0; !v1; spin++) {
           if (i < a.V) asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v1) : "l"(q) : "memory");
           if (v1) {
-            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v1) : "l"(q) : "memory");
+            if (!PLACE_SENTINEL) asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v1) : "l"(q) : "memory");
             break;
           }
           if ((!PLACE_BACKOFF || (spin & 7) == 7) && *(volatile int *)a.done >= a.V) { v1 = -1; break; }
@@ -280,8 +324,13 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_MIN_BLOCKS) k_place_async
     int64_t o = place_var(a, v, gwarp, rb, m, need, lvl);
 #endif
     if (lane == 0) {
-      a.off[v] = o;
-      a.level[v] = lvl;
+      if (PLACE_SENTINEL) {
+        asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(a.level + v), "r"(lvl) : "memory");
+        asm volatile("st.relaxed.gpu.global.s64 [%0], %1;" ::"l"(a.off + v), "l"(o) : "memory");
+      } else {
+        a.off[v] = o;
+        a.level[v] = lvl;
+      }
       if (o + need > fp) fp = o + need;
       if (lvl > dmax) dmax = lvl;
       PT_STAMP(0, v);
@@ -293,7 +342,7 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_MIN_BLOCKS) k_place_async
       // cumulative over the warp barrier above), then decrement every
       // successor's counter with relaxed atomics, SUCC_BATCH rows of 32 in
       // flight at once instead of one acq_rel round trip per 32
-      fence_acq_rel_gpu();
+      if (!PLACE_SENTINEL) fence_acq_rel_gpu();
       for (int64_t base = rb + m; base < re; base += 32 * SUCC_BATCH) {
         int32_t jj[SUCC_BATCH];
         int rem[SUCC_BATCH];
@@ -310,7 +359,7 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_MIN_BLOCKS) k_place_async
         if (!__any_sync(FULL_MASK, any)) continue;
         // acquire the other predecessors' offsets for the successors this
         // warp completed, and release them to whoever claims a published one
-        fence_acq_rel_gpu();
+        if (!PLACE_SENTINEL) fence_acq_rel_gpu();
         __syncwarp();
 #pragma unroll
         for (int c = 0; c < SUCC_BATCH; c++) {
@@ -348,7 +397,7 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_MIN_BLOCKS) k_place_async
         // acq_rel: releases this variable's offset (written by lane 0 before
         // the __syncwarp above; release is cumulative) and, for the last
         // predecessor, acquires every other predecessor's
-        ready = atom_sub_acq_rel(&a.remaining[j]) == 1;
+        ready = (PLACE_SENTINEL ? atom_dec_relaxed(&a.remaining[j]) : atom_sub_acq_rel(&a.remaining[j])) == 1;
       }
       if (ready) PT_STAMP(2, j);
       unsigned bal = __ballot_sync(FULL_MASK, ready);
@@ -366,7 +415,8 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_MIN_BLOCKS) k_place_async
         qb = __shfl_sync(FULL_MASK, qb, __ffs(bal) - 1);
         if (ready) {
           int32_t *q = a.queue + qb + __popc(bal & lanemask_lt());
-          asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(q), "r"(j + 1) : "memory");
+          if (PLACE_SENTINEL) asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(q), "r"(j + 1) : "memory");
+          else asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(q), "r"(j + 1) : "memory");
         }
       }
     }
@@ -584,6 +634,10 @@ extern "C" int mp_plan_pool(mp_ctx *ctx, mp_dgraph *g, int32_t policy, int64_t *
   static int per_sm_cached = 0;
   DBuf<int64_t> &off = g->offsets;
   CUDA_TRY(off.alloc(V, st));
+  if (PLACE_SENTINEL) {
+    CUDA_TRY(cudaMemsetAsync(off.p, 0xff, V * 8, st));
+    CUDA_TRY(cudaMemsetAsync(level.p, 0, V * 4, st));
+  }
   size_t smem = 0;
   if (!per_sm_cached)
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_cached, k_place_async, PLACE_THREADS, smem));
