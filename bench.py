@@ -150,7 +150,7 @@ def stage_bytes(n, p, V, nnz, levels):
         "conflict_prep": V * 24 + V * 24,
         "conflict_fill": nnz * 4 + V * 16,               # CSR column writes + row metadata
         "place_order": V * 8 + V * 4,
-        "place_split": nnz * (4 + 4 + 4),                # read col + rank gather + write partitioned col
+        "place_split": V * (4 + 4 + 4),                  # pcnt read, counters + queue written (rows arrive partitioned)
         "place": nnz // 2 * (4 + 8 + 8) + nnz // 2 * (4 + 4) + V * 24,
         "footprint": V * 16,
     }
