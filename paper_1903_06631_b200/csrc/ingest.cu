@@ -282,6 +282,22 @@ __global__ void k_period_verify(const uint8_t *kind, const int64_t *size, int64_
   }
 }
 
+// Quick filter: candidate p survives if its last min(p, DT_QUICK)
+// fingerprint pairs match (a period must); the smallest survivor is then
+// verified exactly.  Typical traces eliminate every non-period within a few
+// pairs, so the prefix hashes are only needed when that survivor fails.
+constexpr int DT_QUICK = 32;
+__global__ void k_period_quick(const uint8_t *kind, const int64_t *size, int64_t n, unsigned long long *best) {
+  for (int64_t p = 1 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p <= n / 2;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = p < DT_QUICK ? p : DT_QUICK;
+    bool ok = true;
+    for (int64_t k = 1; k <= q; k++)
+      if (kind[n - k] != kind[n - p - k] || size[n - k] != size[n - p - k]) { ok = false; break; }
+    if (ok) atomicMin(best, (unsigned long long)p);
+  }
+}
+
 extern "C" int mp_detect(mp_ctx *ctx, mp_dtrace *t, int64_t *period, mp_err *err) {
   int64_t n = t->n;
   if (n < 2) {
@@ -295,6 +311,28 @@ extern "C" int mp_detect(mp_ctx *ctx, mp_dtrace *t, int64_t *period, mp_err *err
   rc0 = trace_need(ctx, t, TC_KIND | TC_SIZE, err);
   if (rc0) return rc0;
   StageTimer tm(ctx, MP_ST_DETECT);
+  unsigned long long *d_best = (unsigned long long *)ctx->d_small;
+  int *d_bad = (int *)(ctx->d_small + 1);
+  int64_t pmin = 1;
+  {
+    CUDA_TRY(cudaMemsetAsync(d_best, 0xff, 8, ctx->stream));
+    CUDA_TRY(cudaMemsetAsync(d_bad, 0, 4, ctx->stream));
+    LAUNCH(ctx, k_period_quick, grid_for(n / 2, 256, 16384), 256, 0, t->kind.p, t->size.p, n, d_best);
+    LAUNCH(ctx, k_period_verify, grid_for(n / 2, 256, 4096), 256, 0, t->kind.p, t->size.p, n,
+           (const unsigned long long *)d_best, d_bad);
+    int64_t h[2];
+    int rc = dev_read_n(ctx, d_best, h, 16, err);
+    if (rc) return rc;
+    if ((uint64_t)h[0] == ~0ull) {  // no candidate survives: no period
+      mp_set_err(err, MP_E_PERIOD_NOT_FOUND, n, 0, 0, "no period");
+      return MP_E_PERIOD_NOT_FOUND;
+    }
+    if (!(int)h[1]) {
+      *period = h[0];
+      return MP_OK;
+    }
+    pmin = h[0] + 1;  // the smallest survivor is not a period: hash search above it
+  }
   int64_t ntiles = (n + DT_TILE - 1) / DT_TILE;
   DBuf<HPair> agg;
   DBuf<uint64_t> P;
@@ -303,10 +341,11 @@ extern "C" int mp_detect(mp_ctx *ctx, mp_dtrace *t, int64_t *period, mp_err *err
   LAUNCH(ctx, k_hash_tiles, (unsigned)ntiles, DT_THREADS, 0, t->kind.p, t->size.p, n, agg.p);
   LAUNCH(ctx, k_hash_tile_prefix, 1, DT_THREADS, 0, agg.p, ntiles);
   LAUNCH(ctx, k_hash_prefix, (unsigned)ntiles, DT_THREADS, 0, t->kind.p, t->size.p, n, agg.p, P.p);
-  unsigned long long *d_best = (unsigned long long *)ctx->d_small;
-  int *d_bad = (int *)(ctx->d_small + 1);
-  int64_t pmin = 1;
   for (;;) {
+    if (pmin > n / 2) {
+      mp_set_err(err, MP_E_PERIOD_NOT_FOUND, n, 0, 0, "no period");
+      return MP_E_PERIOD_NOT_FOUND;
+    }
     CUDA_TRY(cudaMemsetAsync(d_best, 0xff, 8, ctx->stream));
     CUDA_TRY(cudaMemsetAsync(d_bad, 0, 4, ctx->stream));
     LAUNCH(ctx, k_period_candidates, grid_for((n / 2 - pmin + PC_RUN) / PC_RUN, 256, 8192), 256, 0, P.p, n, pmin,

@@ -105,3 +105,40 @@ def test_timestamp_only_violation_is_reported_after_the_plan():
     t[i] = -1
     got = _outcome(_with(a, t_us=t))
     assert got[0] == "InvariantViolation" and got[1] == i
+
+
+# ---- period detection: the quick filter's smallest survivor is not a period ----
+
+def _fp_trace(kinds, sizes):
+    from paper_1903_06631_b200.trace import TraceArrays
+    n = len(kinds)
+    return TraceArrays.from_columns(np.array(kinds, np.uint8), [f"v{i % 7}" for i in range(n)],
+                                    np.array(sizes, np.int64), np.arange(n, dtype=np.int64))
+
+
+@pytest.mark.parametrize("shift,reps", [(50, 2), (40, 3), (33, 2), (64, 2)])
+def test_detect_when_a_non_period_passes_the_quick_filter(shift, reps):
+    """A block whose last 32 events repeat the 32 events `shift` earlier:
+    p = shift matches the last 32 pairs (the quick filter's window) but not
+    all p of them, so the exact check rejects it and the hash search must
+    find the real period (the block length); oracle.detect restates
+    iteration.py:93-105."""
+    import oracle
+    from paper_1903_06631_b200 import _native as N
+    from paper_1903_06631_b200.errors import PeriodNotFound
+    rng = np.random.default_rng(shift)
+    L = 120
+    sizes = rng.integers(1, 1 << 40, L)
+    sizes[L - 32:] = sizes[L - 32 - shift:L - shift]
+    block = [(0, int(x)) for x in sizes]
+    ev = block * reps
+    arrays = _fp_trace([k for k, _ in ev], [x for _, x in ev])
+    rc, want = oracle.detect(arrays)
+    assert rc == 0 and want == L
+    assert N.detect(arrays) == want
+    # and without a real period: the fallback reports none
+    arrays = _fp_trace([k for k, _ in block], [x for _, x in block])
+    rc, _ = oracle.detect(arrays)
+    assert rc != 0
+    with pytest.raises(PeriodNotFound):
+        N.detect(arrays)
