@@ -35,6 +35,7 @@
 constexpr int SW_THREADS = 128;
 constexpr int SW_WARPS = SW_THREADS / 32;
 constexpr size_t SW_FAST_BYTES = 72 * 1024;
+constexpr int SW_QUICK = 16;  // detect: fingerprint pairs of the quick filter
 constexpr int PL_K = 4;  // placement list entries per lane per pass  // per-CTA shared-memory arena
 
 // ---------------------------------------------------------------------------
@@ -548,9 +549,37 @@ __device__ void sweep_one(const SweepArgs &a, int64_t t, char *slab, char *fast,
   }
 
   // ---- detect_iteration: smallest p with the last 2p fingerprints equal ----
-  if (tid == 0) sh.best_p = LLONG_MAX;
+  // Quick filter first: thread per candidate, a period must match its last
+  // min(p, SW_QUICK) pairs; the smallest survivor is checked exactly by the
+  // CTA.  Typical traces settle in one round; after a few rejected
+  // survivors the warp-per-candidate search below takes over above them.
+  int64_t lo_p = 1;
+  long long found = LLONG_MAX;
+  for (int it = 0; it < 4 && found == LLONG_MAX; it++) {
+    if (tid == 0) sh.best_p = LLONG_MAX;
+    __syncthreads();
+    for (int64_t pp = lo_p + tid; pp <= n / 2; pp += SW_THREADS) {
+      const int64_t qq = pp < SW_QUICK ? pp : SW_QUICK;
+      bool ok = true;
+      for (int64_t k = 1; k <= qq; k++)
+        if (kind[n - k] != kind[n - pp - k] || size[n - k] != size[n - pp - k]) { ok = false; break; }
+      if (ok) {
+        atomicMin(&sh.best_p, (long long)pp);
+        break;  // this thread's later candidates are larger
+      }
+    }
+    __syncthreads();
+    const long long c = sh.best_p;
+    if (c == LLONG_MAX) { lo_p = n / 2 + 1; break; }  // every candidate left fails: no period
+    bool good = true;
+    for (int64_t i = tid; i < c; i += SW_THREADS)
+      good &= kind[n - c + i] == kind[n - 2 * c + i] && size[n - c + i] == size[n - 2 * c + i];
+    if (__syncthreads_and(good)) found = c;
+    else lo_p = c + 1;
+  }
+  if (tid == 0) sh.best_p = found;
   __syncthreads();
-  for (int64_t p = warp + 1; p <= n / 2; p += SW_WARPS) {
+  for (int64_t p = lo_p + warp; found == LLONG_MAX && p <= n / 2; p += SW_WARPS) {
     long long best = __shfl_sync(FULL_MASK, *(volatile long long *)&sh.best_p, 0);
     if (p >= best) break;
     bool ok = true;

@@ -132,3 +132,36 @@ def test_sweep_sharded_runner_matches_single_device():
     for t in range(batch.ntraces):
         assert np.array_equal(got.offsets_of(t), whole.offsets_of(t))
         assert np.array_equal(got.order_of(t), whole.order_of(t))
+
+
+def test_sweep_detect_with_rejected_quick_survivors():
+    """Traces whose last 16 fingerprints reappear at several distances: each
+    distance passes the sweep's quick filter and fails the exact check (up to
+    5 times, past the 4 quick rounds into the warp-per-candidate search);
+    the period and every record must equal the oracle's."""
+    from paper_1903_06631_b200.trace import TraceArrays
+    traces = []
+    for ncopies in (0, 1, 3, 5):
+        rng = np.random.default_rng(100 + ncopies)
+        L = 200
+        sizes = rng.integers(1, 1 << 40, L)
+        tail = sizes[L - 16:].copy()
+        for s in (30, 50, 70, 90, 110)[:ncopies]:
+            sizes[L - s - 16:L - s] = tail
+        for reps in (2, 3):
+            n = L * reps
+            kinds = np.zeros(n, np.uint8)       # all mallocs of distinct fresh names
+            sz = np.tile(sizes, reps)
+            names = [f"x{i}" for i in range(n)]
+            # free each variable right after its malloc so the trace is valid
+            k2 = np.repeat(kinds, 2)
+            k2[1::2] = 1
+            s2 = np.repeat(sz, 2)
+            s2[1::2] = 0
+            n2 = [nm for nm in names for _ in (0, 1)]
+            traces.append(TraceArrays.from_columns(k2, n2, s2, np.arange(2 * n, dtype=np.int64)))
+    batch = sweep.SweepBatch.from_traces(traces)
+    params = sweep.SweepParams(budgets=(0.9, 0.5), threshold_bytes=1)
+    res = sweep.run_sweep(batch, params)
+    compare_with_oracle(batch, res, params)
+    assert all(int(res.traces["period"][t]) == 2 * 200 for t in range(batch.ntraces))
