@@ -21,7 +21,7 @@
 // waiting for a whole wavefront.  The CSR rows arrive partitioned into
 // predecessors and successors by the conflict build (conflict.cu).
 //
-// Memory protocol (PLACE_SENTINEL): offsets and levels are written once,
+// Memory protocol: offsets and levels are written once,
 // from the sentinels -1 / 0, with relaxed stores; successor counters,
 // queue slots and polls are relaxed too.  A variable whose counter reached
 // zero reads its predecessors' offsets until none is a sentinel (a
@@ -43,16 +43,10 @@
 #endif
 // experiment switches (tools/ab_place.sh)
 #ifndef PLACE_SUCC_PIPE
-#define PLACE_SUCC_PIPE 2  // 1: batched relaxed successor decrements between two fences; 2: that for rows with > 32 successors, one acq_rel atomic per successor otherwise; 0: never
-#endif
-#ifndef PLACE_FIRST_ACQ
-#define PLACE_FIRST_ACQ 1  // first queue probe with acquire
+#define PLACE_SUCC_PIPE 2  // successor decrements batched 128 per round trip: 1 always, 2 rows with > 32 successors, 0 never
 #endif
 #ifndef PLACE_BACKOFF
 #define PLACE_BACKOFF 1    // exponential idle backoff
-#endif
-#ifndef PLACE_SENTINEL
-#define PLACE_SENTINEL 1   // write-once offsets with a sentinel instead of release/acquire fences
 #endif
 #ifndef PLACE_K4_ROLLED
 #define PLACE_K4_ROLLED 1  // rolled stage loops for 65..128 predecessors
@@ -99,21 +93,16 @@ __device__ __forceinline__ int32_t ld_relaxed_s32(const int32_t *p) {
   return v;
 }
 
-// Offset and level of placed predecessor j.  Sentinel mode: both are
-// written once (offset from -1, level from 0) with relaxed stores and the
-// counters carry no release/acquire, so a predecessor counted as placed may
-// not be visible yet — read until it is (a non-sentinel value is final).
+// Offset and level of placed predecessor j.  Both are written once (offset
+// from -1, level from 0) with relaxed stores and the counters carry no
+// release/acquire, so a predecessor counted as placed may not be visible
+// yet — read until it is (a non-sentinel value is final).
 __device__ __forceinline__ void pred_off_level(const PlaceArgs &a, int32_t j, int64_t &s, int &l) {
-  if (PLACE_SENTINEL) {
-    for (;;) {
-      s = ld_relaxed_s64(&a.off[j]);
-      l = ld_relaxed_s32(&a.level[j]);
-      if (s >= 0 && l > 0) break;
-      __nanosleep(32);
-    }
-  } else {
-    s = __ldcg(&a.off[j]);
-    l = __ldcg(&a.level[j]);
+  for (;;) {
+    s = ld_relaxed_s64(&a.off[j]);
+    l = ld_relaxed_s32(&a.level[j]);
+    if (s >= 0 && l > 0) break;
+    __nanosleep(32);
   }
 }
 
@@ -208,13 +197,6 @@ __device__ __forceinline__ int atom_dec_relaxed(int32_t *p) {
   return old;
 }
 
-__device__ __forceinline__ int atom_sub_acq_rel(int32_t *p) {
-  int old;
-  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], -1;" : "=r"(old) : "l"(p) : "memory");
-  return old;
-}
-
-__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
 constexpr int SUCC_BATCH = 4;                // successor rows of 32 decremented per round trip
 constexpr unsigned PLACE_MAX_SLEEP = 256;    // ns, idle-warp poll backoff cap
@@ -283,25 +265,16 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_MIN_BLOCKS) k_place_async
       local_done = 0;
       int v1 = 0;
       if (lane == 0) {
-        // acquire: the predecessors' offsets were released before the slot
-        // was published; continuation means not every variable passes
-        // through the queue, so an empty slot ends the warp once all are placed
+        // continuation means not every variable passes through the queue,
+        // so an empty slot ends the warp once all are placed; idle warps back
+        // off exponentially and look at the done count only now and then
+        // (thousands of pollers on one line slow the L2 slice the counters
+        // live in)
         const int32_t *q = a.queue + (i < a.V ? i : 0);
-        // idle warps back off exponentially and look at the done count only
-        // now and then: thousands of pollers on one line slow the L2 slice
-        // the working warps' atomics go through
         unsigned ns = 32;
-        // first probe with acquire (in a busy phase the slot is usually
-        // filled already); later probes relaxed (an acquire load
-        // invalidates L1 on every probe), acquiring once the slot is filled
-        if (PLACE_FIRST_ACQ && !PLACE_SENTINEL && i < a.V)
-          asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v1) : "l"(q) : "memory");
         for (int spin = 0; !v1; spin++) {
           if (i < a.V) asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v1) : "l"(q) : "memory");
-          if (v1) {
-            if (!PLACE_SENTINEL) asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v1) : "l"(q) : "memory");
-            break;
-          }
+          if (v1) break;
           if ((!PLACE_BACKOFF || (spin & 7) == 7) && *(volatile int *)a.done >= a.V) { v1 = -1; break; }
           __nanosleep(PLACE_BACKOFF ? ns : 20);
           if (ns < PLACE_MAX_SLEEP) ns <<= 1;
@@ -324,13 +297,8 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_MIN_BLOCKS) k_place_async
     int64_t o = place_var(a, v, gwarp, rb, m, need, lvl);
 #endif
     if (lane == 0) {
-      if (PLACE_SENTINEL) {
-        asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(a.level + v), "r"(lvl) : "memory");
-        asm volatile("st.relaxed.gpu.global.s64 [%0], %1;" ::"l"(a.off + v), "l"(o) : "memory");
-      } else {
-        a.off[v] = o;
-        a.level[v] = lvl;
-      }
+      asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(a.level + v), "r"(lvl) : "memory");
+      asm volatile("st.relaxed.gpu.global.s64 [%0], %1;" ::"l"(a.off + v), "l"(o) : "memory");
       if (o + need > fp) fp = o + need;
       if (lvl > dmax) dmax = lvl;
       PT_STAMP(0, v);
@@ -338,11 +306,8 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_MIN_BLOCKS) k_place_async
     local_done++;
     __syncwarp();
     if (PLACE_SUCC_PIPE && re - (rb + m) > (PLACE_SUCC_PIPE == 2 ? 32 : 0)) {
-      // release this variable's offset (stored by lane 0; the fence is
-      // cumulative over the warp barrier above), then decrement every
-      // successor's counter with relaxed atomics, SUCC_BATCH rows of 32 in
-      // flight at once instead of one acq_rel round trip per 32
-      if (!PLACE_SENTINEL) fence_acq_rel_gpu();
+      // decrement every successor's counter, SUCC_BATCH rows of 32 in
+      // flight at once instead of one round trip per 32
       for (int64_t base = rb + m; base < re; base += 32 * SUCC_BATCH) {
         int32_t jj[SUCC_BATCH];
         int rem[SUCC_BATCH];
@@ -357,9 +322,6 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_MIN_BLOCKS) k_place_async
 #pragma unroll
         for (int c = 0; c < SUCC_BATCH; c++) any |= rem[c] == 1;
         if (!__any_sync(FULL_MASK, any)) continue;
-        // acquire the other predecessors' offsets for the successors this
-        // warp completed, and release them to whoever claims a published one
-        if (!PLACE_SENTINEL) fence_acq_rel_gpu();
         __syncwarp();
 #pragma unroll
         for (int c = 0; c < SUCC_BATCH; c++) {
@@ -394,10 +356,7 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_MIN_BLOCKS) k_place_async
       int32_t j = 0;
       if (k < re) {
         j = a.col[k];
-        // acq_rel: releases this variable's offset (written by lane 0 before
-        // the __syncwarp above; release is cumulative) and, for the last
-        // predecessor, acquires every other predecessor's
-        ready = (PLACE_SENTINEL ? atom_dec_relaxed(&a.remaining[j]) : atom_sub_acq_rel(&a.remaining[j])) == 1;
+        ready = atom_dec_relaxed(&a.remaining[j]) == 1;
       }
       if (ready) PT_STAMP(2, j);
       unsigned bal = __ballot_sync(FULL_MASK, ready);
@@ -415,8 +374,7 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_MIN_BLOCKS) k_place_async
         qb = __shfl_sync(FULL_MASK, qb, __ffs(bal) - 1);
         if (ready) {
           int32_t *q = a.queue + qb + __popc(bal & lanemask_lt());
-          if (PLACE_SENTINEL) asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(q), "r"(j + 1) : "memory");
-          else asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(q), "r"(j + 1) : "memory");
+          asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(q), "r"(j + 1) : "memory");
         }
       }
     }
@@ -634,10 +592,9 @@ extern "C" int mp_plan_pool(mp_ctx *ctx, mp_dgraph *g, int32_t policy, int64_t *
   static int per_sm_cached = 0;
   DBuf<int64_t> &off = g->offsets;
   CUDA_TRY(off.alloc(V, st));
-  if (PLACE_SENTINEL) {
-    CUDA_TRY(cudaMemsetAsync(off.p, 0xff, V * 8, st));
-    CUDA_TRY(cudaMemsetAsync(level.p, 0, V * 4, st));
-  }
+  // sentinels: -1 offsets, level 0 (see pred_off_level)
+  CUDA_TRY(cudaMemsetAsync(off.p, 0xff, V * 8, st));
+  CUDA_TRY(cudaMemsetAsync(level.p, 0, V * 4, st));
   size_t smem = 0;
   if (!per_sm_cached)
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_cached, k_place_async, PLACE_THREADS, smem));
