@@ -282,6 +282,7 @@ class DeviceSweep:
         err = MpErr()
         raise_for(L.mp_sweep_profile_download(N.ctx(), self._h, ptr(out), C.byref(err)), err)
         self.profile_extra = out[:self.batch.ntraces, 8:]
+        self.profile_raw = out[:self.batch.ntraces]
         return np.diff(out[:self.batch.ntraces, :8], axis=1)
 
     def close(self):

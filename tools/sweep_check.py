@@ -76,6 +76,10 @@ def main():
     for j, nm in enumerate(names):
         print(f"  {nm:24s} med {int(np.median(prof[:, j])):>9d}  " + " ".join(f"{int(prof[t, j]):>9d}" for t in top))
     ex = ds.profile_extra
+    raw = ds.profile_raw
+    print("  placement start / end after CTA start (5 slowest):",
+          [(int(raw[t, 8] - raw[t, 0]), int(raw[t, 9] - raw[t, 0])) for t in top], "CTA end",
+          [int(raw[t, 7] - raw[t, 0]) for t in top])
     print("  placement loop cycles (5 slowest):", [int(ex[t, 1] - ex[t, 0]) for t in top],
           "scan", [int(ex[t, 2]) for t in top], "insert", [int(ex[t, 3]) for t in top])
     print("  budget 0 (5 slowest): sched+overlay", [int(ex[t, 4]) for t in top], "replay", [int(ex[t, 5]) for t in top],
