@@ -218,19 +218,34 @@ __global__ void k_iv_fill(int64_t n, const int32_t *sv, const int64_t *row_off, 
   int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const unsigned lt = lanemask_lt();
   for (int64_t k = warp; k < n; k += nwarps) {
+    // the first 32 partners are read with the interval itself (their
+    // addresses do not depend on its forward count)
+    const int64_t k0 = k + 1 + lane;
+    const int32_t j0 = k0 < n ? sv[3 * k0] : 0, rj0 = k0 < n ? sv[3 * k0 + 1] : 0;
     const int32_t u = sv[3 * k], ru = sv[3 * k + 1], f = sv[3 * k + 2];
     int64_t rbu = row_off[u], reu = row_off[u + 1];
     for (int32_t base = 0; base < f; base += 32) {
       int32_t jx = base + lane;
       bool valid = jx < f;
-      int32_t j = 0, rj = 0;
-      if (valid) {
+      int32_t j = j0, rj = rj0;
+      if (base && valid) {
         j = sv[3 * (k + 1 + jx)];
         rj = sv[3 * (k + 1 + jx) + 1];
       }
       bool isp = valid && rj < ru;  // j precedes u in placement order
       unsigned bp = __ballot_sync(FULL_MASK, isp);
       unsigned bs = __ballot_sync(FULL_MASK, valid && !isp);
+      // the mirrored slot in j's row and u's own cursors are independent
+      // round trips: issue both before waiting on either
+      int32_t qj = 0;
+      int64_t mj = 0;
+      if (isp) {
+        qj = atomicAdd(&sc[j], 1);  // u succeeds j
+        mj = row_off[j + 1] - 1;
+      } else if (valid) {
+        qj = atomicAdd(&pc[j], 1);  // u precedes j
+        mj = row_off[j];
+      }
       int32_t p0 = 0, s0 = 0;
       if (lane == 0) {
         if (bp) p0 = atomicAdd(&pc[u], __popc(bp));
@@ -240,12 +255,10 @@ __global__ void k_iv_fill(int64_t n, const int32_t *sv, const int64_t *row_off, 
       s0 = __shfl_sync(FULL_MASK, s0, 0);
       if (isp) {
         col[rbu + p0 + __popc(bp & lt)] = j;
-        int32_t q = atomicAdd(&sc[j], 1);  // u succeeds j
-        col[row_off[j + 1] - 1 - q] = u;
+        col[mj - qj] = u;
       } else if (valid) {
         col[reu - 1 - (s0 + __popc(bs & lt))] = j;
-        int32_t q = atomicAdd(&pc[j], 1);  // u precedes j
-        col[row_off[j] + q] = u;
+        col[mj + qj] = u;
       }
     }
   }
