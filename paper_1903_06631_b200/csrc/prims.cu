@@ -161,6 +161,12 @@ template int dev_exclusive_scan<int64_t>(mp_ctx *, const int64_t *, int64_t *, i
 // ----------------------------------------------------------------------------
 // radix sort
 
+#ifndef RS_LOOKBACK_BATCH
+#define RS_LOOKBACK_BATCH 8  // predecessor digit counts read per look-back round trip (1: 5 % slower passes)
+#endif
+#ifndef RS_ITEMS32
+#define RS_ITEMS32 16  // keys per thread of a 32-bit pass tile
+#endif
 constexpr int RS_THREADS = 256;
 constexpr int RS_WARPS = RS_THREADS / 32;
 constexpr int RS_BINS = 256;
@@ -271,6 +277,24 @@ __global__ void __launch_bounds__(RS_THREADS) k_os_pass(const K *keys, const uin
     } else {
       atomicExch(mine, OS_AGG | (uint32_t)run);
       uint32_t excl = 0;
+#if RS_LOOKBACK_BATCH > 1
+      // RS_LOOKBACK_BATCH predecessors per round trip, consumed in order
+      for (int64_t p = tile - 1;; p -= RS_LOOKBACK_BATCH) {
+        uint32_t x[RS_LOOKBACK_BATCH];
+#pragma unroll
+        for (int i = 0; i < RS_LOOKBACK_BATCH; i++)
+          x[i] = p - i >= 0 ? *(volatile uint32_t *)(look + (p - i) * RS_BINS + d) : 0u;
+        bool done = false;
+#pragma unroll
+        for (int i = 0; i < RS_LOOKBACK_BATCH; i++) {
+          uint32_t v = x[i];
+          while (!(v & ~OS_MASK)) v = *(volatile uint32_t *)(look + (p - i) * RS_BINS + d);
+          excl += v & OS_MASK;
+          if (v & OS_PFX) { done = true; break; }
+        }
+        if (done) break;
+      }
+#else
       for (int64_t p = tile - 1;;) {
         uint32_t x = *(volatile uint32_t *)(look + p * RS_BINS + d);
         if (!(x & ~OS_MASK)) continue;
@@ -278,6 +302,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_os_pass(const K *keys, const uin
         if (x & OS_PFX) break;
         p--;
       }
+#endif
       atomicExch(mine, OS_PFX | (excl + (uint32_t)run));
       gbase[d] = gstart[d] + (int32_t)excl;
     }
@@ -372,7 +397,7 @@ static int radix_sort_impl(mp_ctx *ctx, K *keys, uint32_t *vals, int64_t n, int 
 }
 
 int dev_radix_sort_u32(mp_ctx *ctx, uint32_t *keys, uint32_t *vals, int64_t n, int bits, mp_err *err) {
-  return radix_sort_impl<uint32_t, 16>(ctx, keys, vals, n, bits, err);
+  return radix_sort_impl<uint32_t, RS_ITEMS32>(ctx, keys, vals, n, bits, err);
 }
 
 int dev_radix_sort_u64(mp_ctx *ctx, uint64_t *keys, uint32_t *vals, int64_t n, int bits, mp_err *err) {
