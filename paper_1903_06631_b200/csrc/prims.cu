@@ -40,6 +40,9 @@ int dev_read_i64(mp_ctx *ctx, const int64_t *d, int64_t *h, mp_err *err) {
 // ----------------------------------------------------------------------------
 // exclusive scan: block partials -> scan of partials -> block scan + offset
 
+#ifndef SCAN_VEC
+#define SCAN_VEC 1  // 16-byte loads/stores of full tiles
+#endif
 constexpr int SCAN_THREADS = 512;
 constexpr int SCAN_ITEMS = 8;
 constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
@@ -76,13 +79,28 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_onepass(const T *in, T *o
   __syncthreads();
   const int64_t tile = s_tile;
   const int64_t base = tile * SCAN_TILE;
-  T v[SCAN_ITEMS];
+  union {
+    T v[SCAN_ITEMS];
+    uint4 q[SCAN_ITEMS * sizeof(T) / 16];
+  } u;
+  T *const v = u.v;
   T s = 0;
+  // full tiles of 16-byte aligned arrays: each thread's run is read as
+  // 16-byte vectors (its SCAN_ITEMS values are contiguous)
+  const bool vec = SCAN_VEC && base + SCAN_TILE <= n && ((((uintptr_t)in) | ((uintptr_t)out)) & 15) == 0;
+  if (vec) {
+    const uint4 *src = (const uint4 *)(in + base + (int64_t)threadIdx.x * SCAN_ITEMS);
 #pragma unroll
-  for (int i = 0; i < SCAN_ITEMS; i++) {
-    int64_t j = base + (int64_t)threadIdx.x * SCAN_ITEMS + i;
-    v[i] = j < n ? in[j] : T(0);
-    s += v[i];
+    for (int i = 0; i < (int)(SCAN_ITEMS * sizeof(T) / 16); i++) u.q[i] = src[i];
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; i++) s += v[i];
+  } else {
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; i++) {
+      int64_t j = base + (int64_t)threadIdx.x * SCAN_ITEMS + i;
+      v[i] = j < n ? in[j] : T(0);
+      s += v[i];
+    }
   }
   T pre = block_excl_scan(s, &s_tot);
   if (threadIdx.x < 32) {
@@ -129,6 +147,18 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_onepass(const T *in, T *o
   }
   __syncthreads();
   T run = s_excl + pre;
+  if (vec) {
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; i++) {
+      T x = v[i];
+      v[i] = run;
+      run += x;
+    }
+    uint4 *dst = (uint4 *)(out + base + (int64_t)threadIdx.x * SCAN_ITEMS);
+#pragma unroll
+    for (int i = 0; i < (int)(SCAN_ITEMS * sizeof(T) / 16); i++) dst[i] = u.q[i];
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < SCAN_ITEMS; i++) {
     int64_t j = base + (int64_t)threadIdx.x * SCAN_ITEMS + i;
