@@ -27,7 +27,8 @@ The line also carries "swap": BASELINE configs[2], the swap-iteration
 overhead on a VGG-16 b128 training iteration (tools/config3_swap.py in a
 subprocess on rank 0's GPU: traced, planned, executed with copy streams for
 10 iterations at 95 % of the traced peak, the reference's SWDOA selection and
-the executor-aware one; lower is better).
+the executor-aware one — strict (copies must fit their windows at 0.9x the
+measured link rates) and with a 4 % stall budget; lower is better).
 
 --impl reference: the reference's CPU algorithm (the C oracle port — the
 Python reference cannot run on this box) on all host cores, one trace
@@ -431,7 +432,7 @@ def run_swap_leg(local_rank: int, frac: float = 0.95) -> dict:
     hooked iteration without swaps (tools/config3_swap.py, own process: the
     pluggable allocator must own the CUDA context from its first malloc)."""
     cmd = [sys.executable, os.path.join(ROOT, "tools", "config3_swap.py"), "--fracs", str(frac),
-           "--modes", "reference_selection,window_fits", "--steps", "10"]
+           "--modes", "reference_selection,window_fits,window_fits_stall4pct", "--steps", "10"]
     env = dict(os.environ, CUDA_VISIBLE_DEVICES=os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",")[local_rank]
                if os.environ.get("CUDA_VISIBLE_DEVICES") else str(local_rank))
     try:
