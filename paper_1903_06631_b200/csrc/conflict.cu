@@ -19,6 +19,9 @@
 constexpr int MAXSEG = 64;
 
 // effective intervals of each variable: [lo_k, min{hi_m > lo_k}) merged
+// GENERAL = false: every variable has at most two segments (profiles); the
+// kernel then carries no per-thread segment arrays
+template <bool GENERAL>
 __global__ void k_norm_count(int64_t nv, const int64_t *seg_off, const int32_t *lo, const int32_t *hi,
                              int64_t *ecnt, int32_t *ea, int32_t *eb, int *overflow, int write,
                              const int64_t *eoff, int32_t *ivar) {
@@ -26,7 +29,7 @@ __global__ void k_norm_count(int64_t nv, const int64_t *seg_off, const int32_t *
   int32_t lmin = INT32_MAX, lmax = INT32_MIN;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
     const int64_t s0 = seg_off[v], s1 = seg_off[v + 1];
-    if (s1 - s0 <= 2) {
+    if (!GENERAL || s1 - s0 <= 2) {
       // profile variables (at most two segments): the same rule in registers
       int32_t l0 = 0, h0 = 0, l1 = 0, h1 = 0;
       int mm = 0;
@@ -60,6 +63,7 @@ __global__ void k_norm_count(int64_t nv, const int64_t *seg_off, const int32_t *
       if (!write) ecnt[v] = c;
       continue;
     }
+    if constexpr (GENERAL) {
     int32_t L[MAXSEG], H[MAXSEG];
     int m = 0;
     for (int64_t s = s0; s < s1; s++) {
@@ -90,6 +94,7 @@ __global__ void k_norm_count(int64_t nv, const int64_t *seg_off, const int32_t *
       cur_end = ne;
     }
     if (!write) ecnt[v] = c;
+    }
   }
   if (!write) {
 #pragma unroll
@@ -265,7 +270,8 @@ __global__ void k_iv_fill(int64_t n, const int32_t *sv, const int64_t *row_off, 
 }
 
 static int build_csr(mp_ctx *ctx, int64_t nv, const int64_t *seg_off_d, const int32_t *lo_d,
-                     const int32_t *hi_d, mp_dgraph *g, mp_err *err) {
+                     const int32_t *hi_d, bool general, mp_dgraph *g, mp_err *err) {
+  auto norm = general ? k_norm_count<true> : k_norm_count<false>;
   cudaStream_t st = ctx->stream;
   // placement order first: the fill writes rows already split by it
   CUDA_TRY(g->rank.alloc(nv, st));
@@ -284,7 +290,7 @@ static int build_csr(mp_ctx *ctx, int64_t nv, const int64_t *seg_off_d, const in
   CUDA_TRY(cudaMemcpyAsync(d_mm, mm_init, 8, cudaMemcpyHostToDevice, st));
   int rc = placement_rank_keys(ctx, nv, g->size.p, d_kmm, err);
   if (rc) return rc;
-  LAUNCH(ctx, k_norm_count, grid_for(nv, 128), 128, 0, nv, seg_off_d, lo_d, hi_d, ecnt.p, (int32_t *)nullptr,
+  LAUNCH(ctx, norm, grid_for(nv, 128), 128, 0, nv, seg_off_d, lo_d, hi_d, ecnt.p, (int32_t *)nullptr,
          d_mm, d_over, 0, (const int64_t *)nullptr, (int32_t *)nullptr);
   int64_t *d_tot = ctx->d_small + 1;
   rc = dev_exclusive_scan<int64_t>(ctx, ecnt.p, eoff.p, nv, d_tot, err);
@@ -307,7 +313,7 @@ static int build_csr(mp_ctx *ctx, int64_t nv, const int64_t *seg_off_d, const in
   DBuf<int32_t> ea, eb, ivar, sv, scur;
   CUDA_TRY(ea.alloc(ni, st)); CUDA_TRY(eb.alloc(ni, st)); CUDA_TRY(ivar.alloc(ni, st));
   CUDA_TRY(sv.alloc(3 * ni, st)); CUDA_TRY(scur.alloc(nv, st));
-  LAUNCH(ctx, k_norm_count, grid_for(nv, 128), 128, 0, nv, seg_off_d, lo_d, hi_d, ecnt.p, ea.p, eb.p,
+  LAUNCH(ctx, norm, grid_for(nv, 128), 128, 0, nv, seg_off_d, lo_d, hi_d, ecnt.p, ea.p, eb.p,
          d_over, 1, eoff.p, ivar.p);
   // order intervals by start.  Interval bounds are op positions, so when
   // their range is small a counting sort does it (order among equal starts
@@ -399,7 +405,7 @@ extern "C" int mp_conflict_from_profile(mp_ctx *ctx, mp_dprofile *P, mp_dgraph *
   if (nv) CUDA_TRY(cudaMemcpyAsync(g->size.p, P->size.p, nv * 8, cudaMemcpyDeviceToDevice, st));
   // profile variables are already in (alloc or -1, name) order: the
   // placement tie-break is the vertex index
-  int rc = build_csr(ctx, nv, so.p, lo.p, hi.p, g, err);
+  int rc = build_csr(ctx, nv, so.p, lo.p, hi.p, false, g, err);
   if (rc) { delete g; return rc; }
   *out = g;
   return MP_OK;
@@ -426,7 +432,7 @@ extern "C" int mp_conflict_from_arcs(mp_ctx *ctx, int32_t nvars, const int64_t *
     CUDA_TRY(cudaMemcpyAsync(g->size.p, size, nv * 8, cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaMemcpyAsync(g->tiekey.p, tiekey, nv * 8, cudaMemcpyHostToDevice, st));
   }
-  int rc = build_csr(ctx, nv, so.p, lo.p, hi.p, g, err);
+  int rc = build_csr(ctx, nv, so.p, lo.p, hi.p, true, g, err);
   if (rc) { delete g; return rc; }
   CUDA_TRY(cudaStreamSynchronize(st));  // host arrays are only borrowed for the call
   *out = g;
