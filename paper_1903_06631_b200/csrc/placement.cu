@@ -199,6 +199,12 @@ __device__ __forceinline__ int atom_dec_relaxed(int32_t *p) {
 
 
 constexpr int SUCC_BATCH = 4;                // successor rows of 32 decremented per round trip
+#ifndef PLACE_SLEEP0_NS
+#define PLACE_SLEEP0_NS 32
+#endif
+#ifndef PLACE_DONE_MASK
+#define PLACE_DONE_MASK 7
+#endif
 #ifndef PLACE_MAX_SLEEP_NS
 #define PLACE_MAX_SLEEP_NS 1024  // 256: 3.5 % slower, 4096: 3 % slower
 #endif
@@ -274,11 +280,11 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_MIN_BLOCKS) k_place_async
         // (thousands of pollers on one line slow the L2 slice the counters
         // live in)
         const int32_t *q = a.queue + (i < a.V ? i : 0);
-        unsigned ns = 32;
+        unsigned ns = PLACE_SLEEP0_NS;
         for (int spin = 0; !v1; spin++) {
           if (i < a.V) asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v1) : "l"(q) : "memory");
           if (v1) break;
-          if ((!PLACE_BACKOFF || (spin & 7) == 7) && *(volatile int *)a.done >= a.V) { v1 = -1; break; }
+          if ((!PLACE_BACKOFF || (spin & PLACE_DONE_MASK) == PLACE_DONE_MASK) && *(volatile int *)a.done >= a.V) { v1 = -1; break; }
           __nanosleep(PLACE_BACKOFF ? ns : 20);
           if (ns < PLACE_MAX_SLEEP) ns <<= 1;
         }
