@@ -82,7 +82,8 @@ def plan_arrays(arrays: TraceArrays, window: tuple[int, int] | None = None,
                 raise
             window = (len(arrays) - p, len(arrays))
         if validate:
-            N.validate(arrays, "structure")
+            # a resident trace has every column: one pass, one readback
+            N.validate(arrays, "structure" if fresh else "all")
         try:
             dp = N.extract(arrays, window[0], window[1])
             g = N.conflict_from_profile(dp)
@@ -93,10 +94,10 @@ def plan_arrays(arrays: TraceArrays, window: tuple[int, int] | None = None,
             else:
                 offs, fp, lv = N.plan_pool(g, POLICY_CODE[policy], nv, out=offsets_out)
         except (MemplanError, ValueError):
-            if validate:
+            if validate and fresh:
                 N.validate(arrays, "times")
             raise
-        if validate:
+        if validate and fresh:
             N.validate(arrays, "times")
         dims = dp.dims()
     finally:
