@@ -1,6 +1,5 @@
 // handles.cuh — device-resident objects behind the opaque C-ABI handles.
 #pragma once
-#include <cstring>
 
 #include "common.cuh"
 
@@ -56,26 +55,11 @@ struct mp_dprofile {
   cudaEvent_t times_ev = nullptr;
   bool times_pending = false;
   DBuf<double> dur;
-  // deferred scalars of mp_extract: peak, peak index, access count, duration
-  DBuf<int64_t> fin;
-  bool fin_pending = false, fin_duration = false;
 };
 
-// resolve what mp_extract left on the device: the scalars (one readback)
-// and the op times computed behind an asynchronous upload (device order on
-// the context stream, and the period duration on the host)
+// wait for deferred op times (device order on the context stream, and the
+// period duration on the host)
 inline int profile_times(mp_ctx *ctx, mp_dprofile *P, mp_err *err) {
-  if (P->fin_pending) {
-    int64_t fin[4];
-    CUDA_TRY(cudaMemcpyAsync(fin, P->fin.p, 32, cudaMemcpyDeviceToHost, ctx->stream));
-    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    const int64_t p = P->d.period;
-    P->d.peak_bytes = p ? fin[0] : 0;
-    P->d.peak_index = p ? fin[1] : 0;
-    P->d.naccess = fin[2];
-    if (P->fin_duration) memcpy(&P->d.duration_us, &fin[3], 8);
-    P->fin_pending = false;
-  }
   if (!P->times_pending) return MP_OK;
   CUDA_TRY(cudaStreamWaitEvent(ctx->stream, P->times_ev, 0));
   CUDA_TRY(cudaEventSynchronize(P->times_ev));

@@ -617,13 +617,14 @@ extern "C" int mp_extract(mp_ctx *ctx, mp_dtrace *t, int64_t start, int64_t end,
   delete tm;
   rc = profile_loads_async(ctx, P, err);
   if (rc) { delete P; return rc; }
-  // peak, peak index, access count, period duration: kept on the device and
-  // read back when the host first needs them (profile_times), so the next
-  // stage (the conflict build needs only nvars) starts without a host wait
-  CUDA_TRY(P->fin.alloc(4, st));
-  CUDA_TRY(cudaMemcpyAsync(P->fin.p, ctx->d_small, 32, cudaMemcpyDeviceToDevice, st));
-  P->fin_pending = true;
-  P->fin_duration = !late_times;
+  // one readback: peak, peak index, access count, period duration
+  int64_t fin[4];
+  rc = dev_read_n(ctx, ctx->d_small, fin, 32, err);
+  if (rc) { delete P; return rc; }
+  P->d.peak_bytes = p ? fin[0] : 0;
+  P->d.peak_index = p ? fin[1] : 0;
+  P->d.naccess = fin[2];
+  if (!late_times) memcpy(&P->d.duration_us, &fin[3], 8);
   P->nnames = t->nvars;
   *out = P;
   return MP_OK;
