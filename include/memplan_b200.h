@@ -169,6 +169,11 @@ int mp_trace_upload(mp_ctx *ctx, const mp_trace_in *in, mp_dtrace **out, mp_err 
  * reads, so grouping and period detection overlap the rest of the transfer.
  * The input buffers stay borrowed until mp_trace_wait returns. */
 int mp_trace_upload_async(mp_ctx *ctx, const mp_trace_in *in, mp_dtrace **out, mp_err *err);
+/* the timestamp column of an asynchronous upload is sent only here (or when a
+ * stage first needs it): call it before the placement, whose kernel a
+ * concurrent host-to-device copy barely slows, unlike the readback-bound
+ * stages before it.  Op times of profiles extracted meanwhile follow it. */
+int mp_trace_flush(mp_dtrace *t, mp_err *err);
 int mp_trace_wait(mp_dtrace *t, mp_err *err);
 int mp_trace_free(mp_dtrace *t);
 /* drop cached derived state (event grouping) so the next stage recomputes it */

@@ -39,7 +39,7 @@ def lib():
         L.mp_ctx_launches.restype = C.c_int64
         L.mp_ctx_stream.restype = C.c_void_p
         for name in ("mp_validate", "mp_detect", "mp_extract", "mp_trace_upload", "mp_trace_upload_async",
-                     "mp_trace_wait", "mp_validate_structure", "mp_validate_times", "mp_profile_download",
+                     "mp_trace_wait", "mp_trace_flush", "mp_validate_structure", "mp_validate_times", "mp_profile_download",
                      "mp_profile_upload", "mp_conflict_from_profile", "mp_conflict_from_arcs",
                      "mp_graph_download", "mp_plan_pool", "mp_ctx_create"):
             getattr(L, name).restype = C.c_int
@@ -132,6 +132,12 @@ def device_trace(arrays, asynchronous: bool = False) -> DTrace:
     except AttributeError:
         pass
     return d
+
+
+def trace_flush(d: DTrace) -> None:
+    """Send the deferred timestamp column of an asynchronous upload now."""
+    err = MpErr()
+    raise_for(lib().mp_trace_flush(d.h, C.byref(err)), err)
 
 
 def trace_wait(d: DTrace) -> None:

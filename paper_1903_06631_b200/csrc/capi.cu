@@ -125,9 +125,12 @@ static int trace_upload(mp_ctx *ctx, const mp_trace_in *in, mp_dtrace **out, boo
                        {4, t->t_us.p, in->t_us, (size_t)n * 8}};
   for (const Col &c : cols) {
     CUDA_TRY(cudaEventCreateWithFlags(&t->col_ev[c.bit], cudaEventDisableTiming));
+    if (c.bit == 4) continue;  // timestamps: at trace_flush_tus
     if (n && c.src) CUDA_TRY(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyHostToDevice, ctx->copy));
     CUDA_TRY(cudaEventRecord(t->col_ev[c.bit], ctx->copy));
   }
+  t->tus_host = in->t_us;
+  t->tus_deferred = true;
   t->pending = TC_ALL;
   *out = t;
   return MP_OK;
@@ -141,12 +144,18 @@ extern "C" int mp_trace_upload_async(mp_ctx *ctx, const mp_trace_in *in, mp_dtra
   return trace_upload(ctx, in, out, true, err);
 }
 
+extern "C" int mp_trace_flush(mp_dtrace *t, mp_err *err) { return trace_flush_tus(t->ctx, t, err); }
+
 extern "C" int mp_trace_wait(mp_dtrace *t, mp_err *err) {
+  int rc = trace_flush_tus(t->ctx, t, err);
+  if (rc) return rc;
   if (t->col_ev[4]) CUDA_TRY(cudaEventSynchronize(t->col_ev[4]));
   return MP_OK;
 }
 
 extern "C" int mp_trace_free(mp_dtrace *t) {
+  mp_err e{};
+  trace_flush_tus(t->ctx, t, &e);  // profiles waiting for op times get them
   if (t->col_ev[4]) {
     // buffers are released stream-ordered on the context stream: after the copies
     cudaStreamWaitEvent(t->ctx->stream, t->col_ev[4], 0);
@@ -194,6 +203,12 @@ extern "C" int mp_profile_download(mp_ctx *ctx, mp_dprofile *P, mp_profile_out *
 }
 
 extern "C" int mp_profile_free(mp_dprofile *p) {
+  if (p->times_src) {  // still registered with a deferred timestamp upload
+    auto &w = p->times_src->tus_waiters;
+    for (size_t i = 0; i < w.size(); i++)
+      if (w[i] == p) { w.erase(w.begin() + i); break; }
+    p->times_src = nullptr;
+  }
   if (p->times_ev) {
     // buffers are released stream-ordered on the context stream: after the op times
     cudaStreamWaitEvent(p->ctx->stream, p->times_ev, 0);

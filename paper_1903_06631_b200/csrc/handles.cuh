@@ -1,7 +1,10 @@
 // handles.cuh — device-resident objects behind the opaque C-ABI handles.
 #pragma once
+#include <vector>
 
 #include "common.cuh"
+
+struct mp_dprofile;
 
 struct mp_dtrace {
   mp_ctx *ctx = nullptr;
@@ -26,12 +29,25 @@ struct mp_dtrace {
   // waited for
   cudaEvent_t col_ev[5] = {};
   unsigned pending = 0;
+  // the timestamp column of an asynchronous upload goes up only at
+  // trace_flush_tus (before the placement, which a concurrent H2D copy barely
+  // slows, unlike the readback-bound stages before it); profiles extracted
+  // meanwhile get their op times then
+  const int64_t *tus_host = nullptr;
+  bool tus_deferred = false;
+  std::vector<mp_dprofile *> tus_waiters;
 };
+
+int trace_flush_tus(mp_ctx *ctx, mp_dtrace *t, mp_err *err);
 
 enum { TC_VAR = 1, TC_KIND = 2, TC_SIZE = 4, TC_INDEX = 8, TC_TUS = 16, TC_ALL = 31 };
 
 // order the context stream after the upload of the columns in `mask`
 inline int trace_need(mp_ctx *ctx, mp_dtrace *t, unsigned mask, mp_err *err) {
+  if ((mask & TC_TUS) && t->tus_deferred) {
+    int rc = trace_flush_tus(ctx, t, err);
+    if (rc) return rc;
+  }
   unsigned m = mask & t->pending;
   for (int b = 0; b < 5; b++)
     if (m & (1u << b)) CUDA_TRY(cudaStreamWaitEvent(ctx->stream, t->col_ev[b], 0));
@@ -55,12 +71,18 @@ struct mp_dprofile {
   cudaEvent_t times_ev = nullptr;
   bool times_pending = false;
   DBuf<double> dur;
+  mp_dtrace *times_src = nullptr;  // registered with a deferred timestamp upload
+  int64_t times_start = 0, times_end = 0;
 };
 
 // wait for deferred op times (device order on the context stream, and the
 // period duration on the host)
 inline int profile_times(mp_ctx *ctx, mp_dprofile *P, mp_err *err) {
   if (!P->times_pending) return MP_OK;
+  if (P->times_src) {
+    int rc = trace_flush_tus(ctx, P->times_src, err);
+    if (rc) return rc;
+  }
   CUDA_TRY(cudaStreamWaitEvent(ctx->stream, P->times_ev, 0));
   CUDA_TRY(cudaEventSynchronize(P->times_ev));
   CUDA_TRY(cudaMemcpy(&P->d.duration_us, P->dur.p, 8, cudaMemcpyDeviceToHost));

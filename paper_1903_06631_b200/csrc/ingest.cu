@@ -424,6 +424,35 @@ __global__ void k_ex_times(const int64_t *t_us, int64_t start, int64_t end, doub
   if (blockIdx.x == 0 && threadIdx.x == 0) *dur = ex_duration(t_us, start, end);
 }
 
+// Enqueue the deferred timestamp upload on the copy stream (it starts at
+// once), then the op times of the profiles extracted meanwhile, ordered
+// after their allocations on the context stream.
+int trace_flush_tus(mp_ctx *ctx, mp_dtrace *t, mp_err *err) {
+  if (!t->tus_deferred) return MP_OK;
+  t->tus_deferred = false;
+  if (t->n && t->tus_host)
+    CUDA_TRY(cudaMemcpyAsync(t->t_us.p, t->tus_host, t->n * 8, cudaMemcpyHostToDevice, ctx->copy));
+  CUDA_TRY(cudaEventRecord(t->col_ev[4], ctx->copy));
+  if (!t->tus_waiters.empty()) {
+    cudaEvent_t ready;
+    CUDA_TRY(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(ready, ctx->stream));
+    CUDA_TRY(cudaStreamWaitEvent(ctx->copy, ready, 0));
+    CUDA_TRY(cudaEventDestroy(ready));
+    for (mp_dprofile *P : t->tus_waiters) {
+      const int64_t p = P->times_end - P->times_start;
+      ctx->launches++;
+      k_ex_times<<<grid_for(p, 256), 256, 0, ctx->copy>>>(t->t_us.p, P->times_start, P->times_end, P->op_times.p,
+                                                         P->dur.p);
+      CUDA_TRY(cudaGetLastError());
+      CUDA_TRY(cudaEventRecord(P->times_ev, ctx->copy));
+      P->times_src = nullptr;
+    }
+    t->tus_waiters.clear();
+  }
+  return MP_OK;
+}
+
 __global__ void k_load_diff(int64_t nv, const int32_t *nseg, const int32_t *seg, const int64_t *size,
                             unsigned long long *diff) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
@@ -598,7 +627,17 @@ extern "C" int mp_extract(mp_ctx *ctx, mp_dtrace *t, int64_t start, int64_t end,
   LAUNCH(ctx, k_ex_access, grid_for(nv, 128), 128, 0, t->kind.p, t->perm.p, t->gstart.p, nv, start, end,
          ncarry, s, carry_ord.p, win_ord.p, o);
   double *d_dur = (double *)(ctx->d_small + 3);
-  if (late_times) {
+  if (late_times && t->tus_deferred) {
+    // the timestamps are not on their way yet: trace_flush_tus computes the
+    // op times right behind them
+    CUDA_TRY(P->dur.alloc(1, st));
+    CUDA_TRY(cudaEventCreateWithFlags(&P->times_ev, cudaEventDisableTiming));
+    P->times_pending = true;
+    P->times_src = t;
+    P->times_start = start;
+    P->times_end = end;
+    t->tus_waiters.push_back(P);
+  } else if (late_times) {
     CUDA_TRY(P->dur.alloc(1, st));
     cudaEvent_t ready;
     CUDA_TRY(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));

@@ -88,6 +88,9 @@ def plan_arrays(arrays: TraceArrays, window: tuple[int, int] | None = None,
             dp = N.extract(arrays, window[0], window[1])
             g = N.conflict_from_profile(dp)
             nv, nnz = N.graph_dims(g)
+            if fresh:
+                # the timestamps go up during the placement (see mp_trace_flush)
+                N.trace_flush(dev)
             if keep_on_device:
                 fp, lv = N.plan_pool_device(g, POLICY_CODE[policy])
                 offs = None
