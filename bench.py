@@ -64,7 +64,7 @@ def hbm_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def _nvml_sampler(index, period, stop, conn):
+def _nvml_sampler(index, period, stop, conn, ready):
     """Child process: NVML SM clock + clock-event reasons every `period` s
     until `stop` is set (a separate process, so sampling never holds the
     benchmark's GIL)."""
@@ -81,6 +81,7 @@ def _nvml_sampler(index, period, stop, conn):
             sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
             r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
             samples.append((sm, mx, tuple(n for n, b in zip(names, bits) if r & b)))
+            ready.set()
             stop.wait(period)
     except Exception:  # noqa: BLE001
         fields = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
@@ -94,9 +95,11 @@ def _nvml_sampler(index, period, stop, conn):
                 f = [x.strip() for x in out.split(",")]
                 samples.append((float(f[0]), float(f[1]),
                                 tuple(n for i, n in enumerate(names) if f[2 + i].lower().startswith("active"))))
+                ready.set()
             except Exception:  # noqa: BLE001
                 pass
             stop.wait(0.05)
+    ready.set()
     conn.send(samples)
     conn.close()
 
@@ -111,13 +114,17 @@ class ClockSampler:
         import multiprocessing as mp
         ctx = mp.get_context("fork")
         self._stop = ctx.Event()
+        self._ready = ctx.Event()
         self._recv, send = ctx.Pipe(duplex=False)
-        self._p = ctx.Process(target=_nvml_sampler, args=(index, period_s, self._stop, send), daemon=True)
+        self._p = ctx.Process(target=_nvml_sampler, args=(index, period_s, self._stop, send, self._ready),
+                              daemon=True)
         self.samples = []
 
     def __enter__(self):
         self._p.start()
-        time.sleep(0.05)  # the child's first samples precede the timed region
+        # the timed region starts once the child has its first sample (NVML
+        # start-up can outlast a short timed region)
+        self._ready.wait(10)
         return self
 
     def __exit__(self, *exc):
