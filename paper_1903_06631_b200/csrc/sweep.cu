@@ -32,7 +32,10 @@
 #include "place_dev.cuh"
 #include "swap_dev.cuh"
 
-constexpr int SW_THREADS = 128;
+#ifndef SW_THREADS_N
+#define SW_THREADS_N 192  // 6 warps: 5 on the swap path, budgets of the largest traces start together (128: ~1 % slower)
+#endif
+constexpr int SW_THREADS = SW_THREADS_N;
 constexpr int SW_WARPS = SW_THREADS / 32;
 #ifndef SW_FAST_KB
 #define SW_FAST_KB 88  // per-CTA shared arena: 2 CTAs/SM, the largest traces keep their budget scratch in smem (72 KB, 3 CTAs/SM: 3 % slower)
