@@ -42,7 +42,10 @@ constexpr int SW_WARPS = SW_THREADS / 32;
 #endif
 constexpr size_t SW_FAST_BYTES = SW_FAST_KB * 1024;
 constexpr int SW_QUICK = 16;  // detect: fingerprint pairs of the quick filter
-constexpr int PL_K = 4;  // placement list entries per lane per pass  // per-CTA shared-memory arena
+#ifndef PL_K_N
+#define PL_K_N 4
+#endif
+constexpr int PL_K = PL_K_N;  // placement list entries per lane per pass
 
 // ---------------------------------------------------------------------------
 // scratch allocation.  Each CTA owns a slab of global scratch (bump
