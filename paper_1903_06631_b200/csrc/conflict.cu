@@ -307,6 +307,9 @@ static int build_csr(mp_ctx *ctx, int64_t nv, const int64_t *seg_off_d, const in
   int mm[2];
   memcpy(mm, &h[4], 8);
   if (nv) {
+    // size keys are descending-order encodings: kmin holds the largest size
+    g->size_hi = (int64_t)(~(uint64_t)h[6] ^ 0x8000000000000000ull);
+    g->size_lo = (int64_t)(~(uint64_t)h[7] ^ 0x8000000000000000ull);
     rc = placement_rank_sort(ctx, nv, g->size.p, g->tiekey.p, g->rank.p, (uint64_t)h[6], (uint64_t)h[7], err);
     if (rc) return rc;
   }

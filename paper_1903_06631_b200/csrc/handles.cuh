@@ -102,6 +102,7 @@ struct mp_dgraph {
   DBuf<int32_t> rank;     // position in the placement order (-size, tie)
   DBuf<int32_t> pcnt;     // row prefix holding the placement predecessors
   int64_t arena_need = 0; // scratch ranges for rows longer than 128
+  int64_t size_lo = INT64_MIN, size_hi = INT64_MAX;  // vertex weight range (when the build knows it)
 };
 
 int build_groups(mp_ctx *ctx, mp_dtrace *t, mp_err *err);

@@ -38,6 +38,9 @@
 
 // PLACE_TRACE=1 builds (tools/place_trace.py) record per-variable
 // %globaltimer stamps: placed, claimed, made ready, gathered, sorted.
+#ifndef PLACE_REC
+#define PLACE_REC 1
+#endif
 #ifndef PLACE_TRACE
 #define PLACE_TRACE 0
 #endif
@@ -80,6 +83,7 @@ struct PlaceArgs {
   int32_t *depth;
   int32_t dbg_v;
   unsigned long long *tdone;  // debug (MP_PLACE_TRACE): %globaltimer when each variable was placed
+  longlong2 *rec;       // placed-variable records (k_place_async<true>, see pred_range)
 };
 
 __device__ __forceinline__ int64_t ld_relaxed_s64(const int64_t *p) {
@@ -93,16 +97,36 @@ __device__ __forceinline__ int32_t ld_relaxed_s32(const int32_t *p) {
   return v;
 }
 
-// Offset and level of placed predecessor j.  Both are written once (offset
-// from -1, level from 0) with relaxed stores and the counters carry no
-// release/acquire, so a predecessor counted as placed may not be visible
-// yet — read until it is (a non-sentinel value is final).
-__device__ __forceinline__ void pred_off_level(const PlaceArgs &a, int32_t j, int64_t &s, int &l) {
-  for (;;) {
-    s = ld_relaxed_s64(&a.off[j]);
-    l = ld_relaxed_s32(&a.level[j]);
-    if (s >= 0 && l > 0) break;
-    __nanosleep(32);
+// Range [s, e) and level of placed predecessor j.  Offsets and levels are
+// written once (from -1 / 0 sentinels) with relaxed stores and the counters
+// carry no release/acquire, so a predecessor counted as placed may not be
+// visible yet — read until it is (a non-sentinel value is final).  REC: one
+// 16-byte record {offset, size | level << 32} per variable, written by one
+// store from all-ones (a half not yet visible reads offset -1 or level -1),
+// so the gather is one load per predecessor instead of three; 1.35 vs 1.38
+// ms on config 4.  Used when every size fits 32 bits.
+template <bool REC>
+__device__ __forceinline__ void pred_range(const PlaceArgs &a, int32_t j, int64_t &s, int64_t &e, int &l) {
+  if constexpr (REC) {
+    for (;;) {
+      long long w0, w1;
+      asm volatile("ld.relaxed.gpu.global.v2.s64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(a.rec + j) : "memory");
+      l = (int)(w1 >> 32);
+      if (w0 >= 0 && l > 0) {
+        s = w0;
+        e = w0 + (int64_t)(uint32_t)w1;
+        return;
+      }
+      __nanosleep(32);
+    }
+  } else {
+    for (;;) {
+      s = ld_relaxed_s64(&a.off[j]);
+      l = ld_relaxed_s32(&a.level[j]);
+      if (s >= 0 && l > 0) break;
+      __nanosleep(32);
+    }
+    e = s + a.size[j];
   }
 }
 
@@ -110,7 +134,7 @@ __device__ __forceinline__ void pred_off_level(const PlaceArgs &a, int32_t j, in
 // _pick_offset.  Ranges are sorted as one 64-bit key (start << IB | slot):
 // equal starts may come in any order (the hole scan only sees the running
 // max of ends), so the slot just makes keys unique and carries the end.
-template <int K>
+template <bool REC, int K>
 __device__ __forceinline__ int64_t place_reg(const PlaceArgs &a, int64_t rb, int m, int64_t need, int &lvl,
                                              bool &ok) {
   const int lane = threadIdx.x & 31;
@@ -128,8 +152,7 @@ __device__ __forceinline__ int64_t place_reg(const PlaceArgs &a, int64_t rb, int
       int32_t j = a.col[rb + i];
       int64_t s;
       int l;
-      pred_off_level(a, j, s, l);
-      e[r] = s + a.size[j];
+      pred_range<REC>(a, j, s, e[r], l);
       lv = max(lv, l);
       big |= (uint64_t)s >> (63 - IB) != 0;
       x[r] = ((uint64_t)s << IB) | (uint64_t)i;
@@ -161,7 +184,7 @@ __device__ __forceinline__ int64_t place_reg(const PlaceArgs &a, int64_t rb, int
   return h.found ? h.best_off : h.top;
 }
 
-template <typename P>
+template <bool REC, typename P>
 __device__ int64_t place_mem(const PlaceArgs &a, P buf, int64_t rb, int m, int64_t need, int &lvl) {
   const int lane = threadIdx.x & 31;
   int n2 = 64;
@@ -172,8 +195,7 @@ __device__ int64_t place_mem(const PlaceArgs &a, P buf, int64_t rb, int m, int64
     if (i < m) {
       int32_t j = a.col[rb + i];
       int l;
-      pred_off_level(a, j, x.s, l);
-      x.e = x.s + a.size[j];
+      pred_range<REC>(a, j, x.s, x.e, l);
       lv = max(lv, l);
     }
     buf[i] = x;
@@ -218,6 +240,7 @@ constexpr int PLACE_THREADS = 256;
 
 
 // offset of one variable whose predecessors are all placed (warp-wide)
+template <bool REC>
 __device__ __forceinline__ int64_t place_var(const PlaceArgs &a, int32_t v, int64_t gwarp, int64_t rb, int m,
                                              int64_t need, int &lvl) {
   const int lane = threadIdx.x & 31;
@@ -225,9 +248,9 @@ __device__ __forceinline__ int64_t place_var(const PlaceArgs &a, int32_t v, int6
   bool ok = true;
   lvl = 1;
   if (m == 0) o = 0;
-  else if (m <= 32) o = place_reg<1>(a, rb, m, need, lvl, ok);
-  else if (m <= 64) o = place_reg<2>(a, rb, m, need, lvl, ok);
-  else if (m <= 128) o = place_reg<4>(a, rb, m, need, lvl, ok);
+  else if (m <= 32) o = place_reg<REC, 1>(a, rb, m, need, lvl, ok);
+  else if (m <= 64) o = place_reg<REC, 2>(a, rb, m, need, lvl, ok);
+  else if (m <= 128) o = place_reg<REC, 4>(a, rb, m, need, lvl, ok);
   else ok = false;
   // long rows, or offsets too large to pack: sort (start, end) pairs in
   // global scratch
@@ -240,7 +263,7 @@ __device__ __forceinline__ int64_t place_var(const PlaceArgs &a, int32_t v, int6
       if (lane == 0) at = atomicAdd(a.arena_top, n2);
       buf = a.arena + __shfl_sync(FULL_MASK, at, 0);
     }
-    o = place_mem(a, buf, rb, m, need, lvl);
+    o = place_mem<REC>(a, buf, rb, m, need, lvl);
   }
   return o;
 }
@@ -249,6 +272,7 @@ __device__ __forceinline__ int64_t place_var(const PlaceArgs &a, int32_t v, int6
 // queue in order; placing a variable decrements its successors' counters
 // and the last predecessor to finish publishes the successor.  No grid-wide
 // barrier: a variable starts the moment its last predecessor is placed.
+template <bool REC>
 __global__ void __launch_bounds__(PLACE_THREADS, PLACE_MIN_BLOCKS) k_place_async(PlaceArgs a) {
   const int lane = threadIdx.x & 31;
   int64_t gwarp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -301,13 +325,20 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_MIN_BLOCKS) k_place_async
 #if PLACE_TRACE
     PlaceArgs ad = a;
     ad.dbg_v = v;
-    int64_t o = place_var(ad, v, gwarp, rb, m, need, lvl);
+    int64_t o = place_var<REC>(ad, v, gwarp, rb, m, need, lvl);
 #else
-    int64_t o = place_var(a, v, gwarp, rb, m, need, lvl);
+    int64_t o = place_var<REC>(a, v, gwarp, rb, m, need, lvl);
 #endif
     if (lane == 0) {
-      asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(a.level + v), "r"(lvl) : "memory");
-      asm volatile("st.relaxed.gpu.global.s64 [%0], %1;" ::"l"(a.off + v), "l"(o) : "memory");
+      if constexpr (REC) {
+        long long w1 = (long long)(((uint64_t)(uint32_t)lvl << 32) | (uint64_t)(uint32_t)need);
+        asm volatile("st.relaxed.gpu.global.v2.s64 [%0], {%1, %2};" ::"l"(a.rec + v), "l"(o), "l"(w1) : "memory");
+        a.off[v] = o;
+        if (PLACE_TRACE) a.level[v] = lvl;
+      } else {
+        asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(a.level + v), "r"(lvl) : "memory");
+        asm volatile("st.relaxed.gpu.global.s64 [%0], %1;" ::"l"(a.off + v), "l"(o) : "memory");
+      }
       if (o + need > fp) fp = o + need;
       if (lvl > dmax) dmax = lvl;
       PT_STAMP(0, v);
@@ -598,16 +629,24 @@ extern "C" int mp_plan_pool(mp_ctx *ctx, mp_dgraph *g, int32_t policy, int64_t *
   unsigned long long *d_need = (unsigned long long *)(ctr.p + 6);
   // the conflict build bounded the long-row scratch by degree (no readback)
   uint64_t arena_need = (uint64_t)g->arena_need;
-  static int per_sm_cached = 0;
+  static int per_sm_cached[2] = {0, 0};
   DBuf<int64_t> &off = g->offsets;
   CUDA_TRY(off.alloc(V, st));
-  // sentinels: -1 offsets, level 0 (see pred_off_level)
-  CUDA_TRY(cudaMemsetAsync(off.p, 0xff, V * 8, st));
-  CUDA_TRY(cudaMemsetAsync(level.p, 0, V * 4, st));
+  // sentinels: -1 offsets, level 0 or -1 (see pred_range)
+  DBuf<longlong2> rec;
+  const bool use_rec = PLACE_REC && g->size_lo >= 0 && g->size_hi <= (int64_t)0xffffffffll;
+  if (use_rec) {
+    CUDA_TRY(rec.alloc(V, st));
+    CUDA_TRY(cudaMemsetAsync(rec.p, 0xff, V * 16, st));
+  } else {
+    CUDA_TRY(cudaMemsetAsync(off.p, 0xff, V * 8, st));
+    CUDA_TRY(cudaMemsetAsync(level.p, 0, V * 4, st));
+  }
   size_t smem = 0;
-  if (!per_sm_cached)
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_cached, k_place_async, PLACE_THREADS, smem));
-  int per_sm = per_sm_cached < 1 ? 1 : per_sm_cached;
+  void (*kern)(PlaceArgs) = use_rec ? k_place_async<true> : k_place_async<false>;
+  int &cached = per_sm_cached[use_rec];
+  if (!cached) CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached, kern, PLACE_THREADS, smem));
+  int per_sm = cached < 1 ? 1 : cached;
   if (const char *e = getenv("MP_PLACE_BLOCKS_PER_SM")) per_sm = atoi(e) < per_sm ? atoi(e) : per_sm;  // experiments
   // all warps resident: spinning consumers must never starve producers
   int64_t warps_needed = V;
@@ -621,7 +660,7 @@ extern "C" int mp_plan_pool(mp_ctx *ctx, mp_dgraph *g, int32_t policy, int64_t *
   CUDA_TRY(arena.alloc((int64_t)arena_need, st));
   PlaceArgs a{V, g->row_off.p, g->col.p, g->pcnt.p, g->size.p, off.p, level.p, remaining.p, queue.p,
               ctr.p, ctr.p + 1, ctr.p + 2, policy, wscratch.p, arena.p, (unsigned long long *)(ctr.p + 8), d_fp, ctr.p + 3,
-              0, nullptr};
+              0, nullptr, use_rec ? rec.p : nullptr};
   const char *trace_path = PLACE_TRACE ? getenv("MP_PLACE_TRACE") : nullptr;
   DBuf<unsigned long long> tdone;
   if (trace_path) {
@@ -640,7 +679,8 @@ extern "C" int mp_plan_pool(mp_ctx *ctx, mp_dgraph *g, int32_t policy, int64_t *
              d_need);
     }
     StageTimer ptm(ctx, MP_ST_PLACE);
-    LAUNCH(ctx, k_place_async, (unsigned)nblocks, PLACE_THREADS, smem, a);
+    if (use_rec) LAUNCH(ctx, k_place_async<true>, (unsigned)nblocks, PLACE_THREADS, smem, a);
+    else LAUNCH(ctx, k_place_async<false>, (unsigned)nblocks, PLACE_THREADS, smem, a);
   }
   if (offsets) CUDA_TRY(cudaMemcpyAsync(offsets, off.p, V * 8, cudaMemcpyDeviceToHost, st));
   if (trace_path) {

@@ -107,3 +107,33 @@ def test_plan_arrays_paths_match_oracle(seed):
             plan = plan_arrays(arrays, policy=policy, path=path)
             assert np.array_equal(plan.offsets, offs), (path, policy)
             assert plan.footprint_bytes == foot and plan.peak_bytes == fp.peak_bytes and plan.period == p
+
+
+@pytest.mark.parametrize("seed,wide", [(0, False), (1, True), (2, True)])
+def test_grid_placement_both_record_layouts(seed, wide):
+    """The grid placement gathers predecessors from 16-byte records when every
+    size fits 32 bits and from the offset/level/size arrays otherwise
+    (placement.cu pred_range); both give the oracle's plan.  `wide` scales
+    the sizes past 2^32."""
+    import oracle as orc
+    from paper_1903_06631_b200 import workloads
+    from paper_1903_06631_b200.pipeline import plan_arrays
+    from paper_1903_06631_b200.trace import TraceArrays, as_arrays
+    a = as_arrays(workloads.random_periodic_trace(seed, slots=40, nvars=12, iterations=5))
+    size = np.array(a.size)
+    if wide:
+        size = size * ((1 << 33) // max(1, int(size.max())) + 1)
+        assert size.max() >= 1 << 32
+    else:
+        assert size.max() < 1 << 32
+    arrays = TraceArrays.from_blob(np.array(a.kind), np.array(a.var), size, np.array(a.t_us), a.name_blob, a.name_off)
+    rc, p = orc.detect(arrays)
+    rc, fp = orc.extract(arrays, len(arrays) - p, len(arrays))
+    off, lo, hi = orc.profile_segments(fp)
+    h, _r, _c = orc.conflict(off, lo, hi)
+    rc, offs, foot = orc.plan(h, fp.size, fp.alloc.astype(np.int64), fp.base, fp.name_ralloc(), fp.name_blob,
+                              fp.name_off, 1)
+    orc.graph_free(h)
+    plan = plan_arrays(arrays, policy="best_fit", path="grid")
+    assert np.array_equal(plan.offsets, offs)
+    assert plan.footprint_bytes == foot
