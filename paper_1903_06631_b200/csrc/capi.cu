@@ -45,9 +45,10 @@ extern "C" int mp_ctx_destroy(mp_ctx *c) {
   return MP_OK;
 }
 
-extern "C" int64_t mp_ctx_launches(mp_ctx *c) { return c->launches; }
+extern "C" int64_t mp_ctx_launches(mp_ctx *c) { CTX_GUARD(c); return c->launches; }
 
 extern "C" int mp_ctx_sync(mp_ctx *c, mp_err *err) {
+  CTX_GUARD(c);
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   return MP_OK;
 }
@@ -55,11 +56,13 @@ extern "C" int mp_ctx_sync(mp_ctx *c, mp_err *err) {
 extern "C" void *mp_ctx_stream(mp_ctx *c) { return (void *)c->stream; }
 
 extern "C" int mp_ctx_set_timing(mp_ctx *c, int on) {
+  CTX_GUARD(c);
   c->timing = on != 0;
   return MP_OK;
 }
 
 extern "C" int mp_ctx_timings(mp_ctx *c, double *ms, int64_t *count, mp_err *err) {
+  CTX_GUARD(c);
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   for (int i = 0; i < MP_NSTAGES; i++) { ms[i] = 0.0; count[i] = 0; }
   for (auto &r : c->pending) {
@@ -74,6 +77,7 @@ extern "C" int mp_ctx_timings(mp_ctx *c, double *ms, int64_t *count, mp_err *err
 }
 
 extern "C" int mp_trace_reset(mp_dtrace *t) {
+  CTX_GUARD(t->ctx);
   t->grouped = false;
   t->perm.release();
   t->gstart.release();
@@ -137,16 +141,19 @@ static int trace_upload(mp_ctx *ctx, const mp_trace_in *in, mp_dtrace **out, boo
 }
 
 extern "C" int mp_trace_upload(mp_ctx *ctx, const mp_trace_in *in, mp_dtrace **out, mp_err *err) {
+  CTX_GUARD(ctx);
   return trace_upload(ctx, in, out, false, err);
 }
 
 extern "C" int mp_trace_upload_async(mp_ctx *ctx, const mp_trace_in *in, mp_dtrace **out, mp_err *err) {
+  CTX_GUARD(ctx);
   return trace_upload(ctx, in, out, true, err);
 }
 
-extern "C" int mp_trace_flush(mp_dtrace *t, mp_err *err) { return trace_flush_tus(t->ctx, t, err); }
+extern "C" int mp_trace_flush(mp_dtrace *t, mp_err *err) { CTX_GUARD(t->ctx); return trace_flush_tus(t->ctx, t, err); }
 
 extern "C" int mp_trace_wait(mp_dtrace *t, mp_err *err) {
+  CTX_GUARD(t->ctx);
   int rc = trace_flush_tus(t->ctx, t, err);
   if (rc) return rc;
   if (t->col_ev[4]) CUDA_TRY(cudaEventSynchronize(t->col_ev[4]));
@@ -154,6 +161,7 @@ extern "C" int mp_trace_wait(mp_dtrace *t, mp_err *err) {
 }
 
 extern "C" int mp_trace_free(mp_dtrace *t) {
+  CTX_GUARD(t->ctx);
   mp_err e{};
   trace_flush_tus(t->ctx, t, &e);  // profiles waiting for op times get them
   if (t->col_ev[4]) {
@@ -167,6 +175,7 @@ extern "C" int mp_trace_free(mp_dtrace *t) {
 }
 
 extern "C" int mp_profile_get_dims(mp_dprofile *p, mp_profile_dims *dims) {
+  CTX_GUARD(p->ctx);
   mp_err e{};
   int rc = profile_times(p->ctx, p, &e);
   if (rc) return rc;
@@ -175,6 +184,7 @@ extern "C" int mp_profile_get_dims(mp_dprofile *p, mp_profile_dims *dims) {
 }
 
 extern "C" int mp_profile_download(mp_ctx *ctx, mp_dprofile *P, mp_profile_out *o, mp_err *err) {
+  CTX_GUARD(ctx);
   {
     int rc = profile_times(ctx, P, err);
     if (rc) return rc;
@@ -203,6 +213,7 @@ extern "C" int mp_profile_download(mp_ctx *ctx, mp_dprofile *P, mp_profile_out *
 }
 
 extern "C" int mp_profile_free(mp_dprofile *p) {
+  CTX_GUARD(p->ctx);
   if (p->times_src) {  // still registered with a deferred timestamp upload
     auto &w = p->times_src->tus_waiters;
     for (size_t i = 0; i < w.size(); i++)
@@ -221,6 +232,7 @@ extern "C" int mp_profile_free(mp_dprofile *p) {
 extern "C" int mp_profile_upload(mp_ctx *ctx, const mp_profile_dims *dims, const mp_profile_out *in,
                                  const uint8_t *name_blob, const int64_t *name_off, int32_t nnames,
                                  mp_dprofile **out, mp_err *err) {
+  CTX_GUARD(ctx);
   cudaStream_t st = ctx->stream;
   mp_dprofile *P = new mp_dprofile();
   P->ctx = ctx;
@@ -300,6 +312,7 @@ extern "C" int mp_standardize(const double *x, int64_t n, double *out) {
 
 extern "C" int mp_profile_compute_loads(mp_ctx *ctx, mp_dprofile *P, int64_t *loads, int64_t *peak,
                                         int64_t *peak_index, mp_err *err) {
+  CTX_GUARD(ctx);
   int rc = profile_loads(ctx, P, err);
   if (rc) return rc;
   if (P->d.period) CUDA_TRY(cudaMemcpyAsync(loads, P->loads.p, P->d.period * 8, cudaMemcpyDeviceToHost, ctx->stream));

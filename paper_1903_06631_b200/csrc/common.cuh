@@ -11,6 +11,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <mutex>
 #include <vector>
 
 #include "../../include/memplan_b200.h"
@@ -24,6 +25,10 @@ struct mp_stage_rec {
 };
 
 struct mp_ctx {
+  // every C-ABI entry point that uses the context (its stream, scratch
+  // cells, timing records) or a handle bound to it holds this for the call:
+  // calls from several host threads on one context serialize
+  std::recursive_mutex mu;
   int device = 0;
   int num_sms = 148;
   cudaStream_t stream = nullptr;
@@ -43,6 +48,8 @@ struct mp_ctx {
     return e;
   }
 };
+
+#define CTX_GUARD(c) std::lock_guard<std::recursive_mutex> _ctx_guard((c)->mu)
 
 // RAII: brackets a stage with events on the context stream when timing is on
 struct StageTimer {

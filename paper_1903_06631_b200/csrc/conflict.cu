@@ -14,6 +14,9 @@
 // The CSR may repeat an edge when a variable owns two intervals; plan_pool
 // only looks at the union of neighbour ranges, and the Python adjacency
 // sets deduplicate.
+#include <algorithm>
+#include <utility>
+
 #include "handles.cuh"
 
 constexpr int MAXSEG = 64;
@@ -395,6 +398,7 @@ __global__ void k_prof_segs(int64_t nv, const int32_t *nseg, const int32_t *seg,
 }
 
 extern "C" int mp_conflict_from_profile(mp_ctx *ctx, mp_dprofile *P, mp_dgraph **out, mp_err *err) {
+  CTX_GUARD(ctx);
   cudaStream_t st = ctx->stream;
   int64_t nv = P->d.nvars;
   DBuf<int64_t> so;
@@ -417,6 +421,7 @@ extern "C" int mp_conflict_from_profile(mp_ctx *ctx, mp_dprofile *P, mp_dgraph *
 extern "C" int mp_conflict_from_arcs(mp_ctx *ctx, int32_t nvars, const int64_t *size, const int64_t *tiekey,
                                      const int64_t *seg_off, const int32_t *seg_lo, const int32_t *seg_hi,
                                      mp_dgraph **out, mp_err *err) {
+  CTX_GUARD(ctx);
   cudaStream_t st = ctx->stream;
   int64_t nv = nvars, ns = seg_off[nvars];
   DBuf<int64_t> so;
@@ -443,12 +448,14 @@ extern "C" int mp_conflict_from_arcs(mp_ctx *ctx, int32_t nvars, const int64_t *
 }
 
 extern "C" int mp_graph_dims(mp_dgraph *g, int64_t *nvars, int64_t *nnz) {
+  CTX_GUARD(g->ctx);
   *nvars = g->nvars;
   *nnz = g->nnz;
   return MP_OK;
 }
 
 extern "C" int mp_graph_download(mp_ctx *ctx, mp_dgraph *g, int64_t *row_off, int32_t *col, mp_err *err) {
+  CTX_GUARD(ctx);
   CUDA_TRY(cudaMemcpyAsync(row_off, g->row_off.p, (g->nvars + 1) * 8, cudaMemcpyDeviceToHost, ctx->stream));
   if (g->nnz) CUDA_TRY(cudaMemcpyAsync(col, g->col.p, g->nnz * 4, cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
@@ -456,6 +463,7 @@ extern "C" int mp_graph_download(mp_ctx *ctx, mp_dgraph *g, int64_t *row_off, in
 }
 
 extern "C" int mp_graph_free(mp_dgraph *g) {
+  CTX_GUARD(g->ctx);
   delete g;
   return MP_OK;
 }
@@ -487,10 +495,70 @@ __global__ void k_partition_rows(int64_t V, const int64_t *row_off, const int32_
   }
 }
 
-extern "C" int mp_graph_from_csr(mp_ctx *ctx, int32_t nvars, const int64_t *row_off, const int32_t *col,
+// The device placement counts, per vertex, the neighbours placed before it
+// and is released by each of them, so it needs each row to hold exactly the
+// vertex's earlier-placed neighbours plus the later-placed vertices that
+// list it.  A caller's graph need not be symmetric: the reference reads only
+// adj[i] when placing i (smartpool.py:131-135), so u constrains v iff
+// u in adj[v] and u precedes v.  Rebuild that relation, mirrored, on the
+// host (self loops and duplicates dropped, ids checked).
+static int normalize_host_csr(int64_t nv, const int64_t *row_off, const int32_t *col, const int64_t *size,
+                              const int64_t *tiekey, std::vector<int64_t> &row_out, std::vector<int32_t> &col_out,
+                              mp_err *err) {
+  std::vector<int64_t> pos(nv);
+  {
+    std::vector<int32_t> order(nv);
+    for (int64_t i = 0; i < nv; i++) order[i] = (int32_t)i;
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+      if (size[a] != size[b]) return size[a] > size[b];
+      int64_t ta = tiekey ? tiekey[a] : a, tb = tiekey ? tiekey[b] : b;
+      return ta < tb;
+    });
+    for (int64_t k = 0; k < nv; k++) pos[order[k]] = k;
+  }
+  std::vector<std::pair<int32_t, int32_t>> pairs;
+  pairs.reserve((size_t)row_off[nv] * 2);
+  for (int64_t v = 0; v < nv; v++) {
+    if (row_off[v + 1] < row_off[v]) {
+      mp_set_err(err, MP_E_VALUE, v, row_off[v], row_off[v + 1], "row offsets must be non-decreasing");
+      return MP_E_VALUE;
+    }
+    for (int64_t e = row_off[v]; e < row_off[v + 1]; e++) {
+      int32_t u = col[e];
+      if (u < 0 || u >= nv) {
+        mp_set_err(err, MP_E_VALUE, v, u, e, "list index out of range");
+        return MP_E_VALUE;
+      }
+      if (pos[u] < pos[v]) {
+        pairs.push_back({(int32_t)v, u});
+        pairs.push_back({u, (int32_t)v});
+      }
+    }
+  }
+  std::sort(pairs.begin(), pairs.end());
+  pairs.erase(std::unique(pairs.begin(), pairs.end()), pairs.end());
+  row_out.assign(nv + 1, 0);
+  col_out.resize(pairs.size());
+  for (size_t k = 0; k < pairs.size(); k++) {
+    row_out[pairs[k].first + 1]++;
+    col_out[k] = pairs[k].second;
+  }
+  for (int64_t v = 0; v < nv; v++) row_out[v + 1] += row_out[v];
+  return MP_OK;
+}
+
+extern "C" int mp_graph_from_csr(mp_ctx *ctx, int32_t nvars, const int64_t *row_off_in, const int32_t *col_in,
                                  const int64_t *size, const int64_t *tiekey, mp_dgraph **out, mp_err *err) {
+  CTX_GUARD(ctx);
   cudaStream_t st = ctx->stream;
-  int64_t nv = nvars, nnz = row_off[nvars];
+  int64_t nv = nvars;
+  std::vector<int64_t> row_v;
+  std::vector<int32_t> col_v;
+  int nrc = normalize_host_csr(nv, row_off_in, col_in, size, tiekey, row_v, col_v, err);
+  if (nrc) return nrc;
+  const int64_t *row_off = row_v.data();
+  const int32_t *col = col_v.data();
+  int64_t nnz = row_off[nv];
   mp_dgraph *g = new mp_dgraph();
   g->ctx = ctx;
   g->nvars = nv;

@@ -124,9 +124,10 @@ static int validate_checks(mp_ctx *ctx, mp_dtrace *t, int checks, mp_err *err) {
   return MP_E_INVARIANT;
 }
 
-extern "C" int mp_validate(mp_ctx *ctx, mp_dtrace *t, mp_err *err) { return validate_checks(ctx, t, VC_ALL, err); }
+extern "C" int mp_validate(mp_ctx *ctx, mp_dtrace *t, mp_err *err) { CTX_GUARD(ctx); return validate_checks(ctx, t, VC_ALL, err); }
 
 extern "C" int mp_validate_structure(mp_ctx *ctx, mp_dtrace *t, mp_err *err) {
+  CTX_GUARD(ctx);
   int rc = validate_checks(ctx, t, VC_STRUCT, err);
   // a structural violation may still be preceded by a timestamp one: the
   // full pass decides which comes first
@@ -135,6 +136,7 @@ extern "C" int mp_validate_structure(mp_ctx *ctx, mp_dtrace *t, mp_err *err) {
 }
 
 extern "C" int mp_validate_times(mp_ctx *ctx, mp_dtrace *t, mp_err *err) {
+  CTX_GUARD(ctx);
   return validate_checks(ctx, t, VC_TIMES, err);
 }
 
@@ -299,6 +301,7 @@ __global__ void k_period_quick(const uint8_t *kind, const int64_t *size, int64_t
 }
 
 extern "C" int mp_detect(mp_ctx *ctx, mp_dtrace *t, int64_t *period, mp_err *err) {
+  CTX_GUARD(ctx);
   int64_t n = t->n;
   if (n < 2) {
     mp_set_err(err, MP_E_PERIOD_NOT_FOUND, n, 0, 0, "no period");
@@ -535,6 +538,7 @@ static ProfOut prof_out(mp_dprofile *P) {
 
 extern "C" int mp_extract(mp_ctx *ctx, mp_dtrace *t, int64_t start, int64_t end, mp_dprofile **out,
                           mp_err *err) {
+  CTX_GUARD(ctx);
   int64_t n = t->n;
   if (!(0 <= start && start < end && end <= n)) {
     mp_set_err(err, MP_E_VALUE, start, end, n, "window out of range");
@@ -674,6 +678,7 @@ extern "C" int mp_extract(mp_ctx *ctx, mp_dtrace *t, int64_t start, int64_t end,
 // trace, its op times and period duration from the caller
 extern "C" int mp_extract_times(mp_ctx *ctx, mp_dtrace *t, int64_t start, int64_t end, const double *op_times,
                                 double duration, mp_dprofile **out, mp_err *err) {
+  CTX_GUARD(ctx);
   int rc = mp_extract(ctx, t, start, end, out, err);
   if (rc) return rc;
   mp_dprofile *P = *out;

@@ -610,6 +610,7 @@ int placement_rank_legacy(mp_ctx *ctx, int64_t V, const int64_t *size, const int
 
 extern "C" int mp_plan_pool(mp_ctx *ctx, mp_dgraph *g, int32_t policy, int64_t *offsets, int64_t *footprint,
                             int64_t *levels, mp_err *err) {
+  CTX_GUARD(ctx);
   if (policy != 0 && policy != 1) {
     mp_set_err(err, MP_E_VALUE, 0, policy, 0, "unknown policy");
     return MP_E_VALUE;

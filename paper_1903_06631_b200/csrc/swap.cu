@@ -73,6 +73,7 @@ __global__ void k_compact(int64_t V, const int32_t *flag, const int32_t *pos, co
 
 extern "C" int mp_swap_candidates(mp_ctx *ctx, mp_dprofile *P, int64_t threshold, double bw, double lat,
                                   mp_cands_io *out, mp_err *err) {
+  CTX_GUARD(ctx);
   {
     int rc_t = profile_times(ctx, P, err);
     if (rc_t) return rc_t;
@@ -150,6 +151,7 @@ static LoadView load_view(mp_dprofile *P) { return LoadView{P->d.period, P->load
 
 extern "C" int mp_swap_scores(mp_ctx *ctx, mp_dprofile *P, const mp_cands_io *c, double *doa, double *aoa,
                               double *wdoa, double *swdoa, int32_t *order, double *peaks, mp_err *err) {
+  CTX_GUARD(ctx);
   {
     int rc_t = profile_times(ctx, P, err);
     if (rc_t) return rc_t;
@@ -186,6 +188,7 @@ extern "C" int mp_swap_scores(mp_ctx *ctx, mp_dprofile *P, const mp_cands_io *c,
 
 extern "C" int mp_swap_gap_area(mp_ctx *ctx, mp_dprofile *P, const mp_cands_io *c, const double *loads,
                                 double *area, mp_err *err) {
+  CTX_GUARD(ctx);
   {
     int rc_t = profile_times(ctx, P, err);
     if (rc_t) return rc_t;
@@ -252,6 +255,7 @@ __global__ void __launch_bounds__(512) k_swap_static(LoadView L, CandView c, con
 
 extern "C" int mp_swap_select_static(mp_ctx *ctx, mp_dprofile *P, const mp_cands_io *c, const double *ranked,
                                      int64_t limit, int32_t *sel, int64_t *nsel, mp_err *err) {
+  CTX_GUARD(ctx);
   StageTimer tm(ctx, MP_ST_SWAP);
   cudaStream_t st = ctx->stream;
   CandDev d;
@@ -318,6 +322,7 @@ __global__ void k_planned_peak(LoadView L, CandView c, const int32_t *subset, in
 
 extern "C" int mp_swap_planned_peak(mp_ctx *ctx, mp_dprofile *P, const mp_cands_io *c, const int32_t *subset,
                                     int64_t nsub, double *peak, mp_err *err) {
+  CTX_GUARD(ctx);
   {
     int rc_t = profile_times(ctx, P, err);
     if (rc_t) return rc_t;
@@ -360,6 +365,7 @@ __global__ void k_swap_schedule(CandView c, const int32_t *sel, int64_t n, const
 extern "C" int mp_swap_schedule(mp_ctx *ctx, const mp_cands_io *c, const int32_t *sel, int64_t n,
                                 const double *ready, const double *deadline, double *t_so, double *t_eo,
                                 double *t_si, double *t_ei, int32_t *event_order, mp_err *err) {
+  CTX_GUARD(ctx);
   StageTimer tm(ctx, MP_ST_SWAP);
   cudaStream_t st = ctx->stream;
   CandDev d;
@@ -469,6 +475,7 @@ __global__ void k_sim_delays(ProfView P, const double *actual, double delay_tota
 
 extern "C" int mp_swap_simulate(mp_ctx *ctx, mp_dprofile *P, const mp_cands_io *c, const int32_t *sel, int64_t n,
                                 int64_t limit, int32_t has_limit, int32_t max_rounds, mp_sim_io *io, mp_err *err) {
+  CTX_GUARD(ctx);
   {
     int rc_t = profile_times(ctx, P, err);
     if (rc_t) return rc_t;
@@ -725,6 +732,7 @@ __global__ void __launch_bounds__(128) k_swap_eval_weights(EvalArgs a) {
 extern "C" int mp_swap_eval_weights(mp_ctx *ctx, mp_dprofile *P, const mp_cands_io *c, const double *z,
                                     const double *weights, int64_t m, int64_t limit, int32_t max_rounds,
                                     int32_t *status, double *overhead, int64_t *nsel, int64_t *aux, mp_err *err) {
+  CTX_GUARD(ctx);
   {
     int rc_t = profile_times(ctx, P, err);
     if (rc_t) return rc_t;

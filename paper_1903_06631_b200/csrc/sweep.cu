@@ -1079,6 +1079,7 @@ struct mp_dsweep {
 };
 
 extern "C" int mp_sweep_upload(mp_ctx *ctx, const mp_sweep_in *in, mp_dsweep **out, mp_err *err) {
+  CTX_GUARD(ctx);
   StageTimer tm(ctx, MP_ST_SWEEP);
   cudaStream_t st = ctx->stream;
   int64_t T = in->ntraces;
@@ -1144,11 +1145,13 @@ extern "C" int mp_sweep_upload(mp_ctx *ctx, const mp_sweep_in *in, mp_dsweep **o
 }
 
 extern "C" int mp_sweep_free(mp_dsweep *s) {
+  CTX_GUARD(s->ctx);
   delete s;
   return MP_OK;
 }
 
 extern "C" int mp_sweep_run(mp_ctx *ctx, mp_dsweep *s, const mp_sweep_params *prm, mp_err *err) {
+  CTX_GUARD(ctx);
   StageTimer tm(ctx, MP_ST_SWEEP);
   cudaStream_t st = ctx->stream;
   if (prm->nbudget < 0 || prm->nbudget > MP_SWEEP_MAX_BUDGETS || (prm->policy != 0 && prm->policy != 1)) {
@@ -1185,6 +1188,7 @@ extern "C" int mp_sweep_run(mp_ctx *ctx, mp_dsweep *s, const mp_sweep_params *pr
 
 extern "C" int mp_sweep_download(mp_ctx *ctx, mp_dsweep *s, mp_sweep_trace *traces, mp_sweep_budget *budgets,
                                  int64_t *offsets, int32_t *cand_order, mp_err *err) {
+  CTX_GUARD(ctx);
   StageTimer tm(ctx, MP_ST_SWEEP);
   cudaStream_t st = ctx->stream;
   if (traces && s->T) CUDA_TRY(cudaMemcpyAsync(traces, s->rec.p, s->T * sizeof(mp_sweep_trace), cudaMemcpyDeviceToHost, st));
@@ -1197,6 +1201,7 @@ extern "C" int mp_sweep_download(mp_ctx *ctx, mp_dsweep *s, mp_sweep_trace *trac
 }
 
 extern "C" int mp_sweep_set_profile(mp_ctx *ctx, mp_dsweep *s, int on, mp_err *err) {
+  CTX_GUARD(ctx);
   if (!on) { s->prof.release(); return MP_OK; }
   CUDA_TRY(s->prof.alloc(s->T * 16 > 0 ? s->T * 16 : 1, ctx->stream));
   CUDA_TRY(cudaMemsetAsync(s->prof.p, 0, (s->T * 16 > 0 ? s->T * 16 : 1) * 8, ctx->stream));
@@ -1204,6 +1209,7 @@ extern "C" int mp_sweep_set_profile(mp_ctx *ctx, mp_dsweep *s, int on, mp_err *e
 }
 
 extern "C" int mp_sweep_profile_download(mp_ctx *ctx, mp_dsweep *s, long long *out, mp_err *err) {
+  CTX_GUARD(ctx);
   if (!s->prof.p) { mp_set_err(err, MP_E_VALUE, 0, 0, 0, "profiling is off"); return MP_E_VALUE; }
   CUDA_TRY(cudaMemcpyAsync(out, s->prof.p, s->T * 16 * 8, cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));

@@ -62,6 +62,21 @@ class DetectedIteration:
 
 
 _LAZY = ("variables", "load", "op_times_us", "events", "op_instance")
+# the fields a device profile is built from (``events`` is not uploaded)
+_DEVICE_FIELDS = ("variables", "load", "op_times_us", "op_instance")
+_SCALARS = ("period", "window", "period_duration_us")
+
+
+def _freeze(name, value):
+    """Value snapshot of a profile field, for in-place edit detection."""
+    if value is None:
+        return None
+    if name == "variables":
+        return tuple((v.var, v.base_var, v.size, v.alloc_index, v.free_index, tuple(v.segments),
+                      tuple(v.accesses), v.persistent, v.wraps) for v in value)
+    if name == "load":
+        return (tuple(value.loads), value.peak_bytes, value.peak_index)
+    return tuple(value)
 
 
 class IterationProfile:
@@ -118,17 +133,42 @@ class IterationProfile:
         if name in _LAZY and name in self.__dict__.get("_pending", ()):
             value = self._materialize(name)
             self.__dict__[name] = value
+            if name in _DEVICE_FIELDS:
+                # the device copy stays valid while this value is unedited
+                self.__dict__.setdefault("_sig", {})[name] = _freeze(name, value)
             return value
         raise AttributeError(name)
 
+    def _materialize_all(self, skip=None) -> None:
+        """Build every still-lazy field (but ``skip``) from the current
+        device columns."""
+        for name in self.__dict__.get("_pending", ()):
+            if name != skip and name not in self.__dict__:
+                getattr(self, name)
+
+    def _drop_device(self, skip=None) -> None:
+        d = self.__dict__
+        if d.get("_dev") is not None or d.get("_flat") is not None:
+            self._materialize_all(skip)
+        d["_dev"] = None
+        d["_flat"] = None
+        d["_sig"] = {}
+
     def __setattr__(self, name, value):
-        if name in _LAZY:
+        if name in _LAZY or (name in _SCALARS and self.__dict__.get("_dev") is not None):
+            # a user edit invalidates the device copy (the other lazy
+            # fields are built from it first)
+            self._drop_device(skip=name)
             self.__dict__[name] = value
-            # a user edit invalidates the device copy
-            self.__dict__["_dev"] = None
-            self.__dict__["_flat"] = None
             return
         object.__setattr__(self, name, value)
+
+    def _device_stale(self) -> bool:
+        """True when a field the device copy was built from has been edited
+        in place since (the reference reads the fields on every call)."""
+        sig = self.__dict__.get("_sig") or {}
+        return any(name in self.__dict__ and _freeze(name, self.__dict__[name]) != frozen
+                   for name, frozen in sig.items())
 
     def _materialize(self, name):
         fp = self._flat_profile()
@@ -261,11 +301,15 @@ def _flatten(profile: IterationProfile) -> FlatProfile:
 
 
 def device_profile(profile: IterationProfile):
-    """Device handle of a profile (uploading a Python-built one once)."""
+    """Device handle of a profile: the extracted one, or an upload of the
+    Python fields — redone whenever a field was edited in place since."""
+    if profile._dev is not None and profile._device_stale():
+        profile._drop_device()
     if profile._dev is None:
         fp = profile._flat_profile()
         profile.__dict__["_dev"] = N.upload_profile(fp)
         profile.__dict__["_dims"] = fp.dims()
+        profile.__dict__["_sig"] = {name: _freeze(name, profile.__dict__.get(name)) for name in _DEVICE_FIELDS}
     return profile._dev
 
 

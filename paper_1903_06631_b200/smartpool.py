@@ -14,6 +14,7 @@ import numpy as np
 
 from . import _native as N
 from .errors import GraphTooLarge, MemplanError, MissingVariable
+from ._abi import F_PERSISTENT
 from .iteration import IterationProfile, Segment, device_profile
 
 POLICY_CODE = {"first_fit": 0, "best_fit": 1}
@@ -28,8 +29,22 @@ class PoolVar:
     persistent: bool
 
 
+def _freeze_vars(vars_):
+    return None if vars_ is None else tuple((pv.var, pv.size, pv.alloc_index) for pv in vars_)
+
+
+def _freeze_adj(adj):
+    return None if adj is None else tuple(frozenset(a) for a in adj)
+
+
 class ConflictGraph:
-    """Weighted interval-conflict graph (smartpool.py:28-33)."""
+    """Weighted interval-conflict graph (smartpool.py:28-33).
+
+    ``vars`` and ``adj`` are plain mutable Python containers, as in the
+    reference; the device CSR built from (or uploaded for) them is reused
+    only while the values it was built from compare equal, so an in-place
+    edit (``g.adj[i].add(j)``, ``g.vars[k].size = ...``) is planned as the
+    reference would plan it."""
 
     def __init__(self, period: int, vars: list[PoolVar] | None = None, adj: list[set[int]] | None = None,
                  peak_load_bytes: int = 0):
@@ -38,6 +53,7 @@ class ConflictGraph:
         self._vars = vars
         self._adj = adj
         self._dev = None
+        self._sig = {}        # frozen vars/adj the device CSR was built from
         self._vars_fn = None  # builds PoolVar list on demand
         self._nv = len(vars) if vars is not None else 0
 
@@ -45,10 +61,13 @@ class ConflictGraph:
     def vars(self) -> list[PoolVar]:
         if self._vars is None and self._vars_fn is not None:
             self._vars = self._vars_fn()
+            if self._dev is not None:
+                self._sig["vars"] = _freeze_vars(self._vars)
         return self._vars
 
     @vars.setter
     def vars(self, value):
+        self.adj  # noqa: B018  (materialize the other half before the device copy goes)
         self._vars = value
         self._dev = None
 
@@ -59,12 +78,19 @@ class ConflictGraph:
             c = col.tolist()
             r = row.tolist()
             self._adj = [set(c[r[i]:r[i + 1]]) for i in range(len(r) - 1)]
+            self._sig["adj"] = _freeze_adj(self._adj)
         return self._adj
 
     @adj.setter
     def adj(self, value):
+        self.vars  # noqa: B018
         self._adj = value
         self._dev = None
+
+    def _device_stale(self) -> bool:
+        return ((self._adj is not None and "adj" in self._sig and _freeze_adj(self._adj) != self._sig["adj"])
+                or (self._vars is not None and "vars" in self._sig
+                    and _freeze_vars(self._vars) != self._sig["vars"]))
 
     @property
     def nvars(self) -> int:
@@ -160,41 +186,81 @@ def conflict_graph_from_arcs(period: int, arcs, peak_load_bytes: int) -> Conflic
     g._dev = N.conflict_from_arcs([pv.size for pv in pool_vars] or [0], tie if n else np.zeros(1, np.int64),
                                   seg_off, lo, hi)
     g._nv = n
+    g._sig = {"vars": _freeze_vars(pool_vars)}
     g._names = [pv.var for pv in pool_vars]
     g._sizes = np.array([pv.size for pv in pool_vars], np.int64)
     return g
 
 
 def build_conflict_graph(profile: IterationProfile) -> ConflictGraph:
-    """Conflict graph of a profile's lifetimes (smartpool.py:82-88)."""
+    """Conflict graph of a profile's lifetimes (smartpool.py:82-88).
+
+    Like the reference's, the graph is a snapshot: its ``vars`` come from the
+    device profile the CSR was built from, not from later edits of
+    ``profile``."""
     dp = device_profile(profile)
     g = ConflictGraph(period=profile.period, vars=None, adj=None, peak_load_bytes=profile.peak_bytes)
     g._dev = N.conflict_from_profile(dp)
-    fp = profile._flat_profile
     g._nv = int(dp.dims().nvars)
-    g._profile = profile
+    arrays, window = profile._arrays, profile.window
+    # a Python-built profile was flattened to upload it; an extracted one
+    # downloads its columns from this handle when first needed
+    snap = {} if profile._flat is None else {"fp": profile._flat}
+
+    def fp():
+        if "fp" not in snap:
+            own = profile.__dict__.get("_flat")
+            if own is not None and profile.__dict__.get("_dev") is dp:
+                snap["fp"] = own
+            else:
+                snap["fp"] = N.download_profile(dp, arrays.names, arrays.name_blob, arrays.name_off, window)
+        return snap["fp"]
 
     def make_vars():
-        return [PoolVar(v.var, v.size, v.alloc_index if v.alloc_index is not None else -1, v.segments,
-                        v.persistent) for v in profile.variables]
+        f = fp()
+        seg, nseg, persistent = f.seg.tolist(), f.nseg.tolist(), (f.flags & F_PERSISTENT).tolist()
+        return [PoolVar(name, size, alloc, tuple((seg[4 * i + 2 * k], seg[4 * i + 2 * k + 1])
+                                                 for k in range(nseg[i])), bool(persistent[i]))
+                for i, (name, size, alloc) in enumerate(zip(f.var_names(), f.size.tolist(), f.alloc.tolist()))]
     g._vars_fn = make_vars
     g._names_fn = lambda: fp().var_names()
     g._sizes_fn = lambda: fp().size
     return g
 
 
+def _host_csr(vars_, adj):
+    """CSR of a Python adjacency as the reference indexes it: rows beyond
+    ``len(vars)`` are never read, negative ids index from the end, an id
+    outside the list raises IndexError (smartpool.py:131-135).  The library
+    mirrors the relation by placement order (mp_graph_from_csr)."""
+    n = len(vars_)
+    if len(adj) < n:
+        raise IndexError("list index out of range")
+    rows = [a if isinstance(a, (set, frozenset, list, tuple)) else list(a) for a in adj[:n]]
+    row = np.zeros(n + 1, np.int64)
+    row[1:] = np.cumsum([len(a) for a in rows]) if n else []
+    col = np.fromiter((j for a in rows for j in a), np.int64, count=int(row[-1]))
+    if col.size and (col.min() < -n or col.max() >= n):
+        raise IndexError("list index out of range")
+    col = np.where(col < 0, col + n, col).astype(np.int32)
+    return row, (col if col.size else np.zeros(1, np.int32))
+
+
 def _graph_device(graph: ConflictGraph):
-    """Device CSR of a graph (uploading a hand-built one)."""
+    """Device CSR of a graph: the one built on the device, or an upload of
+    the Python containers — redone after any in-place edit."""
+    if graph._dev is not None and graph._device_stale():
+        graph.vars, graph.adj  # noqa: B018  (both halves on the host)
+        graph._dev = None
     if graph._dev is None:
         vars_ = graph.vars
         adj = graph.adj
         n = len(vars_)
-        row = np.zeros(n + 1, np.int64)
-        row[1:] = np.cumsum([len(a) for a in adj]) if n else []
-        col = np.array([j for a in adj for j in sorted(a)] or [0], np.int32)
+        row, col = _host_csr(vars_, adj)
         tie = _tie_ranks([pv.alloc_index for pv in vars_], [pv.var for pv in vars_])
         graph._dev = N.graph_from_csr(row, col, [pv.size for pv in vars_] or [0], tie if n else np.zeros(1, np.int64))
         graph._nv = n
+        graph._sig = {"vars": _freeze_vars(vars_), "adj": _freeze_adj(adj)}
     return graph._dev
 
 

@@ -5,7 +5,7 @@ same ``EventKind``/``TraceEvent``/``Trace`` types, the JSONL/CSV formats
 with identical error lines, and ``validate_trace``.  What is new is
 ``TraceArrays``: the columnar layout every device kernel consumes
 (``kind u8 | var i32 | size i64 | t_us i64``, 21 B/event), built once per
-trace and cached on the ``Trace`` object.
+trace and cached on the ``Trace`` object while its events are unchanged.
 
 Variable ids are interned in *lexicographic order of the name strings*, so
 an id comparison is a name comparison (Python ``str`` order is code-point
@@ -170,20 +170,33 @@ def _events_to_arrays(events: Sequence[TraceEvent]) -> TraceArrays:
                                     None if contiguous else index)
 
 
+def _remember(trace: Trace, arrays: TraceArrays) -> None:
+    """Cache the columnar form on a Trace together with a snapshot of its
+    event list.  Events are frozen, so the list holding the same event
+    objects (or equal ones) in the same order means the same columns."""
+    trace.__dict__["_mp_arrays"] = (list(trace.events), arrays)
+
+
 def as_arrays(trace) -> TraceArrays:
-    """Columnar view of a Trace (cached on the object) or TraceArrays."""
+    """Columnar view of a Trace or TraceArrays.
+
+    The reference re-reads ``trace.events`` on every call (trace.py:55-84,
+    iteration.py:93-301), so a cached column set is reused only while the
+    event list still compares equal to the snapshot taken with it — list
+    equality short-circuits on identical elements, so the check is a C-speed
+    pointer walk; any in-place edit, append or replacement rebuilds."""
     if isinstance(trace, TraceArrays):
         return trace
-    events = trace.events if isinstance(trace, Trace) else list(trace)
-    key = (id(events), len(events))
     if isinstance(trace, Trace):
         cached = trace.__dict__.get("_mp_arrays")
-        if cached is not None and cached[0] == key:
+        events = trace.events
+        if cached is not None and type(events) is list and cached[0] == events:
             return cached[1]
-    arrays = _events_to_arrays(events)
-    if isinstance(trace, Trace):
-        trace.__dict__["_mp_arrays"] = (key, arrays)
-    return arrays
+        arrays = _events_to_arrays(events)
+        if type(events) is list:
+            _remember(trace, arrays)
+        return arrays
+    return _events_to_arrays(list(trace))
 
 
 def validate_trace(events: Iterable[TraceEvent]) -> None:
@@ -362,7 +375,7 @@ def parse_trace(data: bytes | str, format: str = "jsonl") -> Trace:
         raise ValueError(f"unknown format {format!r}")
     arrays = read_trace_arrays(data, format)
     trace = arrays.to_trace()
-    trace.__dict__["_mp_arrays"] = ((id(trace.events), len(trace.events)), arrays)
+    _remember(trace, arrays)
     validate_trace(trace)
     return trace
 
