@@ -20,6 +20,13 @@
  *   - all floating point is IEEE binary64 with no contraction (-fmad=false)
  *     and the reference's left-fold order, so results are bit-identical.
  *   - kind codes: 0 malloc, 1 free, 2 read, 3 write (trace.py:24-28).
+ *   - threads: the reference's functions are reentrant.
+ *     Every entry point that takes a context, or a handle (bound to the
+ *     context that created it), holds that context's mutex for the call, so
+ *     calls from several host threads on one context serialize and never
+ *     share scratch; for parallel device work use one context per thread.
+ *   - the plan-serving allocator and swap-copy hooks are declared in
+ *     memplan_alloc.h (libmemplan_alloc.so).
  */
 #ifndef MEMPLAN_B200_H
 #define MEMPLAN_B200_H

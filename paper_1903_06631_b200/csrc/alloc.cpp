@@ -19,6 +19,8 @@
 #include <unordered_map>
 #include <vector>
 
+#include "../../include/memplan_alloc.h"
+
 namespace {
 
 constexpr int64_t ALIGN = 512;
@@ -47,10 +49,15 @@ struct State {
   int64_t iteration = 0;
   std::vector<int64_t> clash_log;                  // (iteration, ordinal, other) triples
   int64_t cur_bytes = 0, peak_bytes = 0;  // passthrough bytes live
-  // address ranges of pools replaced by a later plan: blocks served from
-  // them may still be referenced (e.g. gradients freed by the next
-  // iteration's zero_grad); their frees are no-ops
-  std::vector<std::pair<int64_t, int64_t>> retired;
+  // pools replaced by a later plan while blocks served from them were still
+  // referenced (e.g. gradients freed by the next iteration's zero_grad):
+  // each stays mapped until its last block is freed, so no later
+  // allocation can reuse the address range under a live tensor
+  struct Retired {
+    int64_t base, bytes;
+    std::unordered_map<int64_t, int64_t> live;  // offset -> size
+  };
+  std::vector<Retired> retired;
   // offsets of swapped-out blocks: PyTorch still holds their pointers, so
   // no other block may be served at the same address while they are out
   std::unordered_map<int64_t, int64_t> swapped_out;
@@ -120,17 +127,29 @@ void mp_torch_free(void *ptr, ssize_t size, int device, cudaStream_t stream) {
   (void)device;
   if (s.logging) s.log.push_back({s.seq, 1, (int64_t)ptr, 0});
   char *c = (char *)ptr;
+  const int64_t a = (int64_t)c;
+  // retired pools first: their ranges are still mapped, so no current
+  // block can lie inside one
+  for (size_t r = 0; r < s.retired.size(); r++) {
+    auto &rp = s.retired[r];
+    if (a >= rp.base && a < rp.base + rp.bytes) {
+      rp.live.erase(a - rp.base);
+      if (rp.live.empty()) {
+        cudaFree((void *)rp.base);  // synchronizes: pending work on the block is done
+        s.retired.erase(s.retired.begin() + r);
+      }
+      return;
+    }
+  }
   if (s.pool && c >= s.pool && c < s.pool + s.pool_bytes) {  // pool slots are static
-    s.pool_live.erase((int64_t)(c - s.pool));
+    s.pool_live.erase(a - (int64_t)s.pool);
+    s.swapped_out.erase(a - (int64_t)s.pool);
     return;
   }
-  auto it = s.live.find((int64_t)ptr);
+  auto it = s.live.find(a);
   if (it != s.live.end()) {
     s.cur_bytes -= it->second;
     s.live.erase(it);
-  } else {
-    for (auto &r : s.retired)
-      if ((int64_t)c >= r.first && (int64_t)c < r.first + r.second) return;
   }
   cudaFreeAsync(ptr, stream);
 }
@@ -158,8 +177,12 @@ int mp_alloc_set_plan(int64_t pool_bytes, int64_t n, const int64_t *off, const i
   State &s = S();
   std::lock_guard<std::mutex> g(s.mu);
   if (s.pool) {
-    cudaFree(s.pool);
-    s.retired.push_back({(int64_t)s.pool, s.pool_bytes});
+    // blocks PyTorch still holds (served or swapped out) keep the old pool
+    // mapped; an unreferenced pool goes back to the driver now
+    State::Retired rp{(int64_t)s.pool, s.pool_bytes, std::move(s.pool_live)};
+    for (auto &kv : s.swapped_out) rp.live[kv.first] = kv.second;
+    if (rp.live.empty()) cudaFree(s.pool);
+    else s.retired.push_back(std::move(rp));
   }
   s.pool = nullptr;
   s.pool_bytes = pool_bytes;
@@ -199,6 +222,7 @@ void mp_alloc_stats(int64_t *out) {
   out[5] = s.ordinal;
   out[7] = (int64_t)s.pool_live.size();
   out[8] = s.aliases;
+  out[9] = (int64_t)s.retired.size();
 }
 // swap executor: a swapped-out block's bytes are free for the planned
 // co-tenants until it is swapped back in

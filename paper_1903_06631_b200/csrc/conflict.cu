@@ -67,11 +67,38 @@ __global__ void k_norm_count(int64_t nv, const int64_t *seg_off, const int32_t *
       continue;
     }
     if constexpr (GENERAL) {
+    if (s1 - s0 > MAXSEG) {
+      // many segments: walk the chain a_0 = min lo, e_i = min{hi > a_i},
+      // a_{i+1} = min{lo >= e_i} straight from global memory (the same
+      // intervals as the sorted pass below, O(m) reads per interval)
+      int64_t out = write ? eoff[v] : 0, c = 0;
+      int64_t want = INT64_MIN;  // next start must be >= want
+      for (;;) {
+        int64_t a = INT64_MAX;
+        for (int64_t s = s0; s < s1; s++)
+          if (hi[s] > lo[s] && lo[s] >= want && lo[s] < a) a = lo[s];
+        if (a == INT64_MAX) break;
+        int32_t ne = INT32_MAX;
+        for (int64_t s = s0; s < s1; s++)
+          if (hi[s] > lo[s] && hi[s] > a && hi[s] < ne) ne = hi[s];
+        if (write) {
+          ea[out + c] = (int32_t)a;
+          eb[out + c] = ne;
+          ivar[out + c] = (int32_t)v;
+        } else {
+          lmin = min(lmin, (int32_t)a);
+          lmax = max(lmax, ne);
+        }
+        c++;
+        want = ne;
+      }
+      if (!write) ecnt[v] = c;
+      continue;
+    }
     int32_t L[MAXSEG], H[MAXSEG];
     int m = 0;
     for (int64_t s = s0; s < s1; s++) {
       if (hi[s] <= lo[s]) continue;  // empty segments never enter the sweep
-      if (m == MAXSEG) { *overflow = 1; break; }
       // insertion sort by lo
       int j = m++;
       while (j > 0 && L[j - 1] > lo[s]) { L[j] = L[j - 1]; H[j] = H[j - 1]; j--; }

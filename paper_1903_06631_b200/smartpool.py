@@ -179,8 +179,16 @@ def conflict_graph_from_arcs(period: int, arcs, peak_load_bytes: int) -> Conflic
     n = len(pool_vars)
     seg_off = np.zeros(n + 1, np.int64)
     seg_off[1:] = np.cumsum([len(pv.segments) for pv in pool_vars]) if n else []
-    lo = np.array([s[0] for pv in pool_vars for s in pv.segments] or [0], np.int32)
-    hi = np.array([s[1] for pv in pool_vars for s in pv.segments] or [0], np.int32)
+    lo = [s[0] for pv in pool_vars for s in pv.segments] or [0]
+    hi = [s[1] for pv in pool_vars for s in pv.segments] or [0]
+    try:
+        lo, hi = np.array(lo, np.int32), np.array(hi, np.int32)
+    except OverflowError:
+        # the sweep only compares bounds (smartpool.py:57-77): rank them
+        pts = sorted(set(lo) | set(hi))
+        rank = {x: r for r, x in enumerate(pts)}
+        lo = np.array([rank[x] for x in lo], np.int32)
+        hi = np.array([rank[x] for x in hi], np.int32)
     tie = _tie_ranks([pv.alloc_index for pv in pool_vars], [pv.var for pv in pool_vars])
     g = ConflictGraph(period=period, vars=pool_vars, adj=None, peak_load_bytes=peak_load_bytes)
     g._dev = N.conflict_from_arcs([pv.size for pv in pool_vars] or [0], tie if n else np.zeros(1, np.int64),

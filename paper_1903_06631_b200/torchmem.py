@@ -49,11 +49,11 @@ def install():
 
 
 def stats() -> dict:
-    out = (C.c_int64 * 9)()
+    out = (C.c_int64 * 10)()
     ctl().mp_alloc_stats(out)
     return {"hits": out[0], "misses": out[1], "pool_bytes": out[2], "outside_live_bytes": out[3],
             "outside_peak_bytes": out[4], "ordinal": out[5], "conflicts": out[6], "pool_live_blocks": out[7],
-            "swap_alias_fallbacks": out[8]}
+            "swap_alias_fallbacks": out[8], "retired_pools_mapped": out[9]}
 
 
 class Tracer:

@@ -178,6 +178,34 @@ def graph_asymmetric(m):
     return obs
 
 
-PROGRAMS = {f.__name__: f for f in (trace_replace_event, trace_break_invariant, trace_append_window,
+def _arcs_random(seed, nvars, max_segs, span, offset=0):
+    import random
+    rng = random.Random(seed)
+    arcs = []
+    for i in range(nvars):
+        segs = []
+        for _ in range(rng.choice([1, 2, max_segs // 2, max_segs])):
+            lo = rng.randrange(span)
+            segs.append((offset + lo, offset + lo + rng.choice([0, 1, 2, rng.randrange(1, span // 4 + 2)])))
+        arcs.append((f"a{i:03d}", rng.randrange(1, 1 << 20), rng.randrange(-1, 40), tuple(segs), rng.random() < 0.1))
+    return arcs
+
+
+def _arcs_graph(m, arcs):
+    g = m.conflict_graph_from_arcs(64, arcs, 1 << 22)
+    return [["adj", [sorted(a) for a in g.adj]], ["plan", _plans(m, g)]]
+
+
+def arcs_many_segments(m):
+    """Variables with up to 300 (self-overlapping, some empty) segments."""
+    return _arcs_graph(m, _arcs_random(23, 40, 300, 4000))
+
+
+def arcs_large_bounds(m):
+    """Segment bounds far outside 32 bits."""
+    return _arcs_graph(m, _arcs_random(29, 60, 6, 1000, offset=(1 << 40) - 500))
+
+
+PROGRAMS = {f.__name__: f for f in (arcs_many_segments, arcs_large_bounds, trace_replace_event, trace_break_invariant, trace_append_window,
                                      profile_edit_sizes, profile_edit_segments, graph_edit_adj,
                                      graph_asymmetric)}

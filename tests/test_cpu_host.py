@@ -15,8 +15,12 @@ HEADER = os.path.join(ROOT, "include", "memplan_b200.h")
 LIB = os.path.join(ROOT, "paper_1903_06631_b200", "libmemplan_b200.so")
 
 
-def _declared():
-    text = open(HEADER).read()
+ALLOC_HEADER = os.path.join(ROOT, "include", "memplan_alloc.h")
+ALLOC_LIB = os.path.join(ROOT, "paper_1903_06631_b200", "libmemplan_alloc.so")
+
+
+def _declared(header=HEADER):
+    text = open(header).read()
     return sorted(set(re.findall(r"^(?:const )?(?:int|void|int64_t)\s*\*?\s*(mp_[a-z0-9_]+)\s*\(", text, re.M)))
 
 
@@ -29,6 +33,21 @@ def test_library_exports_every_declared_symbol():
     assert not missing, missing
     assert lib.mp_version() == 1
     assert len(_declared()) >= 30
+
+
+def test_allocator_exports_every_declared_symbol():
+    if not os.path.exists(ALLOC_LIB):
+        subprocess.run(["make", "-s", "-j8", "-C", os.path.join(ROOT, "paper_1903_06631_b200", "csrc")], check=True)
+    import ctypes
+    lib = ctypes.CDLL(ALLOC_LIB)
+    declared = _declared(ALLOC_HEADER)
+    assert {"mp_torch_alloc", "mp_torch_free", "mp_alloc_set_plan", "mp_alloc_mode"} <= set(declared)
+    missing = [s for s in declared if not hasattr(lib, s)]
+    assert not missing, missing
+    # and nothing exported that the header does not declare
+    out = subprocess.run(["nm", "-D", "--defined-only", ALLOC_LIB], capture_output=True, text=True).stdout
+    exported = {ln.split()[-1] for ln in out.splitlines() if " T mp_" in ln}
+    assert exported == set(declared), exported ^ set(declared)
 
 
 def test_library_is_sm100a():
