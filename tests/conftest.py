@@ -13,3 +13,7 @@ for p in (ROOT, os.path.join(ROOT, "tests"), os.path.join(ROOT, "oracle")):
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
     config.addinivalue_line("markers", "slow: long-running parity sweep")
+
+# the reference's own suite is run by test_gpu_reference_suite.py in a child
+# pytest (its `conftest` module would shadow this one)
+collect_ignore = ["reference_suite"]
