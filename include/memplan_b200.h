@@ -433,6 +433,16 @@ int mp_reader_copy(mp_reader *r, uint8_t *kind, int32_t *var, int64_t *size, int
                    int64_t *line, uint8_t *name_blob, int64_t *name_off, int64_t *slow_lines);
 int mp_reader_free(mp_reader *r);
 
+/* ---- host-side small-instance oracle ------------------------------------ */
+
+/* brute_force_optimal_footprint's search (smartpool.py:167-221), host code:
+ * n variables in placement order with sizes size[k]; nb[nb_off[k]..nb_off[k+1])
+ * the positions j < k of k's conflicting variables; cand[0..ncand) the
+ * sorted subset sums of the sizes; *best in = the best-fit footprint, out =
+ * the minimum found (search stops at the first layout <= lower). */
+int mp_brute_force_footprint(int32_t n, const int64_t *size, const int64_t *nb_off, const int32_t *nb,
+                             const int64_t *cand, int64_t ncand, int64_t lower, int64_t *best);
+
 #ifdef __cplusplus
 }
 #endif

@@ -325,14 +325,26 @@ def brute_force_optimal_footprint(graph: ConflictGraph, max_vars: int = 10) -> i
     best = plan_pool(graph, "best_fit").footprint_bytes
     if best <= lower:
         return best
-    order = sorted(range(n), key=lambda i: (-graph.vars[i].size, graph.vars[i].alloc_index, graph.vars[i].var))
-    sizes = [graph.vars[i].size for i in order]
+    vars_, adj = graph.vars, graph.adj
+    order = sorted(range(n), key=lambda i: (-vars_[i].size, vars_[i].alloc_index, vars_[i].var))
+    sizes = [vars_[i].size for i in order]
     pos = {v: k for k, v in enumerate(order)}
-    earlier = [[pos[j] for j in graph.adj[order[k]] if pos[j] < k] for k in range(n)]
+    earlier = [[pos[j] for j in adj[order[k]] if pos[j] < k] for k in range(n)]
     sums = {0}
     for s in sizes:
         sums |= {x + s for x in sums}
     cands = sorted(sums)
+    if cands[-1] < (1 << 62) and min(sizes) >= 0:
+        # the DFS in host C++ (csrc/brute.cpp), same order and cut-offs
+        import ctypes as C
+        nb_off = np.zeros(n + 1, np.int64)
+        nb_off[1:] = np.cumsum([len(e) for e in earlier])
+        nb = np.array([j for e in earlier for j in e] or [0], np.int32)
+        sz, cd = np.array(sizes, np.int64), np.array(cands, np.int64)
+        out = C.c_int64(best)
+        N.lib().mp_brute_force_footprint(C.c_int32(n), N.ptr(sz), N.ptr(nb_off), N.ptr(nb), N.ptr(cd),
+                                         C.c_int64(len(cands)), C.c_int64(lower), C.byref(out))
+        return int(out.value)
     offs = [0] * n
 
     def search(k: int, top: int) -> bool:

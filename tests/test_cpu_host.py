@@ -143,3 +143,53 @@ def test_workload_builders_shapes():
     assert len(acts) == len(wts) == 50
     acts, wts = workloads.vgg16_layers(64)
     assert len(acts) == 21
+
+
+def test_brute_force_search_host_c_matches_python():
+    """mp_brute_force_footprint (csrc/brute.cpp) is the reference's DFS
+    (smartpool.py:188-221) step for step: same result on random small
+    graphs, from the same starting bound."""
+    import ctypes as C
+    import random
+
+    from paper_1903_06631_b200 import _native as N
+
+    def py_search(sizes, earlier, cands, lower, best):
+        offs = [0] * len(sizes)
+
+        def dfs(k, cur):
+            nonlocal best
+            if k == len(sizes):
+                best = cur
+                return best <= lower
+            for off in cands:
+                if off + sizes[k] >= best:
+                    break
+                if any(off < offs[j] + sizes[j] and offs[j] < off + sizes[k] for j in earlier[k]):
+                    continue
+                offs[k] = off
+                if dfs(k + 1, max(cur, off + sizes[k])):
+                    return True
+            return False
+        dfs(0, 0)
+        return best
+
+    rng = random.Random(5)
+    for _ in range(120):
+        n = rng.randrange(1, 7)
+        sizes = sorted((rng.randrange(1, 64) * 8 for _ in range(n)), reverse=True)
+        earlier = [[j for j in range(k) if rng.random() < 0.6] for k in range(n)]
+        sums = {0}
+        for s in sizes:
+            sums |= {x + s for x in sums}
+        cands = sorted(sums)
+        lower = rng.randrange(max(sizes), sum(sizes) + 1)
+        start = sum(sizes) + rng.randrange(0, 2)
+        nb_off = np.zeros(n + 1, np.int64)
+        nb_off[1:] = np.cumsum([len(e) for e in earlier])
+        nb = np.array([j for e in earlier for j in e] or [0], np.int32)
+        out = C.c_int64(start)
+        sz, cd = np.array(sizes, np.int64), np.array(cands, np.int64)
+        N.lib().mp_brute_force_footprint(C.c_int32(n), N.ptr(sz), N.ptr(nb_off), N.ptr(nb), N.ptr(cd),
+                                         C.c_int64(len(cands)), C.c_int64(lower), C.byref(out))
+        assert out.value == py_search(sizes, earlier, cands, lower, start)
