@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import csv
 import io
+import itertools
 import json
 from dataclasses import dataclass, field
 from enum import Enum
@@ -152,22 +153,35 @@ class TraceArrays:
 
 
 def _events_to_arrays(events: Sequence[TraceEvent]) -> TraceArrays:
+    """Columns of a list of event objects.  The per-event work is C-level
+    iteration (attrgetter/map/fromiter); names are interned in first-seen
+    order with a dict, then only the distinct names are sorted."""
+    from operator import attrgetter
     n = len(events)
-    kind = np.empty(n, dtype=np.uint8)
-    size = np.empty(n, dtype=np.int64)
-    t_us = np.empty(n, dtype=np.int64)
-    index = np.empty(n, dtype=np.int64)
-    names = [None] * n
-    code = _CODE_OF_KIND
-    for i, ev in enumerate(events):
-        kind[i] = code[EventKind(ev.kind)]
-        size[i] = ev.size
-        t_us[i] = ev.t_us
-        index[i] = ev.index
-        names[i] = ev.var
-    contiguous = n == 0 or bool(np.array_equal(index, np.arange(n, dtype=np.int64)))
-    return TraceArrays.from_columns(kind, names, size, t_us,
-                                    None if contiguous else index)
+    if n == 0:
+        return TraceArrays(np.zeros(0, np.uint8), np.zeros(0, np.int32), np.zeros(0, np.int64),
+                           np.zeros(0, np.int64), [])
+    code = KIND_CODE
+    kinds = list(map(attrgetter("kind"), events))
+    try:
+        kind = np.fromiter(map(code.__getitem__, kinds), np.uint8, count=n)
+    except KeyError:
+        kind = np.fromiter((code[EventKind(k).value] for k in kinds), np.uint8, count=n)
+    size = np.fromiter(map(attrgetter("size"), events), np.int64, count=n)
+    t_us = np.fromiter(map(attrgetter("t_us"), events), np.int64, count=n)
+    index = np.fromiter(map(attrgetter("index"), events), np.int64, count=n)
+    ids: dict[str, int] = {}
+    first = np.fromiter(map(ids.setdefault, map(attrgetter("var"), events), itertools.count()), np.int64, count=n)
+    # setdefault with the event position: a name keeps the position of its
+    # first event; the distinct positions are then ranked by name
+    uniq = list(ids)
+    seen = np.fromiter(ids.values(), np.int64, count=len(uniq))
+    order = sorted(range(len(uniq)), key=uniq.__getitem__)
+    rank = np.empty(int(seen.max()) + 1, np.int32)
+    rank[seen[order]] = np.arange(len(uniq), dtype=np.int32)
+    var = rank[first]
+    contiguous = bool(np.array_equal(index, np.arange(n, dtype=np.int64)))
+    return TraceArrays(kind, var, size, t_us, [uniq[i] for i in order], None if contiguous else index)
 
 
 def _remember(trace: Trace, arrays: TraceArrays) -> None:
