@@ -141,11 +141,17 @@ __global__ void k_gap_areas(LoadView L, CandView c, const double *cur, double *a
 // scores + the unbudgeted SWDOA greedy, one CTA
 __global__ void __launch_bounds__(512) k_swap_greedy(LoadView L, CandView c, double *cur, uint8_t *taken,
                                                      double *doa, double *aoa, double *wdoa, double *swdoa,
-                                                     int32_t *order, double *peaks, int64_t *W, int32_t *jx) {
+                                                     int32_t *order, double *peaks, int64_t *W, int32_t *jx,
+                                                     int64_t *area) {
   __shared__ SwKey keys[33];
   __shared__ long long sm[PM_SMEM];
-  swdoa_greedy_block(CtaGroup{}, L, c, cur, taken, doa, aoa, wdoa, swdoa, order, peaks, W, jx, keys, sm);
+  swdoa_greedy_block(CtaGroup{}, L, c, cur, taken, doa, aoa, wdoa, swdoa, order, peaks, W, jx, keys, sm, -1, area);
 }
+
+// the greedy's rounds run on one warp with incremental areas up to this
+// many load slots (a round is then O(p / 32 + k / 32) on the warp instead
+// of a CTA pass with six barriers); longer windows keep the CTA rounds
+constexpr int64_t SWAP_WARP_ROUNDS_MAX_P = 8192;
 
 static LoadView load_view(mp_dprofile *P) { return LoadView{P->d.period, P->loads.p, P->op_times.p, P->d.duration_us}; }
 
@@ -169,11 +175,11 @@ extern "C" int mp_swap_scores(mp_ctx *ctx, mp_dprofile *P, const mp_cands_io *c,
   CUDA_TRY(cur.alloc(p, st)); CUDA_TRY(o_doa.alloc(k, st)); CUDA_TRY(o_aoa.alloc(k, st));
   CUDA_TRY(o_wdoa.alloc(k, st)); CUDA_TRY(o_sw.alloc(k, st)); CUDA_TRY(o_peaks.alloc(k + 1, st));
   CUDA_TRY(o_order.alloc(k, st)); CUDA_TRY(taken.alloc(k, st));
-  DBuf<int64_t> W;
+  DBuf<int64_t> W, area;
   DBuf<int32_t> jx;
-  CUDA_TRY(W.alloc(p + 1, st)); CUDA_TRY(jx.alloc(2 * k, st));
+  CUDA_TRY(W.alloc(p + 1, st)); CUDA_TRY(jx.alloc(2 * k, st)); CUDA_TRY(area.alloc(k, st));
   LAUNCH(ctx, k_swap_greedy, 1, 512, 0, load_view(P), cv, cur.p, taken.p, o_doa.p, o_aoa.p, o_wdoa.p, o_sw.p,
-         o_order.p, o_peaks.p, W.p, jx.p);
+         o_order.p, o_peaks.p, W.p, jx.p, p <= SWAP_WARP_ROUNDS_MAX_P ? area.p : nullptr);
   if (k) {
     CUDA_TRY(cudaMemcpyAsync(doa, o_doa.p, k * 8, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaMemcpyAsync(aoa, o_aoa.p, k * 8, cudaMemcpyDeviceToHost, st));

@@ -122,13 +122,23 @@ __device__ __forceinline__ double step_area(const LoadView &L, const double *cur
     if (a < L.op_times[mid]) hi = mid; else lo = mid + 1;
   }
   int64_t r0 = lo - 1 < 0 ? 0 : lo - 1;
+  // the reference stops at the first slot starting at or after b
+  // (op_times is non-decreasing): bound the loop up front so the loads of
+  // later slots are not held behind the exit test of earlier ones
+  int64_t r1 = r0, hi2 = p;
+  while (r1 < hi2) {
+    int64_t mid = (r1 + hi2) >> 1;
+    if (L.op_times[mid] < b) r1 = mid + 1; else hi2 = mid;
+  }
   double total = 0.0;
-  for (int64_t r = r0; r < p; r++) {
-    double s = L.op_times[r];
-    double e = r + 1 < p ? L.op_times[r + 1] : L.duration;
-    if (s >= b) break;
-    double ov = pymin(b, e) - pymax(a, s);
-    if (ov > 0) total += (cur ? cur[r] : (double)iloads[r]) * ov;
+  double s = r0 < r1 ? L.op_times[r0] : 0.0;
+#pragma unroll 4
+  for (int64_t r = r0; r < r1; r++) {
+    const double e = r + 1 < p ? L.op_times[r + 1] : L.duration;
+    const double ov = pymin(b, e) - pymax(a, s);
+    const double x = cur ? cur[r] : (double)iloads[r];
+    if (ov > 0) total += x * ov;
+    s = e;
   }
   return total;
 }
@@ -266,12 +276,84 @@ __device__ __forceinline__ int64_t gap_area_exact(const LoadView &L, const doubl
   return ex < (int64_t)EXACT_2_53 ? ex : -1;
 }
 
+// the same integral without the 2^53 cut (int64; callers keep every
+// integral below 2^62)
+__device__ __forceinline__ int64_t gap_area_raw(const LoadView &L, const double *cur, const int64_t *W, double a,
+                                                double b, int32_t ja, int32_t jb) {
+  const double d = L.duration;
+  if (b <= d) return b <= a ? 0 : area_to(L, cur, W, jb, b) - area_to(L, cur, W, ja, a);
+  int64_t x = d <= a ? 0 : W[L.p] - area_to(L, cur, W, ja, a);
+  int64_t y = b - d <= 0 ? 0 : area_to(L, cur, W, jb, b - d);
+  return x + y;
+}
+
+// ---------------------------------------------------------------------------
+// incremental gap areas.  Picking candidate c subtracts c.size from the
+// load on c's absence slots, so every other candidate's exact integral
+// drops by c.size times the wall time its gap shares with those slots:
+// one O(1) update per candidate per round instead of a pass over the load.
+
+// slot r spans [op_times[r], end(r)) in wall time
+__device__ __forceinline__ double slot_end(const LoadView &L, int64_t r) {
+  return r + 1 < L.p ? L.op_times[r + 1] : L.duration;
+}
+
+__device__ __forceinline__ double overlap(double x0, double x1, double y0, double y1) {
+  const double lo = x0 > y0 ? x0 : y0, hi = x1 < y1 ? x1 : y1;
+  return hi > lo ? hi - lo : 0.0;
+}
+
+// wall time of [y0, y1) inside candidate i's gap ([a, b], wrapping at the
+// duration like gap_area)
+__device__ __forceinline__ double gap_overlap(const LoadView &L, double a, double b, double y0, double y1) {
+  const double d = L.duration;
+  if (b <= d) return b <= a ? 0.0 : overlap(a, b, y0, y1);
+  return (d <= a ? 0.0 : overlap(a, d, y0, y1)) + (b - d <= 0 ? 0.0 : overlap(0.0, b - d, y0, y1));
+}
+
+// The absence slots of candidate q (lo+1 .. hi-1 modulo p, each counted
+// once per hit, as apply_absence subtracts once per hit: autoswap.py:119-129)
+// as wall-time pieces: `full` whole periods plus up to two ranges.
+struct AbsencePieces {
+  double full;          // whole periods, each [op_times[0], duration)
+  double y0[2], y1[2];  // partial ranges (empty when y1 <= y0)
+};
+__device__ __forceinline__ AbsencePieces absence_pieces(const LoadView &L, const CandView &c, int32_t q) {
+  const int64_t p = L.p, lo = c.out_index[q], hi = c.in_index[q] + (c.spans[q] ? p : 0);
+  AbsencePieces a{0.0, {0.0, 0.0}, {0.0, 0.0}};
+  const int64_t n = hi - lo - 1;
+  if (n <= 0) return a;
+  const int64_t full = n / p, rem = n - full * p, st = (lo + 1) % p;
+  a.full = (double)full;
+  if (rem) {
+    const int64_t last = st + rem - 1;
+    a.y0[0] = L.op_times[st];
+    if (last < p) {
+      a.y1[0] = slot_end(L, last);
+    } else {
+      a.y1[0] = L.duration;
+      a.y0[1] = L.op_times[0];
+      a.y1[1] = slot_end(L, last - p);
+    }
+  }
+  return a;
+}
+
+// wall time candidate i's gap [a, b] shares with those pieces
+__device__ __forceinline__ double absence_overlap(const LoadView &L, const AbsencePieces &q, double a, double b) {
+  double t = q.full != 0.0 ? q.full * gap_overlap(L, a, b, L.op_times[0], L.duration) : 0.0;
+  if (q.y1[0] > q.y0[0]) t += gap_overlap(L, a, b, q.y0[0], q.y1[0]);
+  if (q.y1[1] > q.y0[1]) t += gap_overlap(L, a, b, q.y0[1], q.y1[1]);
+  return t;
+}
+
 // One pass over the current load: max(cur) (Python max: the first maximal
 // value) and, when `exact` is requested and holds, W = the exclusive prefix
 // of cur[q] * len_q (p + 1 entries).  `exact` comes back false when some cur
 // is not an integer in [0, 2^53) or cur * duration may overflow.  Group-wide;
 // sm: >= PM_SMEM long longs of shared memory.
-constexpr int PM_SUM = 0, PM_TOT = 32, PM_MAX = 33, PM_MXR = 65, PM_OK = 66, PM_OKR = 98, PM_SMEM = 100;
+constexpr int PM_SUM = 0, PM_TOT = 32, PM_MAX = 33, PM_MXR = 65, PM_OK = 66, PM_OKR = 98, PM_R0 = 100,
+              PM_DONE = 101, PM_SMEM = 102;
 
 template <class G>
 __device__ double prefix_max_block(const G &g, const LoadView &L, const double *cur, int64_t *W, long long *sm,
@@ -346,11 +428,84 @@ __device__ double prefix_max_block(const G &g, const LoadView &L, const double *
 // above it is then decided); returns the number of picks made.  Any of
 // doa/aoa/wdoa/swdoa may be null.  Scratch: W[p + 1], jx[2k]; shared
 // memory keys >= 33 SwKey, sm >= PM_SMEM long longs.
+// The rounds of the greedy on one warp, with incremental exact areas A[i]
+// (see absence_overlap).  Runs while every round is exact in the sense of
+// prefix_max_block (all loads integers in [0, 2^53), max * duration < 2^62);
+// returns the first round it did not finish (== the pick count when it
+// ended normally, with *done set).  Lane-strided; warp-collective.
+static __device__ int64_t swdoa_rounds_warp(const LoadView &L, const CandView &c, double *cur, uint8_t *taken,
+                                     double *swdoa, int32_t *order, double *peaks, int64_t *A, int64_t stop,
+                                     bool &done) {
+  const int lane = threadIdx.x & 31;
+  const int64_t p = L.p, k = c.k;
+  const double d = L.duration;
+  done = false;
+  for (int64_t round = 0;; round++) {
+    double mx = -INF_D, mn = INF_D;
+    for (int64_t r = lane; r < p; r += 32) {
+      const double x = cur[r];
+      mx = r == lane ? x : pymax(mx, x);
+      mn = x < mn ? x : mn;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      mx = pymax(mx, __shfl_xor_sync(FULL_MASK, mx, o));
+      mn = fmin(mn, __shfl_xor_sync(FULL_MASK, mn, o));
+    }
+    if (lane == 0) peaks[round] = mx;
+    if (round == k || (stop >= 0 && f_le_i(mx, stop))) {
+      done = true;
+      return round;
+    }
+    if (!(mn >= 0 && mx < EXACT_2_53 && mx * d < EXACT_2_62)) return round;
+    SwKey best{-1, 0, 0.0, 0};
+    for (int64_t i = lane; i < k; i += 32) {
+      if (taken[i]) continue;
+      const int64_t ex = A[i];
+      SwKey o{(int32_t)i, c.name_rank[i], ex < (int64_t)EXACT_2_53 ? (double)ex : gap_area(L, cur, c.out_t[i], c.in_t[i]),
+              c.size[i]};
+      if (swdoa_better(o, best)) best = o;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      SwKey x = shfl_xor_key(best, o);
+      if (swdoa_better(x, best)) best = x;
+    }
+    const int32_t pick = best.i;
+    if (lane == 0) {
+      order[round] = pick;
+      if (swdoa) swdoa[pick] = best.area;
+      taken[pick] = 1;
+    }
+    // the pick's absence, then every remaining candidate's area
+    const int64_t lo = c.out_index[pick], hi = c.in_index[pick] + (c.spans[pick] ? p : 0);
+    const double sz = (double)c.size[pick];
+    if (hi - lo - 1 <= p) {
+      // lo + 1 .. hi - 1, split at the period end (no modulo per slot)
+      const int64_t e1 = hi < p ? hi : p;
+      for (int64_t x = lo + 1 + lane; x < e1; x += 32) cur[x] -= sz;
+      for (int64_t x = (lo + 1 > p ? lo + 1 - p : 0) + lane; x < hi - p; x += 32) cur[x] -= sz;
+    } else {
+      for (int64_t r = lane; r < p; r += 32) {
+        const int h = absence_hits(r, lo, hi, p);
+        for (int q = 0; q < h; q++) cur[r] -= sz;
+      }
+    }
+    const AbsencePieces ap = absence_pieces(L, c, pick);
+    const int64_t psz = c.size[pick];
+    for (int64_t i = lane; i < k; i += 32) {
+      if (i == pick || taken[i]) continue;
+      A[i] -= psz * (int64_t)absence_overlap(L, ap, c.out_t[i], c.in_t[i]);
+    }
+    __syncwarp();
+  }
+}
+
 template <class G>
 __device__ int64_t swdoa_greedy_block(const G &g, const LoadView &L, const CandView &c, double *cur,
                                       uint8_t *taken, double *doa, double *aoa, double *wdoa, double *swdoa,
                                       int32_t *order, double *peaks, int64_t *W, int32_t *jx, SwKey *keys,
-                                      long long *sm, int64_t stop = -1) {
+                                      long long *sm, int64_t stop = -1, int64_t *A = nullptr) {
   const int64_t p = L.p, k = c.k;
   const int tid = g.idx(), nt = g.size();
   bool times_ok = int_valued(L.duration);
@@ -372,7 +527,32 @@ __device__ int64_t swdoa_greedy_block(const G &g, const LoadView &L, const CandV
   }
   times_ok = g.sync_and(times_ok);
   const int lane = tid & 31, w = tid >> 5, nw = (nt + 31) >> 5;
-  for (int64_t round = 0;; round++) {
+  int64_t round0 = 0;
+  if (A && times_ok) {
+    // exact integrals of the initial load from its prefix, then the rounds
+    // on warp 0 while they stay exact (the group waits at one barrier)
+    bool exact = true;
+    prefix_max_block(g, L, cur, W, sm, exact);
+    if (exact) {
+      for (int64_t i = tid; i < k; i += nt)
+        A[i] = gap_area_raw(L, cur, W, c.out_t[i], c.in_t[i], jx[2 * i], jx[2 * i + 1]);
+      g.sync();
+      if (w == 0) {
+        bool done;
+        const int64_t r = swdoa_rounds_warp(L, c, cur, taken, swdoa, order, peaks, A, stop, done);
+        if (lane == 0) {
+          sm[PM_R0] = r;
+          sm[PM_DONE] = done;
+        }
+      }
+      g.sync();
+      round0 = sm[PM_R0];
+      const bool done = sm[PM_DONE] != 0;
+      g.sync();
+      if (done) return round0;
+    }
+  }
+  for (int64_t round = round0;; round++) {
     bool exact = times_ok;
     const double pk = prefix_max_block(g, L, cur, W, sm, exact);
     if (tid == 0) peaks[round] = pk;

@@ -232,12 +232,14 @@ struct SwapScratch {
 struct GreedyArrays {
   double *cur;
   int64_t *W;
+  int64_t *area;  // incremental exact gap areas
   int32_t *jx;
   uint8_t *taken;
   template <class A>
   __host__ __device__ void take(A &b, int64_t p, int64_t k) {
     cur = b.template take<double>(p);
     W = b.template take<int64_t>(p + 1);
+    area = b.template take<int64_t>(k);
     jx = b.template take<int32_t>(2 * k);
     taken = b.template take<uint8_t>(k);
   }
@@ -965,7 +967,7 @@ __device__ void sweep_one(const SweepArgs &a, int64_t t, char *slab, char *fast,
     }
     if (gi == 0 && a.prof) a.prof[t * 16 + 3] = clock64();
     norder = need ? swdoa_greedy_block(sg, L, cv, gr.cur, gr.taken, nullptr, nullptr, nullptr, nullptr, kp.order,
-                                       kp.peaks, gr.W, gr.jx, sh.keys, sh.gsm, stop)
+                                       kp.peaks, gr.W, gr.jx, sh.keys, sh.gsm, stop, gr.area)
                   : 0;
     if (gi == 0 && a.prof) a.prof[t * 16 + 4] = clock64();
     for (int64_t q = gi; q < norder; q += gn) corder[q] = cc.var[kp.order[q]];
