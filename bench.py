@@ -167,6 +167,13 @@ def stage_bytes(n, p, V, nnz, levels):
 # ---------------------------------------------------------------------------
 
 
+def config4(args, world, n, period):
+    """The `config` dict both arms print (same keys and values)."""
+    return {"workload": "interval_trace_1M (BASELINE configs[3])", "nvars": NVARS, "events": int(n),
+            "period": int(period), "policy": "best_fit", "accesses": bool(args.accesses),
+            "l2": "flushed (256 MiB write) between steps", "parallelism": f"replicas x{world}"}
+
+
 def build_workload(accesses: bool):
     from paper_1903_06631_b200 import workloads
     arrays, window = workloads.interval_trace(NVARS, seed=0, accesses=accesses)
@@ -296,7 +303,18 @@ def sweep_cpu_baseline(batch, params, procs):
     return dt, chunks, outs
 
 
-def run_sweep_bench(args, rank, world, local_rank):
+def ncu_traffic(kernel: str):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed
+    ncu capture (profiles/r2_ncu_kernels.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2_ncu_kernels.json")) as fh:
+            k = json.load(fh)["kernels"].get(kernel)
+        return k["dram_read_bytes"] + k["dram_write_bytes"] if k else None
+    except Exception:  # noqa: BLE001
+        return None
+
+
+def run_sweep_bench(args, rank, world, local_rank, hbm_gbs):
     import torch
     from paper_1903_06631_b200 import _native as N
     from paper_1903_06631_b200 import sweep, workloads
@@ -341,7 +359,21 @@ def run_sweep_bench(args, rank, world, local_rank):
                              pinned(nev * 8).view(np.int64), pinned(nev * 4).view(np.int32), hb.ev_off, params, hb)
     e2e_ms = []
     for i in range(args.warmup + args.steps):
-        ms, out = timed(lambda: sweep.run_sweep(hb, params, out=hout))
+        if world == 1:
+            ms, out = timed(lambda: sweep.run_sweep(hb, params, out=hout))
+        else:
+            # the whole sharded call: each rank's upload + launch + download,
+            # then the gather of every rank's records to rank 0 (host wall
+            # clock from a common barrier; max over ranks below)
+            import torch.distributed as dist
+            dist.barrier()
+            t0 = time.perf_counter()
+            out = sweep.run_sweep(hb, params, out=hout)
+            got = [None] * world if rank == 0 else None
+            dist.gather_object((parts[rank], out.records_only()), got, dst=0)
+            if rank == 0:
+                full = sweep.concat_results(got, batch)
+            ms = (time.perf_counter() - t0) * 1e3
         if i >= args.warmup:
             e2e_ms.append(ms)
     step_ms, e2e_step = float(np.mean(res_ms)), float(np.mean(e2e_ms))
@@ -351,6 +383,8 @@ def run_sweep_bench(args, rank, world, local_rank):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         step_ms, e2e_step = float(tt[0]), float(tt[1])
     units = batch.ntraces * len(params.budgets)
+    d2h = int(res.traces.nbytes + res.budgets.nbytes + 12 * mine.ev_off[-1])
+    algo = int(mine.nbytes) + d2h
     vars_total = int(res.traces["nvars"].sum())
     if world > 1:
         import torch.distributed as dist
@@ -364,9 +398,25 @@ def run_sweep_bench(args, rank, world, local_rank):
            "sharding": f"LPT over {world} rank(s), no data-path collective",
            "gpu_launches": launches,
            "e2e": {"value": units / (e2e_step * 1e-3), "unit": "units/s", "ms_per_step": e2e_step,
-                   "h2d_bytes_per_step": int(mine.nbytes),
-                   "d2h_bytes_per_step": int(res.traces.nbytes + res.budgets.nbytes + 12 * mine.ev_off[-1])},
+                   "h2d_bytes_per_step": int(mine.nbytes), "d2h_bytes_per_step": d2h,
+                   "timing": "CUDA events on the library stream" if world == 1 else
+                             "host wall clock from a barrier through the gather to rank 0, max over ranks"},
+           "roofline": {"bound": "latency (one CTA per trace: the largest traces' sequential chains)",
+                        "kernel": "k_sweep", "achieved": algo / (step_ms * 1e-3) / 1e9, "peak": hbm_gbs,
+                        "unit": "GB/s", "frac": algo / (step_ms * 1e-3) / 1e9 / hbm_gbs,
+                        "algorithmic_bytes": algo, "traffic": ncu_traffic("k_sweep"),
+                        "note": "bytes = trace columns read + records written; see DESIGN 4b"},
            "budget_status": {str(k): int(v) for k, v in zip(*np.unique(res.budgets["status"], return_counts=True))}}
+    if world > 1 and rank == 0:
+        # per-N parity: the gathered records equal one rank planning the
+        # whole batch (which the N=1 run checks against the oracle)
+        ds1 = sweep.DeviceSweep(batch)
+        ds1.run(params)
+        one = ds1.download()
+        ds1.close()
+        out["parity"] = {"gathered_equal_single_rank": bool(
+            one.traces.tobytes() == full.traces.tobytes() and one.budgets.tobytes() == full.budgets.tobytes()
+            and np.array_equal(one.offsets, full.offsets) and np.array_equal(one.cand_order, full.cand_order))}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         procs = os.cpu_count() or 1
         dt, chunks, outs = sweep_cpu_baseline(batch, params, procs)
@@ -421,17 +471,127 @@ def run_reference(args, rank, world):
                 step_s.append(max(o["seconds"] for o in outs))
     step = float(np.mean(step_s))
     value = procs * outs[0]["nvars"] / step
+    arrays, window = build_workload(args.accesses)
+    n = len(arrays)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
-            "data": "synthetic", "config": {"workload": "interval_trace_1M (BASELINE configs[3])",
-                                            "nvars": NVARS, "policy": "best_fit"},
+            "data": "synthetic", "config": config4(args, world, n, window[1] - window[0]),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port",
                              "sample": f"{procs} replicas of the full 1M-var trace, one per process "
                                        "(C oracle; the Python reference is not on this box)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def run_config1_leg(args, hbm_gbs) -> dict:
+    """BASELINE configs[0]: SmartPool plan of the ResNet-50 b32 trace.
+
+    resident: the one-trace sweep kernel (csrc/sweep.cu, one CTA) with the
+    trace already in HBM; e2e: the public call (pipeline.plan_arrays, which
+    takes the one-CTA path for a trace this small) from pinned host columns,
+    upload and offsets readback inside the timed region; cpu_baseline: the C
+    oracle (detect + extract + conflict + plan) on one host core."""
+    import torch
+    from paper_1903_06631_b200 import _native as N
+    from paper_1903_06631_b200 import sweep, synth, workloads
+    from paper_1903_06631_b200.pipeline import plan_arrays
+    from paper_1903_06631_b200.trace import TraceArrays, as_arrays
+    arrays = as_arrays(synth.generate_synthetic_trace(workloads.resnet50_spec(32)))
+    stream = torch.cuda.ExternalStream(N.stream_ptr())
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def timed(fn):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        out = fn()
+        e.record(stream)
+        e.synchronize()
+        return s.elapsed_time(e), out
+
+    reps = max(args.steps, 20)
+    ds = sweep.DeviceSweep(sweep.SweepBatch.from_traces([arrays]))
+    prm = sweep.SweepParams(budgets=())
+    for _ in range(args.warmup):
+        ds.run(prm)
+    res_ms = [timed(lambda: ds.run(prm))[0] for _ in range(reps)]
+    res = ds.download()
+    ds.close()
+    keep, cols = [], {}
+    for name in ("kind", "var", "size", "t_us"):
+        t, v = pinned_like(getattr(arrays, name))
+        keep.append(t)
+        cols[name] = v
+    host = TraceArrays(cols["kind"], cols["var"], cols["size"], cols["t_us"], arrays.names)
+    out_t, out_offs = pinned_like(np.zeros(len(arrays), np.int64))
+    keep.append(out_t)
+    e2e_ms = []
+    for i in range(args.warmup + reps):
+        ms, plan = timed(lambda: plan_arrays(host, offsets_out=out_offs))
+        if i >= args.warmup:
+            e2e_ms.append(ms)
+    # C oracle, one core: a bounded sample of repeated plans (~1 s)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as orc
+    t0, k = time.perf_counter(), 0
+    while k < 3 or time.perf_counter() - t0 < 1.0:
+        rc, p = orc.detect(arrays)
+        rc, fp = orc.extract(arrays, len(arrays) - p, len(arrays))
+        off, lo, hi = orc.profile_segments(fp)
+        h, _r, _c = orc.conflict(off, lo, hi)
+        rc, offs, foot = orc.plan(h, fp.size, fp.alloc.astype(np.int64), fp.base, fp.name_ralloc(),
+                                  fp.name_blob, fp.name_off, 1)
+        orc.graph_free(h)
+        k += 1
+    cpu_s = (time.perf_counter() - t0) / k
+    r = res.traces[0]
+    nv = int(r["nvars"])
+    res_step, e2e_step = float(np.median(res_ms)), float(np.median(e2e_ms))
+    # algorithmic bytes (SURVEY 8(d) config 1): events 21 B in, per variable
+    # 40 B profile + 8 B offset, 2E x 4 B adjacency
+    edges = int(r["edges"])
+    algo = len(arrays) * 21 + nv * 48 + 2 * edges * 4
+    return {"workload": "resnet50_b32 plan (BASELINE configs[0])", "events": len(arrays), "period": int(r["period"]),
+            "nvars": nv, "peak_bytes": int(r["peak_bytes"]), "footprint_bytes": int(r["footprint_bytes"]),
+            "value": nv / (res_step * 1e-3), "unit": "vars/s", "us_per_plan": res_step * 1e3,
+            "e2e": {"value": nv / (e2e_step * 1e-3), "unit": "vars/s", "us_per_plan": e2e_step * 1e3,
+                    "h2d_bytes_per_step": int(sum(cols[c].nbytes for c in cols)), "d2h_bytes_per_step": nv * 8},
+            "roofline": {"bound": "latency (one CTA: sequential placement walk)", "achieved": algo / (res_step * 1e-3) / 1e9,
+                         "peak": hbm_gbs, "unit": "GB/s", "frac": algo / (res_step * 1e-3) / 1e9 / hbm_gbs,
+                         "algorithmic_bytes": algo},
+            "cpu_baseline": {"value": nv / cpu_s, "unit": "vars/s", "cores": 1, "kind": "port",
+                             "sample": f"{k} plans of the same trace, C oracle 1 thread, {cpu_s * 1e6:.0f} us each"},
+            "parity": {"offsets_equal_oracle": bool(np.array_equal(offs, res.offsets_of(0))
+                                                    and np.array_equal(offs, out_offs[:nv])),
+                       "footprint_equal": foot == int(r["footprint_bytes"]) == plan.footprint_bytes,
+                       "peak_equal": fp.peak_bytes == int(r["peak_bytes"])}}
+
+
+def run_config2_leg(local_rank: int, steps: int = 20) -> dict:
+    """BASELINE configs[1]: a VGG-16 b64 training iteration served from the
+    SmartPool plan through the pluggable allocator (tools/config2_pool.py in
+    its own process: the allocator must own the CUDA context from its first
+    malloc).  Footprint vs the cnmem-style first-fit arena and PyTorch's
+    caching allocator; allocator host us per call; iteration times."""
+    cmd = [sys.executable, os.path.join(ROOT, "tools", "config2_pool.py"), "--batch", "64", "--steps", str(steps)]
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES=os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",")[local_rank]
+               if os.environ.get("CUDA_VISIBLE_DEVICES") else str(local_rank))
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+        d = json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception as exc:  # noqa: BLE001  (the main line must still print)
+        return {"error": f"{type(exc).__name__}: {str(exc)[:200]}"}
+    keep = ("window_vars", "peak_load_bytes", "smartpool_footprint_bytes", "alpha", "cnmem_style_first_fit_bytes",
+            "smartpool_vs_first_fit", "torch_caching_max_reserved", "torch_caching_max_allocated",
+            "iter_ms_served", "iter_ms_passthrough", "iter_ms_torch_default", "hook_us_per_call",
+            "hook_calls_per_iter", "served_losses_equal_passthrough")
+    a = d.get("allocator", {})
+    return {"workload": "VGG-16 b64 training iteration served from the plan (BASELINE configs[1])",
+            "data": "synthetic (random-init VGG-16, random batch)", **{k: d.get(k) for k in keep},
+            "allocator": {k: a.get(k) for k in ("hits", "misses", "conflicts")}}
 
 
 def run_swap_leg(local_rank: int, frac: float = 0.95) -> dict:
@@ -462,7 +622,25 @@ def run_swap_leg(local_rank: int, frac: float = 0.95) -> dict:
             "rows": rows}
 
 
+def torchrun_cmd(nproc: int, script: str, argv: list) -> list:
+    """The driver's own launch line: one process per GPU on this node,
+    rendezvous on 127.0.0.1 at a free port."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+            "--master-addr", "127.0.0.1", "--master-port", str(port), script, *argv]
+
+
 def main():
+    if "WORLD_SIZE" not in os.environ:
+        # `bench.py --gpus N` outside torchrun: launch the N ranks ourselves
+        pre = argparse.ArgumentParser(add_help=False)
+        pre.add_argument("--gpus", type=int, default=1)
+        n = pre.parse_known_args()[0].gpus
+        if n > 1:
+            return subprocess.run(torchrun_cmd(n, os.path.abspath(__file__), sys.argv[1:])).returncode
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
@@ -472,6 +650,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="skip the config-5 batched sweep leg")
     ap.add_argument("--no-swap", action="store_true", help="skip the config-3 swap-overhead leg")
+    ap.add_argument("--no-config1", action="store_true", help="skip the config-1 ResNet-50 plan leg")
+    ap.add_argument("--no-config2", action="store_true", help="skip the config-2 served VGG-16 leg")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -486,7 +666,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         dist.barrier()
     arrays, r = run_ours(args, rank, world, local_rank)
-    r["sweep"] = None if args.no_sweep else run_sweep_bench(args, rank, world, local_rank)
+    r["sweep"] = None if args.no_sweep else run_sweep_bench(args, rank, world, local_rank, hbm_peak()[0])
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
@@ -500,26 +680,16 @@ def main():
     per_stage = {k: ms / steps for k, (ms, _c) in stages.items()}
     dom = max(per_stage, key=per_stage.get)
     achieved = sb.get(dom, 0) / (per_stage[dom] * 1e-3) / 1e9
-    # DRAM traffic per launch of the dominant kernel, from the committed
-    # `ncu --set full` capture (profiles/r1_ncu_kernels.json)
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "r1_ncu_kernels.json")) as fh:
-            k = json.load(fh).get({"place": "k_place_async", "conflict_fill": "k_iv_fill"}.get(dom, ""), None)
-        if k:
-            traffic = k["dram_read_bytes"] + k["dram_write_bytes"]
-    except Exception:  # noqa: BLE001
-        pass
+    # DRAM traffic per launch of the dominant kernel, from the committed ncu
+    # capture (profiles/r2_ncu_kernels.json, tools/ncu_stages.sh)
+    traffic = ncu_traffic({"place": "k_place_async", "conflict_fill": "k_iv_fill"}.get(dom, ""))
     stage_roof = {s: round(sb[s] / (ms * 1e-3) / 1e9 / peak, 4) for s, ms in per_stage.items() if s in sb and ms > 0}
     line = {
         "metric": METRIC, "value": r["vars_total"] / (r["step_ms"] * 1e-3), "unit": UNIT,
         "n_gpus": world, "steps": steps, "warmup": args.warmup, "ms_per_step": r["step_ms"],
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
         "data": "synthetic",
-        "config": {"workload": "interval_trace_1M (BASELINE configs[3])", "nvars": NVARS,
-                   "events": r["n"], "period": plan.period, "policy": "best_fit",
-                   "accesses": bool(args.accesses), "l2": "flushed (256 MiB write) between steps",
-                   "parallelism": f"replicas x{world}"},
+        "config": config4(args, world, r["n"], plan.period),
         "result": {"peak_bytes": plan.peak_bytes, "footprint_bytes": plan.footprint_bytes,
                    "alpha": plan.competitive_ratio, "levels": plan.levels, "csr_entries": plan.nnz,
                    "offsets_sha256": r["sha"][:16]},
@@ -536,6 +706,10 @@ def main():
     }
     if r.get("sweep") is not None:
         line["sweep"] = r["sweep"]
+    if not args.no_config1 and world == 1:
+        line["config1"] = run_config1_leg(args, peak)
+    if not args.no_config2 and world == 1:
+        line["config2"] = run_config2_leg(local_rank)
     if not args.no_swap:
         line["swap"] = run_swap_leg(local_rank)
     if not args.no_cpu_baseline:

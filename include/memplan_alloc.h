@@ -52,6 +52,10 @@ int64_t mp_alloc_pool_base(void);
  * peak bytes, ordinal, conflicts, live pool blocks, swap alias fallbacks,
  * retired pools still mapped */
 void mp_alloc_stats(int64_t *out);
+/* out[4]: mp_torch_alloc calls, their total host ns, mp_torch_free calls,
+ * their total host ns (entry to return, lock wait included); zeroed by
+ * mp_alloc_reset_peak */
+void mp_alloc_call_stats(int64_t *out);
 void mp_alloc_reset_peak(void);
 /* (iteration, ordinal, clashing block) triples of refused slots */
 int64_t mp_alloc_clash_log(int64_t *out, int64_t cap);

@@ -15,6 +15,8 @@
 #include <stdint.h>
 #include <sys/types.h>
 
+#include <time.h>
+
 #include <mutex>
 #include <unordered_map>
 #include <vector>
@@ -62,6 +64,8 @@ struct State {
   // no other block may be served at the same address while they are out
   std::unordered_map<int64_t, int64_t> swapped_out;
   int64_t aliases = 0;
+  // host-side cost of the hooks (entry to return, lock wait included)
+  int64_t alloc_calls = 0, alloc_ns = 0, free_calls = 0, free_ns = 0;
 };
 
 State &S() {
@@ -71,13 +75,32 @@ State &S() {
 
 inline int64_t round_up(int64_t n) { return (n + ALIGN - 1) / ALIGN * ALIGN; }
 
+inline int64_t now_ns() {
+  timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return (int64_t)ts.tv_sec * 1000000000 + ts.tv_nsec;
+}
+
+// adds the time since `start` (taken before the lock) to (calls, ns) when
+// the enclosing hook returns
+struct HookTimer {
+  int64_t t0, &calls, &ns;
+  HookTimer(int64_t &c, int64_t &n, int64_t start) : t0(start), calls(c), ns(n) {}
+  ~HookTimer() {
+    calls++;
+    ns += now_ns() - t0;
+  }
+};
+
 }  // namespace
 
 extern "C" {
 
 void *mp_torch_alloc(ssize_t size, int device, cudaStream_t stream) {
   State &s = S();
+  const int64_t t0 = now_ns();
   std::lock_guard<std::mutex> g(s.mu);
+  HookTimer tm(s.alloc_calls, s.alloc_ns, t0);
   int64_t rs = round_up(size > 0 ? size : 1);
   void *p = nullptr;
   if (s.mode == 1) {
@@ -122,7 +145,9 @@ void *mp_torch_alloc(ssize_t size, int device, cudaStream_t stream) {
 
 void mp_torch_free(void *ptr, ssize_t size, int device, cudaStream_t stream) {
   State &s = S();
+  const int64_t t0 = now_ns();
   std::lock_guard<std::mutex> g(s.mu);
+  HookTimer tm(s.free_calls, s.free_ns, t0);
   (void)size;
   (void)device;
   if (s.logging) s.log.push_back({s.seq, 1, (int64_t)ptr, 0});
@@ -247,8 +272,17 @@ int mp_alloc_pool_reclaim(int64_t off, int64_t size) {
   s.pool_live[off] = size;
   return 0;
 }
+void mp_alloc_call_stats(int64_t *out) {
+  State &s = S();
+  std::lock_guard<std::mutex> g(s.mu);
+  out[0] = s.alloc_calls;
+  out[1] = s.alloc_ns;
+  out[2] = s.free_calls;
+  out[3] = s.free_ns;
+}
 void mp_alloc_reset_peak() {
   std::lock_guard<std::mutex> g(S().mu);
+  S().alloc_calls = S().alloc_ns = S().free_calls = S().free_ns = 0;
   S().peak_bytes = S().cur_bytes;
   S().hits = S().misses = S().conflicts = S().aliases = 0;
 }

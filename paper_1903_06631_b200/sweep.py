@@ -178,6 +178,10 @@ class SweepResult:
     params: SweepParams = field(default_factory=SweepParams)
     batch: "SweepBatch | None" = None
 
+    def records_only(self) -> "SweepResult":
+        """The records without the input batch (what a rank sends in a gather)."""
+        return SweepResult(self.traces, self.budgets, self.offsets, self.cand_order, self.ev_off, self.params, None)
+
     def offsets_of(self, t: int) -> np.ndarray:
         e0 = int(self.ev_off[t])
         return self.offsets[e0:e0 + int(self.traces["nvars"][t])]
@@ -367,7 +371,7 @@ def run_sweep_sharded(batch: SweepBatch, params: SweepParams | None = None, rank
         return concat_results([(mine, res)], batch)
     import torch.distributed as dist
     gathered = [None] * world if rank == 0 else None
-    dist.gather_object((mine, res), gathered, dst=0, group=group)
+    dist.gather_object((mine, res.records_only() if res is not None else None), gathered, dst=0, group=group)
     if rank != 0:
         return None
     return concat_results([g for g in gathered if g[1] is not None], batch)

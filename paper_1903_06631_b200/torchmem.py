@@ -53,7 +53,17 @@ def stats() -> dict:
     ctl().mp_alloc_stats(out)
     return {"hits": out[0], "misses": out[1], "pool_bytes": out[2], "outside_live_bytes": out[3],
             "outside_peak_bytes": out[4], "ordinal": out[5], "conflicts": out[6], "pool_live_blocks": out[7],
-            "swap_alias_fallbacks": out[8], "retired_pools_mapped": out[9]}
+            "swap_alias_fallbacks": out[8], "retired_pools_mapped": out[9], **call_stats()}
+
+
+def call_stats() -> dict:
+    """Host cost of the allocator hooks since the last reset: calls and mean
+    microseconds per call (lock wait included)."""
+    out = (C.c_int64 * 4)()
+    ctl().mp_alloc_call_stats(out)
+    return {"alloc_calls": out[0], "alloc_ns": out[1], "free_calls": out[2], "free_ns": out[3],
+            "alloc_us_per_call": out[1] / out[0] / 1e3 if out[0] else None,
+            "free_us_per_call": out[3] / out[2] / 1e3 if out[2] else None}
 
 
 class Tracer:

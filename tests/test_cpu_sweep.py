@@ -88,3 +88,24 @@ def test_sharded_sweep_gathers_over_gloo(tmp_path):
     assert np.load(out + ".traces.npy").tobytes() == whole.traces.tobytes()
     assert np.load(out + ".budgets.npy").tobytes() == whole.budgets.tobytes()
     assert np.array_equal(np.load(out + ".offsets.npy"), whole.offsets)
+
+
+def test_bench_launcher_runs_the_sharded_sweep_on_two_ranks(tmp_path):
+    """bench.py --gpus N re-launches itself with bench.torchrun_cmd; the same
+    launch line drives a 2-rank gloo sweep whose gathered records equal one
+    process planning the whole batch."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import bench
+    out = str(tmp_path / "res")
+    cmd = bench.torchrun_cmd(2, os.path.join(root, "tests", "_torchrun_sweep_worker.py"), [out])
+    assert cmd[cmd.index("--master-addr") + 1] == "127.0.0.1" and "--nproc-per-node=2" in cmd
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    subprocess.run(cmd, check=True, timeout=300, env=env, cwd=root)
+    batch = sweep.SweepBatch.from_traces(workloads.sweep_traces(n_models=6, n_scales=3))
+    whole = oracle_runner(batch, sweep.SweepParams())
+    assert np.load(out + ".traces.npy").tobytes() == whole.traces.tobytes()
+    assert np.load(out + ".budgets.npy").tobytes() == whole.budgets.tobytes()
+    assert np.array_equal(np.load(out + ".offsets.npy"), whole.offsets)

@@ -127,7 +127,9 @@ def main():
     def served_step():
         torchmem.begin_iteration()
         return step()
+    cs0 = torchmem.call_stats()
     ms_serve, losses_serve = timed(served_step, a.steps, lossbuf)
+    cs1 = torchmem.call_stats()
     restore()
     _ms, losses_serve2 = timed(served_step, a.steps, lossbuf)
     st = torchmem.stats()
@@ -175,7 +177,12 @@ def main():
         "smartpool_vs_first_fit": 1 - plan.footprint_bytes / arena if arena else None,
         "torch_caching_max_reserved": ref.get("max_reserved"), "torch_caching_max_allocated": ref.get("max_allocated"),
         "iter_ms_served": ms_serve, "iter_ms_passthrough": ms_pass, "iter_ms_torch_default": ref.get("ms"),
-        "allocator": st, "clashes": torchmem.clash_log()[:12],
+        "allocator": st, "hook_us_per_call": {
+            k: (cs1[k + "_ns"] - cs0[k + "_ns"]) / (cs1[k + "_calls"] - cs0[k + "_calls"]) / 1e3
+            if cs1[k + "_calls"] > cs0[k + "_calls"] else None
+            for k in ("alloc", "free")},
+        "hook_calls_per_iter": {k: (cs1[k + "_calls"] - cs0[k + "_calls"]) / a.steps for k in ("alloc", "free")},
+        "clashes": torchmem.clash_log()[:12],
         "served_losses_equal_passthrough": losses_serve == losses_pass,
         "losses_served": losses_serve[:6], "losses_passthrough": losses_pass[:6],
         "passthrough_repeatable": losses_pass == losses_pass2, "served_repeatable": losses_serve == losses_serve2,
