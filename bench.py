@@ -594,12 +594,15 @@ def run_config2_leg(local_rank: int, steps: int = 20) -> dict:
             "allocator": {k: a.get(k) for k in ("hits", "misses", "conflicts")}}
 
 
-def run_swap_leg(local_rank: int, frac: float = 0.95) -> dict:
+SWAP_FRACS = "0.98,0.95,0.92,0.9,0.88,0.85,0.83"
+
+
+def run_swap_leg(local_rank: int, fracs: str = SWAP_FRACS, steps: int = 50) -> dict:
     """BASELINE configs[2]: swap-iteration overhead % vs the same served,
     hooked iteration without swaps (tools/config3_swap.py, own process: the
     pluggable allocator must own the CUDA context from its first malloc)."""
-    cmd = [sys.executable, os.path.join(ROOT, "tools", "config3_swap.py"), "--fracs", str(frac),
-           "--modes", "reference_selection,window_fits,window_fits_stall4pct", "--steps", "10"]
+    cmd = [sys.executable, os.path.join(ROOT, "tools", "config3_swap.py"), "--fracs", fracs,
+           "--modes", "reference_selection,window_fits", "--steps", str(steps)]
     env = dict(os.environ, CUDA_VISIBLE_DEVICES=os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",")[local_rank]
                if os.environ.get("CUDA_VISIBLE_DEVICES") else str(local_rank))
     try:
@@ -607,18 +610,34 @@ def run_swap_leg(local_rank: int, frac: float = 0.95) -> dict:
         d = json.loads(out.stdout.strip().splitlines()[-1])
     except Exception as exc:  # noqa: BLE001  (the main line must still print)
         return {"error": f"{type(exc).__name__}: {str(exc)[:200]}"}
+    bw = d["link_bw_bytes_per_s"]
     rows = []
     for l in d["limits"]:
+        link = l.get("link") or {}
+        ach = {k: v.get("bytes_per_s") for k, v in link.items()}
         rows.append({"mode": l["mode"], "limit_frac": l["frac"], "error": l.get("error"),
+                     "selected": l.get("selected"), "executed": l.get("executed"),
                      "measured_overhead_pct": l.get("measured_overhead_pct"),
+                     # the reference's simulate() under the limit; when its
+                     # replay deadlocks (the reference calls the plan
+                     # infeasible) this is its replay without the limit
                      "predicted_overhead_pct": l.get("predicted_overhead_pct"),
+                     "reference_replay": "SwapDeadlock at the limit" if l.get("sim_limit_deadlock") else (
+                         None if l.get("error") else "ok"),
+                     "predicted_executed_overhead_pct": l.get("predicted_executed_overhead_pct"),
                      "pool_reduction_vs_noswap": l.get("pool_reduction_vs_noswap"),
                      "bytes_moved_per_iter": l.get("swap_bytes_per_iter"),
+                     "link_achieved_bytes_per_s": ach or None,
+                     "link_frac": {k: (v / bw[k] if v and bw.get(k) else None) for k, v in ach.items()} or None,
                      "losses_equal_unswapped": l.get("losses_equal_unswapped")})
     return {"workload": "VGG-16 b128 training iteration (BASELINE configs[2])",
             "metric": "swap-iter overhead % vs no-swap", "unit": "%", "higher_is_better": False,
             "data": "synthetic (random-init VGG-16, random batch)", "iter_ms_noswap": d["iter_ms_served_hooked"],
-            "traced_peak_bytes": d["traced_peak_bytes"], "link_bytes_per_s": d["link_bw_bytes_per_s"],
+            "steps_per_row": steps, "traced_peak_bytes": d["traced_peak_bytes"],
+            "load_min_frac": d["load_min_all_candidates_absent"] / d["traced_peak_bytes"],
+            "link_bytes_per_s": bw,
+            "link_roofline": "achieved = bytes / copy-stream busy time (CUDA events around each copy, last "
+                             "iteration); frac against the measured pinned D2H / H2D rate",
             "rows": rows}
 
 

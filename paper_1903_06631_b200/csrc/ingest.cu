@@ -22,13 +22,6 @@
 // ---------------------------------------------------------------------------
 // grouping
 
-__global__ void k_group_init(const int32_t *var, int64_t n, uint32_t *keys, uint32_t *vals) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    keys[i] = (uint32_t)var[i];
-    vals[i] = (uint32_t)i;
-  }
-}
-
 // gstart[v] = lower_bound(v) in the sorted keys: each position where the
 // key changes writes the starts of the ids from the previous key + 1 up to
 // its own (ids without events get an empty run); the last position closes
@@ -53,8 +46,9 @@ int build_groups(mp_ctx *ctx, mp_dtrace *t, mp_err *err) {
   CUDA_TRY(keys.alloc(n, ctx->stream));
   CUDA_TRY(t->perm.alloc(n, ctx->stream));
   CUDA_TRY(t->gstart.alloc((int64_t)t->nvars + 1, ctx->stream));
-  LAUNCH(ctx, k_group_init, grid_for(n, 256), 256, 0, t->var.p, n, keys.p, t->perm.p);
-  int rc = dev_radix_sort_u32(ctx, keys.p, t->perm.p, n, bits_for((uint64_t)(t->nvars > 0 ? t->nvars - 1 : 0)), err);
+  // the first pass reads the var column itself and carries the positions
+  int rc = dev_radix_sort_u32_iota(ctx, (const uint32_t *)t->var.p, keys.p, t->perm.p, n,
+                                   bits_for((uint64_t)(t->nvars > 0 ? t->nvars - 1 : 0)), err);
   if (rc) return rc;
   if (n) LAUNCH(ctx, k_group_bounds, grid_for(n, 256), 256, 0, keys.p, n, t->nvars, t->gstart.p);
   else CUDA_TRY(cudaMemsetAsync(t->gstart.p, 0, ((int64_t)t->nvars + 1) * 8, ctx->stream));

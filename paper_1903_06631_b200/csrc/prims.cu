@@ -1,12 +1,15 @@
 // prims.cu — device-wide scan and stable LSD radix sort (sm_100a).
 //
 // The radix sort is the "vectorised radix sort" the ingest and conflict
-// stages stand on: per 8-bit digit pass, (1) a tile histogram kernel,
-// (2) an exclusive scan of the digit-major count matrix, (3) a scatter
-// kernel that ranks keys inside the tile with warp match_any (stable: warp w
-// owns a contiguous run, processed round by round in lane order), stages
-// the tile in shared memory in digit order and writes each digit run out
-// contiguously so global stores coalesce.
+// stages stand on, two variants of 8-bit digit passes:
+//  * reduce-then-scan (large inputs): per pass a tile histogram kernel, one
+//    exclusive scan of the digit-major (digit, tile) count matrix, and a
+//    scatter kernel that ranks keys stably inside the tile (ballot
+//    multisplit), stages the tile in shared memory in digit order and writes
+//    each digit run out contiguously;
+//  * one-sweep (inputs of about one wave of tiles): the global digit
+//    histograms of every pass up front, then one kernel per pass whose tiles
+//    resolve their digit offsets by decoupled look-back.
 #include "common.cuh"
 
 void mp_set_err(mp_err *e, int32_t code, int64_t index, int64_t a0, int64_t a1, const char *msg) {
@@ -195,7 +198,13 @@ template int dev_exclusive_scan<int64_t>(mp_ctx *, const int64_t *, int64_t *, i
 #define RS_LOOKBACK_BATCH 8  // predecessor digit counts read per look-back round trip (1: 5 % slower passes)
 #endif
 #ifndef RS_ITEMS32
-#define RS_ITEMS32 16  // keys per thread of a 32-bit pass tile
+#define RS_ITEMS32 16  // keys per thread of a 32-bit one-sweep pass tile
+#endif
+#ifndef RS_RTS_ITEMS32
+#define RS_RTS_ITEMS32 12  // keys per thread of a 32-bit reduce-then-scan tile (16: 119 registers, 8: 4 % slower)
+#endif
+#ifndef RS_RTS_MIN_N
+#define RS_RTS_MIN_N 2000000  // below this many keys a one-sweep pass's look-back is short: keep it
 #endif
 constexpr int RS_THREADS = 256;
 constexpr int RS_WARPS = RS_THREADS / 32;
@@ -369,9 +378,257 @@ __global__ void __launch_bounds__(RS_THREADS) k_os_pass(const K *keys, const uin
   }
 }
 
+// ----------------------------------------------------------------------------
+// Reduce-then-scan LSD radix sort (the default; RS_ONESWEEP=1 restores the
+// one-sweep kernels above).  Per pass: (1) k_rs_hist counts each tile's
+// digits into a digit-major matrix mat[d * ntiles + tile]; (2) one exclusive
+// scan of the matrix gives every (digit, tile) run its global start — the
+// digit base and the tile prefix at once, so no tile waits on a look-back
+// (the one-sweep passes spent a quarter of their time there: a tile posted
+// late in a wave walks back over every tile of the wave still in flight);
+// (3) k_rs_scatter ranks each tile's keys stably and writes each digit run
+// contiguously through shared memory.  Ranking uses a ballot multisplit (one
+// vote per digit bit) instead of match.any, whose latency serialised the
+// per-warp ranking loop.
+#ifndef RS_ONESWEEP
+#define RS_ONESWEEP 0
+#endif
+
+// lanes of the warp holding the same digit (d < 1 << RB), among `valid` lanes
+template <int RB>
+__device__ __forceinline__ unsigned multisplit_peers(unsigned d, unsigned valid) {
+  unsigned peers = valid;
+#pragma unroll
+  for (int b = 0; b < RB; b++) {
+    const bool bit = (d >> b) & 1u;
+    const unsigned bb = __ballot_sync(FULL_MASK, bit);
+    peers &= bit ? bb : ~bb;
+  }
+  return peers;
+}
+
+template <typename K, int RB, int ITEMS>
+__global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const K *keys, int64_t n, int shift, int32_t ntiles,
+                                                        int32_t *mat) {
+  constexpr int BINS = 1 << RB;
+  constexpr int TILE = RS_THREADS * ITEMS;
+  constexpr int VK = 16 / sizeof(K);  // keys per 16-byte vector
+  __shared__ int32_t h[2][BINS];  // two copies halve same-address contention on skewed digits
+  for (int i = threadIdx.x; i < 2 * BINS; i += RS_THREADS) h[i / BINS][i % BINS] = 0;
+  const int64_t base = (int64_t)blockIdx.x * TILE;
+  int32_t *hh = h[(threadIdx.x >> 5) & 1];
+  // every load issued before the first atomic
+  union {
+    uint4 q[ITEMS / VK];
+    K k[ITEMS];
+  } u;
+  const bool full = base + TILE <= n && (((uintptr_t)keys) & 15) == 0;
+  if (full) {
+    const uint4 *src = (const uint4 *)(keys + base);
+#pragma unroll
+    for (int i = 0; i < ITEMS / VK; i++) u.q[i] = src[i * RS_THREADS + threadIdx.x];
+  } else {
+#pragma unroll
+    for (int i = 0; i < ITEMS; i++) {
+      const int64_t j = base + (int64_t)i * RS_THREADS + threadIdx.x;
+      u.k[i] = j < n ? keys[j] : K(0);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < ITEMS; i++) {
+    const int64_t j = full ? 0 : base + (int64_t)i * RS_THREADS + threadIdx.x;
+    if (j < n) atomicAdd(&hh[(unsigned)(u.k[i] >> shift) & (BINS - 1)], 1);
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d < BINS; d += RS_THREADS) mat[(int64_t)d * ntiles + blockIdx.x] = h[0][d] + h[1][d];
+}
+
+// vals == nullptr: the values are the input positions (iota)
+#ifndef RS_MINB
+#define RS_MINB 3  // resident scatter CTAs per SM the register budget must allow
+#endif
+#ifndef RS_MATCH
+#define RS_MATCH 0  // rank with match.any instead of the ballot multisplit
+#endif
+template <typename K, int RB, int ITEMS>
+__global__ void __launch_bounds__(RS_THREADS, RS_MINB) k_rs_scatter(const K *keys, const uint32_t *vals, K *okeys,
+                                                           uint32_t *ovals, int64_t n, int shift, int32_t ntiles,
+                                                           const int32_t *offs) {
+  constexpr int BINS = 1 << RB;
+  constexpr int TILE = RS_THREADS * ITEMS;
+  constexpr int PER_WARP = 32 * ITEMS;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  K *sk = (K *)smem_raw;
+  uint32_t *sv = (uint32_t *)(sk + TILE);
+  __shared__ int32_t whist[RS_WARPS][BINS];
+  __shared__ int32_t dstart[BINS];
+  __shared__ int32_t gpos[BINS];
+  __shared__ int32_t wtot[RS_WARPS];
+
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t tile = blockIdx.x;
+  const int64_t base = tile * (int64_t)TILE;
+  for (int d = lane; d < BINS; d += 32) whist[w][d] = 0;
+  for (int d = threadIdx.x; d < BINS; d += RS_THREADS) gpos[d] = offs[(int64_t)d * ntiles + tile];
+  K k[ITEMS];
+  uint32_t v[ITEMS];
+  int loc[ITEMS];
+#pragma unroll
+  for (int i = 0; i < ITEMS; i++) {
+    const int64_t j = base + (int64_t)w * PER_WARP + i * 32 + lane;
+    const bool ok = j < n;
+    k[i] = ok ? keys[j] : K(0);
+    v[i] = ok ? (vals ? vals[j] : (uint32_t)j) : 0u;
+  }
+  __syncwarp();
+  const unsigned lt = lanemask_lt();
+#pragma unroll
+  for (int i = 0; i < ITEMS; i++) {
+    const int64_t j = base + (int64_t)w * PER_WARP + i * 32 + lane;
+    const unsigned valid = __ballot_sync(FULL_MASK, j < n);
+    const unsigned d = (unsigned)(k[i] >> shift) & (BINS - 1);
+#if RS_MATCH
+    const unsigned peers = __match_any_sync(FULL_MASK, j < n ? d : (1u << RB) + lane) & valid;
+#else
+    const unsigned peers = multisplit_peers<RB>(d, valid);
+#endif
+    int b = 0;
+    if (j < n) b = whist[w][d];
+    loc[i] = b + __popc(peers & lt);
+    __syncwarp();
+    if (j < n && (peers & lt) == 0) whist[w][d] = b + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  // per digit: exclusive prefix over warps; the tile's count of the digit
+  for (int d = threadIdx.x; d < BINS; d += RS_THREADS) {
+    int32_t run = 0;
+#pragma unroll
+    for (int ww = 0; ww < RS_WARPS; ww++) {
+      const int32_t t = whist[ww][d];
+      whist[ww][d] = run;
+      run += t;
+    }
+    dstart[d] = run;
+  }
+  __syncthreads();
+  // exclusive scan of the tile's digit counts: each warp scans BINS / RS_WARPS
+  {
+    constexpr int PER = BINS / RS_WARPS;  // contiguous digits per warp (>= 32)
+    int32_t c = 0;
+    for (int ch = 0; ch < PER; ch += 32) {
+      const int d = w * PER + ch + lane;
+      const int32_t x = dstart[d];
+      const int32_t xi = warp_incl_scan_add(x);
+      dstart[d] = c + xi - x;
+      c += __shfl_sync(FULL_MASK, xi, 31);
+    }
+    if (lane == 0) wtot[w] = c;
+    __syncthreads();
+    int32_t add = 0;
+    for (int ww = 0; ww < w; ww++) add += wtot[ww];
+    for (int ch = 0; ch < PER; ch += 32) dstart[w * PER + ch + lane] += add;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < ITEMS; i++) {
+    const int64_t j = base + (int64_t)w * PER_WARP + i * 32 + lane;
+    if (j < n) {
+      const unsigned d = (unsigned)(k[i] >> shift) & (BINS - 1);
+      const int pos = dstart[d] + whist[w][d] + loc[i];
+      sk[pos] = k[i];
+      sv[pos] = v[i];
+    }
+  }
+  __syncthreads();
+  int64_t cnt = n - base;
+  if (cnt > TILE) cnt = TILE;
+  for (int i = threadIdx.x; i < cnt; i += RS_THREADS) {
+    const K key = sk[i];
+    const unsigned d = (unsigned)(key >> shift) & (BINS - 1);
+    const int64_t pos = (int64_t)gpos[d] + (i - dstart[d]);
+    okeys[pos] = key;
+    ovals[pos] = sv[i];
+  }
+}
+
+__global__ void k_rs_iota(uint32_t *v, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    v[i] = (uint32_t)i;
+}
+
+// stable sort of (kin, vin) on key bits [0, bits) into (kout, vout); vin ==
+// nullptr sorts the positions 0..n-1.  kin/vin may alias kout/vout.
 template <typename K, int ITEMS>
+static int radix_sort_rts(mp_ctx *ctx, const K *kin, const uint32_t *vin, K *kout, uint32_t *vout, int64_t n,
+                          int bits, mp_err *err) {
+  constexpr int RB = 8, BINS = 1 << RB;
+  constexpr int TILE = RS_THREADS * ITEMS;
+  cudaStream_t st = ctx->stream;
+  if (n <= 0) return MP_OK;
+  if (n > (int64_t)INT32_MAX) {
+    mp_set_err(err, MP_E_UNSUPPORTED, 0, n, 0, "radix sort of more than 2^31 keys");
+    return MP_E_UNSUPPORTED;
+  }
+  const int passes = bits <= 0 ? 0 : (bits + RB - 1) / RB;
+  if (passes == 0) {
+    if (kout != kin) CUDA_TRY(cudaMemcpyAsync(kout, kin, n * sizeof(K), cudaMemcpyDeviceToDevice, st));
+    if (!vin) LAUNCH(ctx, k_rs_iota, grid_for(n, 256), 256, 0, vout, n);
+    else if (vout != vin) CUDA_TRY(cudaMemcpyAsync(vout, vin, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+    return MP_OK;
+  }
+  const int32_t ntiles = (int32_t)((n + TILE - 1) / TILE);
+  DBuf<K> ka, kb;
+  DBuf<uint32_t> va, vb;
+  DBuf<int32_t> mat;
+  CUDA_TRY(mat.alloc((int64_t)BINS * ntiles, st));
+  const bool alias = kout == kin || (vin && vout == vin);
+  // pass p reads src and writes dst; the last pass writes the caller's
+  // output unless it aliases the input of a single pass
+  const int need = passes > 1 ? 2 : (alias ? 1 : 0);
+  if (need >= 1) { CUDA_TRY(ka.alloc(n, st)); CUDA_TRY(va.alloc(n, st)); }
+  if (need >= 2 && passes > 2) { CUDA_TRY(kb.alloc(n, st)); CUDA_TRY(vb.alloc(n, st)); }
+  const size_t smem = (size_t)TILE * (sizeof(K) + sizeof(uint32_t));
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_rs_scatter<K, RB, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_set = true;
+  }
+  const K *sk = kin;
+  const uint32_t *sv = vin;
+  for (int p = 0; p < passes; p++) {
+    K *dk;
+    uint32_t *dv;
+    const bool last = p == passes - 1;
+    if (last && !(passes == 1 && alias)) { dk = kout; dv = vout; }
+    else if ((p & 1) == 0) { dk = ka.p; dv = va.p; }
+    else { dk = kb.p; dv = vb.p; }
+    const int shift = RB * p;
+    LAUNCH(ctx, (k_rs_hist<K, RB, ITEMS>), (unsigned)ntiles, RS_THREADS, 0, sk, n, shift, ntiles, mat.p);
+    int rc = dev_exclusive_scan<int32_t>(ctx, mat.p, mat.p, (int64_t)BINS * ntiles, nullptr, err);
+    if (rc) return rc;
+    LAUNCH(ctx, (k_rs_scatter<K, RB, ITEMS>), (unsigned)ntiles, RS_THREADS, smem, sk, sv, dk, dv, n, shift, ntiles,
+           mat.p);
+    sk = dk;
+    sv = dv;
+  }
+  if (sk != kout) {
+    CUDA_TRY(cudaMemcpyAsync(kout, sk, n * sizeof(K), cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(vout, sv, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+  }
+  return MP_OK;
+}
+
+int dev_radix_sort_u32_iota(mp_ctx *ctx, const uint32_t *kin, uint32_t *kout, uint32_t *vout, int64_t n, int bits,
+                            mp_err *err) {
+  return radix_sort_rts<uint32_t, RS_RTS_ITEMS32>(ctx, kin, nullptr, kout, vout, n, bits, err);
+}
+
+template <typename K, int ITEMS, int RTS_ITEMS>
 static int radix_sort_impl(mp_ctx *ctx, K *keys, uint32_t *vals, int64_t n, int bits, mp_err *err) {
   if (n <= 1 || bits <= 0) return MP_OK;
+  if (!RS_ONESWEEP && n >= RS_RTS_MIN_N) return radix_sort_rts<K, RTS_ITEMS>(ctx, keys, vals, keys, vals, n, bits, err);
   if (n > (int64_t)OS_MASK) {
     mp_set_err(err, MP_E_UNSUPPORTED, 0, n, 0, "radix sort of more than 2^30 keys");
     return MP_E_UNSUPPORTED;
@@ -427,9 +684,9 @@ static int radix_sort_impl(mp_ctx *ctx, K *keys, uint32_t *vals, int64_t n, int 
 }
 
 int dev_radix_sort_u32(mp_ctx *ctx, uint32_t *keys, uint32_t *vals, int64_t n, int bits, mp_err *err) {
-  return radix_sort_impl<uint32_t, RS_ITEMS32>(ctx, keys, vals, n, bits, err);
+  return radix_sort_impl<uint32_t, RS_ITEMS32, RS_RTS_ITEMS32>(ctx, keys, vals, n, bits, err);
 }
 
 int dev_radix_sort_u64(mp_ctx *ctx, uint64_t *keys, uint32_t *vals, int64_t n, int bits, mp_err *err) {
-  return radix_sort_impl<uint64_t, 8>(ctx, keys, vals, n, bits, err);
+  return radix_sort_impl<uint64_t, 8, 8>(ctx, keys, vals, n, bits, err);
 }

@@ -82,12 +82,37 @@ def next_point(pt: int) -> int:
     return pt + 1
 
 
-def plan_actions(profile, selection, limit_bytes: int, points, slot_of) -> tuple[list[SwapAction], list[dict]]:
+def schedule_in_events(profile, sim) -> dict[str, int]:
+    """Window event index at which the reference's replay starts each
+    swap-in: the first op whose replayed start time (natural time plus the
+    delays ``simulate`` charged before it, swapsim.py:303-340) is at or after
+    the final schedule's ``t_start_in`` (swapsim.py:84-96).  Spanning
+    candidates (swap-in in the next iteration) are not mapped."""
+    tau = np.asarray(profile.op_times_us, np.float64)
+    delay = np.zeros(len(tau), np.float64)
+    w0 = profile.window[0]
+    for d in sim.delayed_ops:
+        delay[d.index - w0] += d.delay_us
+    actual = tau + np.cumsum(delay)
+    out = {}
+    for e in sim.schedule.events:
+        c = sim.schedule.candidates[e.var]
+        if c.spans_iterations:
+            continue
+        out[e.var] = int(np.searchsorted(actual, e.t_start_in - 1e-6, side="left"))
+    return out
+
+
+def plan_actions(profile, selection, limit_bytes: int, points, slot_of,
+                 in_events: dict | None = None) -> tuple[list[SwapAction], list[dict]]:
     """Absence of each selected variable, in selection (priority) order:
     from the first to the last event of its access gap where the load,
     with the absences decided so far, is still above the limit.  Leaving as
     late and returning as early as the limit allows keeps the stalls (the
     copy/compute event waits) as short as the memory target permits.
+    With ``in_events`` (``schedule_in_events``) a swap-in is issued at the
+    reference schedule's start instead, or as soon after it as the pool
+    bytes are free, and never after the op that waits for it.
     Returns the executable actions and the skipped ones with the reason."""
     loads = np.asarray(profile.load.loads, np.int64).copy()
     acts, skipped = [], []
@@ -112,8 +137,13 @@ def plan_actions(profile, selection, limit_bytes: int, points, slot_of) -> tuple
             skipped.append({"var": c.var, "why": "no absence window at op granularity"})
             continue
         loads[a:b] -= c.size
+        issue_in = int(next_point(points[b - 1]))
+        if in_events is not None and c.var in in_events:
+            ev = in_events[c.var]
+            if ev < len(points):
+                issue_in = max(issue_in, min(int(points[ev]), int(points[r2])))
         acts.append(SwapAction(c.var, slot_of[c.var], int(c.size), r1, a, b, r2, int(next_point(points[r1])),
-                               int(points[a]), int(next_point(points[b - 1])), int(points[r2])))
+                               int(points[a]), issue_in, int(points[r2])))
     return acts, skipped
 
 
@@ -256,7 +286,9 @@ class SwapExecutor:
             self.host.append(h)
             self.dev.append((base + offsets[x.var], n))
             self.off.append(int(offsets[x.var]))
-            ev = {k: torch.cuda.Event() for k in ("out_src", "out_done", "in_src", "in_done")}
+            ev = {k: torch.cuda.Event() for k in ("out_src", "in_src")}
+            # timed: the last iteration's copy durations (copy_stats)
+            ev.update({k: torch.cuda.Event(enable_timing=True) for k in ("out_t0", "out_done", "in_t0", "in_done")})
             x._ev = ev
             for pt, fn in ((x.issue_out, self._issue_out), (x.wait_out, self._wait_out),
                            (x.issue_in, self._issue_in), (x.wait_in, self._wait_in)):
@@ -306,6 +338,7 @@ class SwapExecutor:
         x = self.actions[i]
         x._ev["out_src"].record(self.compute)
         self.s_out.wait_event(x._ev["out_src"])
+        x._ev["out_t0"].record(self.s_out)
         _copy(self.host[i], self.dev[i], d2h=True, stream=self.s_out)
         x._ev["out_done"].record(self.s_out)
         self.bytes_out += x.size
@@ -323,12 +356,24 @@ class SwapExecutor:
                                "(the run's lifetimes drifted from the plan)")
         x._ev["in_src"].record(self.compute)
         self.s_in.wait_event(x._ev["in_src"])
+        x._ev["in_t0"].record(self.s_in)
         _copy(self.host[i], self.dev[i], d2h=False, stream=self.s_in)
         x._ev["in_done"].record(self.s_in)
         self.bytes_in += x.size
 
     def _wait_in(self, i):
         self.compute.wait_event(self.actions[i]._ev["in_done"])
+
+    def copy_stats(self) -> dict:
+        """Bytes and copy-stream busy time of the LAST iteration's copies
+        (call after a synchronize): the achieved host-link rate of the
+        executed plan, per direction."""
+        out = {}
+        for d, (t0, t1) in (("d2h", ("out_t0", "out_done")), ("h2d", ("in_t0", "in_done"))):
+            ms = sum(x._ev[t0].elapsed_time(x._ev[t1]) for x in self.actions)
+            nb = sum(x.size for x in self.actions)
+            out[d] = {"bytes": int(nb), "busy_ms": ms, "bytes_per_s": nb / (ms * 1e-3) if ms > 0 else None}
+        return out
 
     def begin(self):
         self.k = 0

@@ -13,7 +13,10 @@ CUDA allocation):
    model.
 4. For each memory limit (fraction of the traced peak load) and selection
    mode — the reference's SWDOA selection among the executable candidates;
-   the same restricted to candidates whose round trip fits their gap; and
+   the same with each swap-in issued at the reference schedule's start
+   (``reference_schedule``: the replayed op at ``t_start_in``, no earlier
+   than its pool bytes are free); the same restricted to candidates whose
+   round trip fits their gap; and
    ``swapexec.select_window_fits`` (ours: copies must fit the executor's
    windows at the measured link rates, optionally with a 4 % stall budget) —
    schedule, simulation (predicted overhead), mapping onto op-granular hook
@@ -177,8 +180,8 @@ def main():
     ms_hook2, _l, _x, _p, _s = run([], hooked=True)
     fit_cands = [c for c in exec_cands if c.gap_us >= c.delta_out_us + c.delta_in_us]
     rows = []
-    pools = {"reference_selection": exec_cands, "transfer_fits_gap": fit_cands, "window_fits": exec_cands,
-             "window_fits_stall4pct": exec_cands}
+    pools = {"reference_selection": exec_cands, "reference_schedule": exec_cands, "transfer_fits_gap": fit_cands,
+             "window_fits": exec_cands, "window_fits_stall4pct": exec_cands}
     for mode in [m for m in a.modes.split(",") if m]:
         pool = pools[mode]
         for frac in [float(x) for x in a.fracs.split(",") if x]:
@@ -203,9 +206,14 @@ def main():
                 # still runs the selection (its pool layout is the cap)
                 row["sim_limit_deadlock"] = True
                 sim = swapsim.simulate(sched, prof, None)
-            acts, skipped = swapexec.plan_actions(prof, sel, limit, points, slot_of)
+            in_ev = swapexec.schedule_in_events(prof, sim) if mode == "reference_schedule" else None
+            acts, skipped = swapexec.plan_actions(prof, sel, limit, points, slot_of, in_events=in_ev)
             ms, losses, ex, plan, st = run(acts)
             by = {c.var: c for c in sel}
+            # the reference's replay of just the executed subset, no limit:
+            # the transfer-bound overhead of the copies that actually run
+            exe = [by[x.var] for x in acts]
+            sim_x = swapsim.simulate(swapsim.build_schedule(exe, prof), prof, None) if exe else None
             reasons = {}
             for sk in skipped:
                 reasons[sk["why"]] = reasons.get(sk["why"], 0) + 1
@@ -215,11 +223,13 @@ def main():
                 "executed_planned_peak_bytes": autoswap.planned_peak([by[x.var] for x in acts], prof),
                 "swap_bytes_per_iter": int(sum(x.size for x in acts)),
                 "predicted_overhead_pct": sim.overhead_pct, "predicted_peak_bytes": sim.achieved_peak_bytes,
+                "predicted_executed_overhead_pct": sim_x.overhead_pct if sim_x else 0.0,
                 "iter_ms": ms, "measured_overhead_pct": (ms / ms_hook - 1) * 100,
                 "pool_footprint_bytes": plan.footprint_bytes, "pool_policy": plan.policy,
                 "pool_arc_peak_bytes": plan.arc_peak_bytes,
                 "pool_reduction_vs_noswap": 1 - plan.footprint_bytes / plan0.footprint_bytes,
                 "losses_equal_unswapped": losses == losses_plain, "allocator": st,
+                "link": ex.copy_stats() if acts else None,
             })
             rows.append(row)
     load_min = swapsim.compute_load_min(prof, exec_cands)
