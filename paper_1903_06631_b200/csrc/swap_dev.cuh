@@ -699,7 +699,11 @@ struct PeakCurve {
   }
 };
 
-// replay state (lane 0 owns it)
+// replay state (lane 0 owns it).  The heads of both transfer queues — the
+// next swap-out completion and the next planned swap-in with its size and
+// duration — are cached in registers and refreshed only when a queue moves,
+// so probing for the next transfer (every op, usually "nothing before this
+// op") costs no shared-memory round trips.
 template <class CurveT>
 struct Replay {
   int64_t k_in, k_out, ncomp, n;
@@ -708,37 +712,66 @@ struct Replay {
   int64_t ndl;
   bool has_limit;
   int64_t limit;
+  double nx_t;      // comp_t[k_out], or INF when k_out >= ncomp
+  int64_t nx_sz;    // comp_sz[k_out]
+  int64_t hv;       // in_order[k_in], or -1 when k_in >= n
+  double hv_plan, hv_din;
+  int64_t hv_size;
 };
+
+template <class CurveT>
+__device__ __forceinline__ void rp_out_head(Replay<CurveT> &R, const SimScratch &S) {
+  if (R.k_out < R.ncomp) {
+    R.nx_t = S.comp_t[R.k_out];
+    R.nx_sz = S.comp_sz[R.k_out];
+  } else {
+    R.nx_t = INF_D;
+  }
+}
+
+template <class CurveT>
+__device__ __forceinline__ void rp_in_head(Replay<CurveT> &R, const SimScratch &S, const CandView &c,
+                                           const int32_t *sel) {
+  if (R.k_in < R.n) {
+    R.hv = S.in_order[R.k_in];
+    R.hv_plan = S.plan_in[R.hv];
+    const int32_t ci = sel[R.hv];
+    R.hv_size = c.size[ci];
+    R.hv_din = c.din[ci];
+  } else {
+    R.hv = -1;
+  }
+}
 
 // _Replay._step, swapsim.py:256-282: 1 stepped, 0 beyond horizon,
 // -1 IndexError (the reference defect at swapsim.py:266-267)
 template <class CurveT>
 __device__ __forceinline__ int rp_step(Replay<CurveT> &R, SimScratch &S, const CandView &c, const int32_t *sel, double horizon) {
-  double t_out = R.k_out < R.ncomp ? S.comp_t[R.k_out] : INF_D;
+  const double t_out = R.nx_t;
   double t_in = INF_D;
-  int64_t hv = -1;
-  if (R.k_in < R.n) {
-    hv = S.in_order[R.k_in];
-    double start = pymax(pymax(S.plan_in[hv], R.in_busy), R.head_floor);
-    if (R.has_limit && R.cv.load + c.size[sel[hv]] > R.limit) start = INF_D;
+  if (R.hv >= 0) {
+    double start = pymax(pymax(R.hv_plan, R.in_busy), R.head_floor);
+    if (R.has_limit && R.cv.load + R.hv_size > R.limit) start = INF_D;
     t_in = start;
   }
   double t = pymin(t_out, t_in);
   if (t > horizon) return 0;
   if (t_out <= t_in) {
     if (R.k_out >= R.ncomp) return -1;
-    int64_t sz = S.comp_sz[R.k_out++];
-    R.cv.load -= sz;
+    R.k_out++;
+    R.cv.load -= R.nx_sz;
     R.head_floor = pymax(R.head_floor, t_out);
     R.cv.point(t_out);
+    rp_out_head(R, S);
   } else {
-    R.cv.load += c.size[sel[hv]];
+    R.cv.load += R.hv_size;
     R.cv.point(t_in);
-    double end = t_in + c.din[sel[hv]];
+    double end = t_in + R.hv_din;
     R.in_busy = end;
-    S.in_done[hv] = end;
-    S.in_has[hv] = 1;
+    S.in_done[R.hv] = end;
+    S.in_has[R.hv] = 1;
     R.k_in++;
+    rp_in_head(R, S, c, sel);
   }
   return 1;
 }
@@ -803,19 +836,25 @@ __device__ int replay_run(Replay<CurveT> &R, SimScratch &S, const ProfView &P, c
     R.k_in = 0; R.in_busy = 0.0; R.head_floor = 0.0; R.ncomp = 0; R.k_out = 0;
     R.out_busy = 0.0; R.delay = 0.0; R.ndl = 0;
     R.cv.reset(l0);
+    rp_out_head(R, S);
+    rp_in_head(R, S, c, sel);
     int64_t filled = 0;
     for (int64_t w = 0; w < nwords && status == MP_OK; w++) {
       uint32_t bits = S.busy_op[w];
       while (bits) {
         const int64_t r = w * 32 + __ffs(bits) - 1;
         bits &= bits - 1;
+        // this op's inputs, loaded together up front
+        const double tau_r = P.tau[r];
+        const int32_t wt = S.in_wait[r];
+        const int64_t dd = S.delta[r];
+        const int32_t trig = S.out_trigger[r];
         if (FILL_ACTUAL)
           for (; filled < r; filled++) S.actual[filled] = P.tau[filled] + R.delay;
-        double t0 = P.tau[r] + R.delay, t = t0;
+        double t0 = tau_r + R.delay, t = t0;
         int st;
         while ((st = rp_step(R, S, c, sel, t)) == 1) {}
         if (st < 0) { status = MP_E_SIM_INDEXERROR; break; }
-        int32_t wt = S.in_wait[r];
         if (wt >= 0) {
           int ws = 1;
           while (!S.in_has[wt]) {
@@ -834,7 +873,6 @@ __device__ int replay_run(Replay<CurveT> &R, SimScratch &S, const ProfView &P, c
             if (st < 0) { status = MP_E_SIM_INDEXERROR; break; }
           }
         }
-        int64_t dd = S.delta[r];
         if (dd > 0 && R.has_limit) {
           while (R.cv.load + dd > R.limit) {
             if (R.k_out >= R.ncomp) {
@@ -842,8 +880,10 @@ __device__ int replay_run(Replay<CurveT> &R, SimScratch &S, const ProfView &P, c
               status = MP_E_SWAP_DEADLOCK;
               break;
             }
-            double t_free = S.comp_t[R.k_out];
-            int64_t sz = S.comp_sz[R.k_out++];
+            const double t_free = R.nx_t;
+            const int64_t sz = R.nx_sz;
+            R.k_out++;
+            rp_out_head(R, S);
             R.cv.load -= sz;
             R.head_floor = pymax(R.head_floor, t_free);
             R.cv.point(t_free);
@@ -868,15 +908,15 @@ __device__ int replay_run(Replay<CurveT> &R, SimScratch &S, const ProfView &P, c
             if (st < 0) { status = MP_E_SIM_INDEXERROR; break; }
           }
         }
-        int32_t trig = S.out_trigger[r];
         if (trig >= 0) {
           double op_end = r + 1 < p ? P.tau[r + 1] : P.duration;
-          double ready = t + (op_end - P.tau[r]);
+          double ready = t + (op_end - tau_r);
           double start = pymax(ready, R.out_busy);
           R.out_busy = start + c.dout[sel[trig]];
           S.comp_t[R.ncomp] = R.out_busy;
           S.comp_sz[R.ncomp] = c.size[sel[trig]];
           R.ncomp++;
+          if (R.k_out == R.ncomp - 1) { R.nx_t = R.out_busy; R.nx_sz = S.comp_sz[R.k_out]; }
         }
       }
     }
