@@ -417,6 +417,28 @@ def run_sweep_bench(args, rank, world, local_rank, hbm_gbs):
         out["parity"] = {"gathered_equal_single_rank": bool(
             one.traces.tobytes() == full.traces.tobytes() and one.budgets.tobytes() == full.budgets.tobytes()
             and np.array_equal(one.offsets, full.offsets) and np.array_equal(one.cand_order, full.cand_order))}
+    if rank == 0 and world == 1:
+        # strong-scaling evidence on one GPU: every rank's LPT shard of the
+        # batch timed as its own launch, one after another; a rank's kernel
+        # is the N-GPU step's device time when the ranks run side by side
+        # (no data-path collective), so max over ranks bounds the N-GPU
+        # kernel.  The floor is the longest single trace on its own.
+        def shard_ms(sub, reps=5):
+            d = sweep.DeviceSweep(sub)
+            d.run(params)
+            t = sorted(timed(lambda: d.run(params))[0] for _ in range(reps))
+            d.close()
+            return t[len(t) // 2]
+        proj = {}
+        for nw in (2, 4, 8):
+            per = [shard_ms(batch.subset(p)) for p in sweep.shard([batch.events_of(t) for t in range(batch.ntraces)], nw)]
+            proj[str(nw)] = {"max_rank_kernel_ms": max(per), "min_rank_kernel_ms": min(per),
+                             "speedup_vs_1": step_ms / max(per)}
+        big = int(np.argmax([batch.events_of(t) for t in range(batch.ntraces)]))
+        proj["largest_trace_alone_ms"] = shard_ms(batch.subset([big]))
+        proj["how"] = ("each rank's LPT shard launched alone on this GPU (median of 5, L2 flushed); "
+                       "no multi-GPU run: an N-GPU step's device time is its slowest rank")
+        out["shard_projection"] = proj
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         procs = os.cpu_count() or 1
         dt, chunks, outs = sweep_cpu_baseline(batch, params, procs)
