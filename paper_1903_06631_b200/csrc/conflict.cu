@@ -424,10 +424,197 @@ __global__ void k_prof_segs(int64_t nv, const int32_t *nseg, const int32_t *seg,
   }
 }
 
+// ---------------------------------------------------------------------------
+// Profile fast path.  A profile variable has one or two segments with bounds
+// in [0, period], so its effective intervals (at most two) get fixed slots
+// 2v, 2v+1 and need no counting pass or offset scan; one kernel computes
+// them, histograms their starts and ends for the counting sort (bounds are
+// op positions: base 0, range period + 1) and reduces the size-key range
+// the placement order needs, so the build reads back once before the
+// placement-order sort instead of twice.
+
+// effective intervals of one <= 2-segment variable (k_norm_count's rule):
+// returns their count, intervals in (a0, b0), (a1, b1)
+__device__ __forceinline__ int prof_effective(int ns, int4 sg, int32_t &a0, int32_t &b0, int32_t &a1, int32_t &b1) {
+  int32_t l0 = 0, h0 = 0, l1 = 0, h1 = 0;
+  int mm = 0;
+  for (int q = 0; q < ns; q++) {
+    const int32_t a = q ? sg.z : sg.x, b = q ? sg.w : sg.y;
+    if (b <= a) continue;
+    if (mm == 0) { l0 = a; h0 = b; }
+    else if (a < l0) { l1 = l0; h1 = h0; l0 = a; h0 = b; }
+    else { l1 = a; h1 = b; }
+    mm++;
+  }
+  int c = 0;
+  int32_t cur_end = INT32_MIN;
+  for (int k = 0; k < mm; k++) {
+    const int32_t lk = k ? l1 : l0;
+    if (lk < cur_end) continue;
+    int32_t ne = INT32_MAX;
+    if (h0 > lk && h0 < ne) ne = h0;
+    if (mm > 1 && h1 > lk && h1 < ne) ne = h1;
+    if (c == 0) { a0 = lk; b0 = ne; } else { a1 = lk; b1 = ne; }
+    c++;
+    cur_end = ne;
+  }
+  return c;
+}
+
+__global__ void k_prof_intervals(int64_t nv, const int32_t *nseg, const int32_t *seg, const int64_t *size,
+                                 int32_t *ea, int32_t *eb, int64_t *cnt, int32_t *hs, int32_t *he,
+                                 unsigned long long *kmm) {
+  unsigned long long lmn = ~0ull, lmx = 0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
+    const int4 sg = reinterpret_cast<const int4 *>(seg)[v];
+    int32_t a0 = -1, b0 = -1, a1 = -1, b1 = -1;
+    const int c = prof_effective(nseg[v], sg, a0, b0, a1, b1);
+    reinterpret_cast<int2 *>(ea)[v] = make_int2(c > 0 ? a0 : -1, c > 1 ? a1 : -1);
+    reinterpret_cast<int2 *>(eb)[v] = make_int2(b0, b1);
+    if (c > 0) { atomicAdd(&hs[a0], 1); atomicAdd(&he[b0], 1); }
+    if (c > 1) { atomicAdd(&hs[a1], 1); atomicAdd(&he[b1], 1); }
+    cnt[2 * v] = 0;
+    cnt[2 * v + 1] = 0;
+    const uint64_t k = desc_size_key(size[v]);
+    lmn = k < lmn ? k : lmn;
+    lmx = k > lmx ? k : lmx;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long x = __shfl_xor_sync(FULL_MASK, lmn, o), y = __shfl_xor_sync(FULL_MASK, lmx, o);
+    lmn = x < lmn ? x : lmn;
+    lmx = y > lmx ? y : lmx;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&kmm[0], lmn);
+    atomicMax(&kmm[1], lmx);
+  }
+}
+
+// slots in start order (counting sort; order among equal starts is free)
+__global__ void k_prof_scatter(int64_t nslots, const int32_t *ea, const int32_t *offs, int32_t *cur, uint32_t *perm) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nslots; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t x = ea[i];
+    if (x >= 0) perm[offs[x] + atomicAdd(&cur[x], 1)] = (uint32_t)i;
+  }
+}
+
+// k_iv_counts_dense with the slot's variable implicit (slot >> 1)
+__global__ void k_prof_counts(int64_t n, const uint32_t *perm, const int32_t *ea, const int32_t *eb,
+                              const int32_t *offs, const int32_t *cum_e, int64_t *cnt, const int32_t *rank,
+                              int32_t *sv) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t iid = perm[k];
+    const int64_t f = (int64_t)offs[eb[iid]] - k - 1;
+    const int64_t bw = k - cum_e[ea[iid] + 1];
+    cnt[iid] = f + bw;
+    const int32_t v = (int32_t)(iid >> 1);
+    sv[3 * k] = v;
+    sv[3 * k + 1] = rank[v];
+    sv[3 * k + 2] = (int32_t)f;
+  }
+}
+
+// row bounds from the slot scan, and the long-row scratch bound
+__global__ void k_prof_rows(int64_t nv, const int64_t *sub_off, int64_t *row_off, unsigned long long *need) {
+  unsigned long long s = 0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v <= nv; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r0 = sub_off[2 * v];
+    row_off[v] = r0;
+    if (v < nv) {
+      const int64_t d = sub_off[2 * v + 2] - r0;
+      if (d > 128) {
+        unsigned long long n2 = 64;
+        while (n2 < (unsigned long long)d) n2 <<= 1;
+        s += n2;
+      }
+    }
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(need, s);
+}
+
+static int build_csr_profile(mp_ctx *ctx, mp_dprofile *P, mp_dgraph *g, mp_err *err) {
+  cudaStream_t st = ctx->stream;
+  const int64_t nv = P->d.nvars, p = P->d.period, ns = 2 * nv;
+  CUDA_TRY(g->rank.alloc(nv, st));
+  CUDA_TRY(g->pcnt.alloc(nv, st));
+  StageTimer *tm = new StageTimer(ctx, MP_ST_CONFLICT_PREP);
+  DBuf<int32_t> ea, eb, hs, he, offs_s, cum_e, curs, sv, scur;
+  DBuf<int64_t> cnt, sub_off;
+  CUDA_TRY(ea.alloc(ns, st)); CUDA_TRY(eb.alloc(ns, st));
+  CUDA_TRY(hs.alloc(p + 2, st)); CUDA_TRY(he.alloc(p + 2, st));
+  CUDA_TRY(offs_s.alloc(p + 2, st)); CUDA_TRY(cum_e.alloc(p + 2, st)); CUDA_TRY(curs.alloc(p + 1, st));
+  CUDA_TRY(cnt.alloc(ns + 1, st)); CUDA_TRY(sub_off.alloc(ns + 1, st));
+  CUDA_TRY(cudaMemsetAsync(hs.p, 0, (p + 2) * 4, st));
+  CUDA_TRY(cudaMemsetAsync(he.p, 0, (p + 2) * 4, st));
+  CUDA_TRY(cudaMemsetAsync(curs.p, 0, (p + 1) * 4, st));
+  // d_small: [0..1] size-key range, [2] interval count, [3] arena need, [4] nnz
+  unsigned long long *d_kmm = (unsigned long long *)ctx->d_small;
+  int32_t *d_ni = (int32_t *)(ctx->d_small + 2);
+  CUDA_TRY(cudaMemsetAsync(d_kmm, 0xff, 8, st));
+  CUDA_TRY(cudaMemsetAsync(d_kmm + 1, 0, 8, st));
+  LAUNCH(ctx, k_prof_intervals, grid_for(nv, 256), 256, 0, nv, P->nseg.p, P->seg.p, P->size.p, ea.p, eb.p, cnt.p,
+         hs.p, he.p, d_kmm);
+  int rc = dev_exclusive_scan<int32_t>(ctx, hs.p, offs_s.p, p + 1, d_ni, err);
+  if (rc) return rc;
+  rc = dev_exclusive_scan<int32_t>(ctx, he.p, cum_e.p, p + 2, nullptr, err);
+  if (rc) return rc;
+  int64_t h[3];
+  rc = dev_read_n(ctx, ctx->d_small, h, 24, err);
+  if (rc) return rc;
+  const int64_t ni = (int32_t)h[2];
+  g->size_hi = (int64_t)(~(uint64_t)h[0] ^ 0x8000000000000000ull);
+  g->size_lo = (int64_t)(~(uint64_t)h[1] ^ 0x8000000000000000ull);
+  rc = placement_rank_sort(ctx, nv, g->size.p, nullptr, g->rank.p, (uint64_t)h[0], (uint64_t)h[1], err);
+  if (rc) return rc;
+  DBuf<uint32_t> perm;
+  CUDA_TRY(perm.alloc(ni, st)); CUDA_TRY(sv.alloc(3 * ni, st)); CUDA_TRY(scur.alloc(nv, st));
+  LAUNCH(ctx, k_prof_scatter, grid_for(ns, 256), 256, 0, ns, ea.p, offs_s.p, curs.p, perm.p);
+  LAUNCH(ctx, k_prof_counts, grid_for(ni, 256), 256, 0, ni, perm.p, ea.p, eb.p, offs_s.p, cum_e.p, cnt.p, g->rank.p,
+         sv.p);
+  int64_t *d_tot = ctx->d_small + 4;
+  rc = dev_exclusive_scan<int64_t>(ctx, cnt.p, sub_off.p, ns, d_tot, err);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(sub_off.p + ns, d_tot, 8, cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(g->row_off.alloc(nv + 1, st));
+  unsigned long long *d_arena = (unsigned long long *)(ctx->d_small + 3);
+  CUDA_TRY(cudaMemsetAsync(d_arena, 0, 8, st));
+  LAUNCH(ctx, k_prof_rows, grid_for(nv + 1, 256, 2048), 256, 0, nv, sub_off.p, g->row_off.p, d_arena);
+  int64_t h2[2];
+  rc = dev_read_n(ctx, ctx->d_small + 3, h2, 16, err);
+  if (rc) return rc;
+  g->nvars = nv;
+  g->nnz = h2[1];
+  g->arena_need = h2[0];
+  CUDA_TRY(g->col.alloc(g->nnz, st));
+  CUDA_TRY(cudaMemsetAsync(scur.p, 0, nv * 4, st));
+  CUDA_TRY(cudaMemsetAsync(g->pcnt.p, 0, nv * 4, st));
+  delete tm;
+  StageTimer fill(ctx, MP_ST_CONFLICT_FILL);
+  LAUNCH(ctx, k_iv_fill, grid_for(ni * 32, 256, 148 * 64), 256, 0, ni, sv.p, g->row_off.p, g->pcnt.p, scur.p,
+         g->col.p);
+  return MP_OK;
+}
+
+#ifndef CONFLICT_PROFILE_FAST
+#define CONFLICT_PROFILE_FAST 1
+#endif
+
 extern "C" int mp_conflict_from_profile(mp_ctx *ctx, mp_dprofile *P, mp_dgraph **out, mp_err *err) {
   CTX_GUARD(ctx);
   cudaStream_t st = ctx->stream;
   int64_t nv = P->d.nvars;
+  if (CONFLICT_PROFILE_FAST && nv > 0 && P->d.period + 1 <= 16 * nv + 4096 && 2 * nv < INT32_MAX) {
+    mp_dgraph *g = new mp_dgraph();
+    g->ctx = ctx;
+    CUDA_TRY(g->size.alloc(nv, st));
+    CUDA_TRY(cudaMemcpyAsync(g->size.p, P->size.p, nv * 8, cudaMemcpyDeviceToDevice, st));
+    int rc = build_csr_profile(ctx, P, g, err);
+    if (rc) { delete g; return rc; }
+    *out = g;
+    return MP_OK;
+  }
   DBuf<int64_t> so;
   DBuf<int32_t> lo, hi;
   CUDA_TRY(so.alloc(nv + 1, st)); CUDA_TRY(lo.alloc(2 * nv, st)); CUDA_TRY(hi.alloc(2 * nv, st));

@@ -105,6 +105,9 @@ struct mp_dgraph {
   int64_t size_lo = INT64_MIN, size_hi = INT64_MAX;  // vertex weight range (when the build knows it)
 };
 
+// descending size as an ascending unsigned key (placement order, smartpool.py:91-98)
+__device__ __forceinline__ uint64_t desc_size_key(int64_t s) { return ~((uint64_t)s ^ 0x8000000000000000ull); }
+
 int build_groups(mp_ctx *ctx, mp_dtrace *t, mp_err *err);
 int placement_rank(mp_ctx *ctx, int64_t V, const int64_t *size, const int64_t *tiekey, int32_t *rank,
                    mp_err *err);

@@ -436,8 +436,6 @@ __global__ void k_tie_keys(int64_t V, const int64_t *tiekey, uint64_t *keys, uin
   }
 }
 
-// descending size as an ascending unsigned key
-__device__ __forceinline__ uint64_t desc_size_key(int64_t s) { return ~((uint64_t)s ^ 0x8000000000000000ull); }
 
 __global__ void k_size_keys(int64_t V, const int64_t *size, const uint32_t *vals, uint64_t *keys,
                             unsigned long long *mn, unsigned long long *mx) {
