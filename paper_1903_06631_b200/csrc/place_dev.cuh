@@ -208,3 +208,133 @@ __device__ __forceinline__ void warp_bitonic_keys_rolled(uint64_t (&x)[K]) {
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Lane-major forms for 64-128 ranges: sorted position p = lane * K + r.  The
+// bitonic network is the same, with the low log2(K) index bits inside a
+// lane's registers: every stage with j < K is a register compare-exchange
+// (13 of the 28 stages for K = 4, against 3 in the register-major form),
+// and _pick_offset becomes ONE pass: a lane's K consecutive ranges in
+// order, one warp max-scan of the lanes' end maxima, one reduction.
+
+template <int K>
+__device__ __forceinline__ void lm_cx_regs(uint64_t (&x)[K], int j, int k, int lane) {
+#pragma unroll
+  for (int r = 0; r < K; r++) {
+    if ((r & j) == 0) {
+      const int r2 = r | j;
+      const bool up = ((lane * K + r) & k) == 0;
+      const bool sw = (x[r2] < x[r]) == up;
+      const uint64_t a = sw ? x[r2] : x[r], b = sw ? x[r] : x[r2];
+      x[r] = a;
+      x[r2] = b;
+    }
+  }
+}
+
+// unrolled
+template <int K>
+__device__ __forceinline__ void warp_bitonic_keys_lm_unrolled(uint64_t (&x)[K]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 2; k <= 32 * K; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j < K) {
+        lm_cx_regs<K>(x, j, k, lane);
+      } else {
+        const int jl = j / K;
+        const bool lower = (lane & jl) == 0;
+#pragma unroll
+        for (int r = 0; r < K; r++) {
+          const uint64_t o = __shfl_xor_sync(FULL_MASK, x[r], jl);
+          const bool up = ((lane * K + r) & k) == 0;
+          x[r] = cx_key(x[r], o, lower == up);
+        }
+      }
+    }
+  }
+}
+
+// rolled stage loops (runtime k, j); j < K branches to the register form
+template <int K>
+__device__ __forceinline__ void warp_bitonic_keys_lm(uint64_t (&x)[K]) {
+  static_assert(K == 2 || K == 4, "lane-major network is for 64 or 128 keys");
+  const int lane = threadIdx.x & 31;
+#pragma unroll 1
+  for (int k = 2; k <= 32 * K; k <<= 1) {
+#pragma unroll 1
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j < K) {
+        if (K == 4 && j == 2) lm_cx_regs<K>(x, 2, k, lane);
+        else lm_cx_regs<K>(x, 1, k, lane);
+      } else {
+        const int jl = j / K;
+        const bool lower = (lane & jl) == 0;
+#pragma unroll
+        for (int r = 0; r < K; r++) {
+          const uint64_t o = __shfl_xor_sync(FULL_MASK, x[r], jl);
+          const bool up = ((lane * K + r) & k) == 0;
+          x[r] = cx_key(x[r], o, lower == up);
+        }
+      }
+    }
+  }
+}
+
+// _pick_offset over 32 * K sorted ranges held lane-major (s[r], e[r] of
+// position lane * K + r, valid below m); returns the offset
+template <int K>
+__device__ __forceinline__ int64_t hole_lm(const int64_t (&s)[K], const int64_t (&e)[K], int m, int64_t need,
+                                           int policy) {
+  const int lane = threadIdx.x & 31;
+  int64_t lmax = INT64_MIN;
+#pragma unroll
+  for (int r = 0; r < K; r++)
+    if (lane * K + r < m && e[r] > lmax) lmax = e[r];
+  const int64_t incl = warp_incl_scan_max(lmax);
+  int64_t excl = __shfl_up_sync(FULL_MASK, incl, 1);
+  if (lane == 0) excl = INT64_MIN;
+  int64_t run = excl > 0 ? excl : 0;
+  bool mine = false;
+  int64_t my_off = 0, bl = INT64_MAX, bo = INT64_MAX;
+#pragma unroll
+  for (int r = 0; r < K; r++) {
+    if (lane * K + r >= m) continue;
+    if (s[r] > run && s[r] - run >= need) {
+      const int64_t len = s[r] - run;
+      if (!mine) { mine = true; my_off = run; }
+      if (len < bl || (len == bl && run < bo)) { bl = len; bo = run; }
+    }
+    if (e[r] > run) run = e[r];
+  }
+  const int64_t cmax = __shfl_sync(FULL_MASK, incl, 31);
+  const int64_t top = cmax > 0 ? cmax : 0;
+  if (policy == 0) {
+    const unsigned bal = __ballot_sync(FULL_MASK, mine);
+    return bal ? __shfl_sync(FULL_MASK, my_off, __ffs(bal) - 1) : top;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const int64_t ol = __shfl_xor_sync(FULL_MASK, bl, o), oo = __shfl_xor_sync(FULL_MASK, bo, o);
+    if (ol < bl || (ol == bl && oo < bo)) { bl = ol; bo = oo; }
+  }
+  return bl != INT64_MAX ? bo : top;
+}
+
+// bitonic sort of the first N (<= 32) lanes' keys, one per lane: lanes >= N
+// hold the all-ones padding already, so the 32-key result is sorted too
+template <int N>
+__device__ __forceinline__ void warp_bitonic_keys_first(uint64_t &x) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 2; k <= N; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const uint64_t o = __shfl_xor_sync(FULL_MASK, x, j);
+      const bool up = (lane & k) == 0;
+      const bool lower = (lane & j) == 0;
+      x = cx_key(x, o, lower == up);
+    }
+  }
+}

@@ -51,6 +51,18 @@
 #ifndef PLACE_BACKOFF
 #define PLACE_BACKOFF 1    // exponential idle backoff
 #endif
+#ifndef PLACE_LANE_MAJOR
+#define PLACE_LANE_MAJOR 1  // 64-128 predecessors: lane-major network + one-pass hole scan
+#endif
+#ifndef PLACE_LM_KMIN
+#define PLACE_LM_KMIN 2  // 4: only the 65-128 rows (1.28 ms), 2: also 33-64 (1.21 ms vs 1.34 register-major)
+#endif
+#ifndef PLACE_SHORT_NETS
+#define PLACE_SHORT_NETS 1  // rows of <= 8 / 16 predecessors sort with an 8 / 16-wide network
+#endif
+#ifndef PLACE_LM_K4_UNROLLED
+#define PLACE_LM_K4_UNROLLED 0
+#endif
 #ifndef PLACE_K4_ROLLED
 #define PLACE_K4_ROLLED 1  // rolled stage loops for 65..128 predecessors
 #endif
@@ -162,8 +174,35 @@ __device__ __forceinline__ int64_t place_reg(const PlaceArgs &a, int64_t rb, int
   if (!ok) return 0;
   lvl = warp_max_i32(lv) + 1;
   if (lane == 0) PT_STAMP(3, a.dbg_v);
-  if constexpr (K <= 2 || !PLACE_K4_ROLLED) warp_bitonic_keys<K>(x);
-  else warp_bitonic_keys_rolled<K>(x);
+  if constexpr (PLACE_LANE_MAJOR && K >= PLACE_LM_KMIN) {
+    // lane-major network and one-pass hole scan (place_dev.cuh)
+    if constexpr (K == 2 || PLACE_LM_K4_UNROLLED) warp_bitonic_keys_lm_unrolled<K>(x);
+    else warp_bitonic_keys_lm<K>(x);
+    if (lane == 0) PT_STAMP(4, a.dbg_v);
+    int64_t ss[K], es[K];
+#pragma unroll
+    for (int r = 0; r < K; r++) {
+      const int src = (int)(x[r] & ((1u << IB) - 1));
+      es[r] = INT64_MIN;
+#pragma unroll
+      for (int q = 0; q < K; q++) {
+        const int64_t t = __shfl_sync(FULL_MASK, e[q], src & 31);
+        if ((src >> 5) == q) es[r] = t;
+      }
+      ss[r] = (int64_t)(x[r] >> IB);
+    }
+    return hole_lm<K>(ss, es, m, need, a.policy);
+  }
+  if constexpr (K == 1 && PLACE_SHORT_NETS) {
+    // a network only as wide as the row (m <= 8 / 16: 6 / 10 stages, not 15)
+    if (m <= 8) warp_bitonic_keys_first<8>(x[0]);
+    else if (m <= 16) warp_bitonic_keys_first<16>(x[0]);
+    else warp_bitonic_keys_first<32>(x[0]);
+  } else if constexpr (K <= 2 || !PLACE_K4_ROLLED) {
+    warp_bitonic_keys<K>(x);
+  } else {
+    warp_bitonic_keys_rolled<K>(x);
+  }
   if (lane == 0) PT_STAMP(4, a.dbg_v);
   HoleState h{0, 0, 0, false};
 #pragma unroll
