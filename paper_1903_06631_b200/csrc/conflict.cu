@@ -612,6 +612,7 @@ extern "C" int mp_conflict_from_profile(mp_ctx *ctx, mp_dprofile *P, mp_dgraph *
     CUDA_TRY(cudaMemcpyAsync(g->size.p, P->size.p, nv * 8, cudaMemcpyDeviceToDevice, st));
     int rc = build_csr_profile(ctx, P, g, err);
     if (rc) { delete g; return rc; }
+    g->peak_hint = P->d.peak_bytes;
     *out = g;
     return MP_OK;
   }
@@ -628,6 +629,7 @@ extern "C" int mp_conflict_from_profile(mp_ctx *ctx, mp_dprofile *P, mp_dgraph *
   // placement tie-break is the vertex index
   int rc = build_csr(ctx, nv, so.p, lo.p, hi.p, false, g, err);
   if (rc) { delete g; return rc; }
+  g->peak_hint = P->d.peak_bytes;
   *out = g;
   return MP_OK;
 }

@@ -103,6 +103,7 @@ struct mp_dgraph {
   DBuf<int32_t> pcnt;     // row prefix holding the placement predecessors
   int64_t arena_need = 0; // scratch ranges for rows longer than 128
   int64_t size_lo = INT64_MIN, size_hi = INT64_MAX;  // vertex weight range (when the build knows it)
+  int64_t peak_hint = -1;  // peak load of the profile the graph came from (a footprint lower bound), -1 unknown
 };
 
 // descending size as an ascending unsigned key (placement order, smartpool.py:91-98)

@@ -338,3 +338,46 @@ __device__ __forceinline__ void warp_bitonic_keys_first(uint64_t &x) {
     }
   }
 }
+
+// hole_lm on 32-bit values (every end below 2^31): one shuffle per scan
+// level and redux reductions
+template <int K>
+__device__ __forceinline__ int64_t hole_lm32(const int32_t (&s)[K], const int32_t (&e)[K], int m, int32_t need,
+                                             int policy) {
+  const int lane = threadIdx.x & 31;
+  int32_t lmax = INT32_MIN;
+#pragma unroll
+  for (int r = 0; r < K; r++)
+    if (lane * K + r < m && e[r] > lmax) lmax = e[r];
+  int32_t incl = lmax;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t u = __shfl_up_sync(FULL_MASK, incl, o);
+    if (lane >= o && u > incl) incl = u;
+  }
+  int32_t excl = __shfl_up_sync(FULL_MASK, incl, 1);
+  if (lane == 0) excl = INT32_MIN;
+  int32_t run = excl > 0 ? excl : 0;
+  bool mine = false;
+  int32_t my_off = 0, bl = INT32_MAX, bo = INT32_MAX;
+#pragma unroll
+  for (int r = 0; r < K; r++) {
+    if (lane * K + r >= m) continue;
+    if (s[r] > run && s[r] - run >= need) {
+      const int32_t len = s[r] - run;
+      if (!mine) { mine = true; my_off = run; }
+      if (len < bl || (len == bl && run < bo)) { bl = len; bo = run; }
+    }
+    if (e[r] > run) run = e[r];
+  }
+  const int32_t cmax = __shfl_sync(FULL_MASK, incl, 31);
+  const int32_t top = cmax > 0 ? cmax : 0;
+  if (policy == 0) {
+    const unsigned bal = __ballot_sync(FULL_MASK, mine);
+    return bal ? __shfl_sync(FULL_MASK, my_off, __ffs(bal) - 1) : top;
+  }
+  // (length, offset) minimum: non-negative, so the unsigned redux order is right
+  const unsigned ml = __reduce_min_sync(FULL_MASK, (unsigned)bl);
+  const unsigned mo = __reduce_min_sync(FULL_MASK, (unsigned)bl == ml ? (unsigned)bo : 0xffffffffu);
+  return ml != (unsigned)INT32_MAX ? (int64_t)mo : (int64_t)top;
+}

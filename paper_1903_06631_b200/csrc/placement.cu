@@ -57,6 +57,9 @@
 #ifndef PLACE_LM_KMIN
 #define PLACE_LM_KMIN 2  // 4: only the 65-128 rows (1.28 ms), 2: also 33-64 (1.21 ms vs 1.34 register-major)
 #endif
+#ifndef PLACE_HOLE32
+#define PLACE_HOLE32 1  // 32-bit hole scan when every end is below 2^31
+#endif
 #ifndef PLACE_SHORT_NETS
 #define PLACE_SHORT_NETS 1  // rows of <= 8 / 16 predecessors sort with an 8 / 16-wide network
 #endif
@@ -146,7 +149,7 @@ __device__ __forceinline__ void pred_range(const PlaceArgs &a, int32_t j, int64_
 // _pick_offset.  Ranges are sorted as one 64-bit key (start << IB | slot):
 // equal starts may come in any order (the hole scan only sees the running
 // max of ends), so the slot just makes keys unique and carries the end.
-template <bool REC, int K>
+template <bool REC, int K, bool NARROW>
 __device__ __forceinline__ int64_t place_reg(const PlaceArgs &a, int64_t rb, int m, int64_t need, int &lvl,
                                              bool &ok) {
   const int lane = threadIdx.x & 31;
@@ -172,12 +175,29 @@ __device__ __forceinline__ int64_t place_reg(const PlaceArgs &a, int64_t rb, int
   }
   ok = !__any_sync(FULL_MASK, big);
   if (!ok) return 0;
+  // NARROW kernel (pools under 2^31 bytes): every end and the request below
+  // 2^31 lets the hole scan run in 32 bits; any wider value takes the 64-bit
+  // scan for this variable
+  bool narrow = false;
+  if constexpr (NARROW) {
+    bool wide = need >= (int64_t)INT32_MAX;
+#pragma unroll
+    for (int r = 0; r < K; r++) wide |= e[r] >= (int64_t)INT32_MAX;
+    narrow = !__any_sync(FULL_MASK, wide);
+  }
   lvl = warp_max_i32(lv) + 1;
   if (lane == 0) PT_STAMP(3, a.dbg_v);
-  if constexpr (PLACE_LANE_MAJOR && K >= PLACE_LM_KMIN) {
+  if constexpr ((PLACE_LANE_MAJOR && K >= PLACE_LM_KMIN) || (K == 1 && NARROW)) {
     // lane-major network and one-pass hole scan (place_dev.cuh)
-    if constexpr (K == 2 || PLACE_LM_K4_UNROLLED) warp_bitonic_keys_lm_unrolled<K>(x);
-    else warp_bitonic_keys_lm<K>(x);
+    if constexpr (K == 1) {
+      if (m <= 8) warp_bitonic_keys_first<8>(x[0]);
+      else if (m <= 16) warp_bitonic_keys_first<16>(x[0]);
+      else warp_bitonic_keys_first<32>(x[0]);
+    } else if constexpr (K == 2 || PLACE_LM_K4_UNROLLED) {
+      warp_bitonic_keys_lm_unrolled<K>(x);
+    } else {
+      warp_bitonic_keys_lm<K>(x);
+    }
     if (lane == 0) PT_STAMP(4, a.dbg_v);
     int64_t ss[K], es[K];
 #pragma unroll
@@ -190,6 +210,12 @@ __device__ __forceinline__ int64_t place_reg(const PlaceArgs &a, int64_t rb, int
         if ((src >> 5) == q) es[r] = t;
       }
       ss[r] = (int64_t)(x[r] >> IB);
+    }
+    if (NARROW && narrow) {
+      int32_t s32[K], e32[K];
+#pragma unroll
+      for (int r = 0; r < K; r++) { s32[r] = (int32_t)ss[r]; e32[r] = (int32_t)es[r]; }
+      return hole_lm32<K>(s32, e32, m, (int32_t)need, a.policy);
     }
     return hole_lm<K>(ss, es, m, need, a.policy);
   }
@@ -279,7 +305,7 @@ constexpr int PLACE_THREADS = 256;
 
 
 // offset of one variable whose predecessors are all placed (warp-wide)
-template <bool REC>
+template <bool REC, bool NARROW>
 __device__ __forceinline__ int64_t place_var(const PlaceArgs &a, int32_t v, int64_t gwarp, int64_t rb, int m,
                                              int64_t need, int &lvl) {
   const int lane = threadIdx.x & 31;
@@ -287,9 +313,9 @@ __device__ __forceinline__ int64_t place_var(const PlaceArgs &a, int32_t v, int6
   bool ok = true;
   lvl = 1;
   if (m == 0) o = 0;
-  else if (m <= 32) o = place_reg<REC, 1>(a, rb, m, need, lvl, ok);
-  else if (m <= 64) o = place_reg<REC, 2>(a, rb, m, need, lvl, ok);
-  else if (m <= 128) o = place_reg<REC, 4>(a, rb, m, need, lvl, ok);
+  else if (m <= 32) o = place_reg<REC, 1, NARROW>(a, rb, m, need, lvl, ok);
+  else if (m <= 64) o = place_reg<REC, 2, NARROW>(a, rb, m, need, lvl, ok);
+  else if (m <= 128) o = place_reg<REC, 4, NARROW>(a, rb, m, need, lvl, ok);
   else ok = false;
   // long rows, or offsets too large to pack: sort (start, end) pairs in
   // global scratch
@@ -311,7 +337,7 @@ __device__ __forceinline__ int64_t place_var(const PlaceArgs &a, int32_t v, int6
 // queue in order; placing a variable decrements its successors' counters
 // and the last predecessor to finish publishes the successor.  No grid-wide
 // barrier: a variable starts the moment its last predecessor is placed.
-template <bool REC>
+template <bool REC, bool NARROW>
 __global__ void __launch_bounds__(PLACE_THREADS, PLACE_MIN_BLOCKS) k_place_async(PlaceArgs a) {
   const int lane = threadIdx.x & 31;
   int64_t gwarp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -364,9 +390,9 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_MIN_BLOCKS) k_place_async
 #if PLACE_TRACE
     PlaceArgs ad = a;
     ad.dbg_v = v;
-    int64_t o = place_var<REC>(ad, v, gwarp, rb, m, need, lvl);
+    int64_t o = place_var<REC, NARROW>(ad, v, gwarp, rb, m, need, lvl);
 #else
-    int64_t o = place_var<REC>(a, v, gwarp, rb, m, need, lvl);
+    int64_t o = place_var<REC, NARROW>(a, v, gwarp, rb, m, need, lvl);
 #endif
     if (lane == 0) {
       if constexpr (REC) {
@@ -667,7 +693,7 @@ extern "C" int mp_plan_pool(mp_ctx *ctx, mp_dgraph *g, int32_t policy, int64_t *
   unsigned long long *d_need = (unsigned long long *)(ctr.p + 6);
   // the conflict build bounded the long-row scratch by degree (no readback)
   uint64_t arena_need = (uint64_t)g->arena_need;
-  static int per_sm_cached[2] = {0, 0};
+  static int per_sm_cached[4] = {0, 0, 0, 0};
   DBuf<int64_t> &off = g->offsets;
   CUDA_TRY(off.alloc(V, st));
   // sentinels: -1 offsets, level 0 or -1 (see pred_range)
@@ -681,8 +707,12 @@ extern "C" int mp_plan_pool(mp_ctx *ctx, mp_dgraph *g, int32_t policy, int64_t *
     CUDA_TRY(cudaMemsetAsync(level.p, 0, V * 4, st));
   }
   size_t smem = 0;
-  void (*kern)(PlaceArgs) = use_rec ? k_place_async<true> : k_place_async<false>;
-  int &cached = per_sm_cached[use_rec];
+  // the 32-bit hole scan pays off only when the pool fits 2^31 bytes: the
+  // narrow kernel when the traced peak (a lower bound of the footprint) does
+  const bool narrow = PLACE_HOLE32 && g->peak_hint >= 0 && g->peak_hint < (int64_t)INT32_MAX;
+  void (*kern)(PlaceArgs) = use_rec ? (narrow ? k_place_async<true, true> : k_place_async<true, false>)
+                                    : (narrow ? k_place_async<false, true> : k_place_async<false, false>);
+  int &cached = per_sm_cached[2 * use_rec + narrow];
   if (!cached) CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached, kern, PLACE_THREADS, smem));
   int per_sm = cached < 1 ? 1 : cached;
   if (const char *e = getenv("MP_PLACE_BLOCKS_PER_SM")) per_sm = atoi(e) < per_sm ? atoi(e) : per_sm;  // experiments
@@ -717,8 +747,7 @@ extern "C" int mp_plan_pool(mp_ctx *ctx, mp_dgraph *g, int32_t policy, int64_t *
              d_need);
     }
     StageTimer ptm(ctx, MP_ST_PLACE);
-    if (use_rec) LAUNCH(ctx, k_place_async<true>, (unsigned)nblocks, PLACE_THREADS, smem, a);
-    else LAUNCH(ctx, k_place_async<false>, (unsigned)nblocks, PLACE_THREADS, smem, a);
+    LAUNCH(ctx, kern, (unsigned)nblocks, PLACE_THREADS, smem, a);
   }
   if (offsets) CUDA_TRY(cudaMemcpyAsync(offsets, off.p, V * 8, cudaMemcpyDeviceToHost, st));
   if (trace_path) {

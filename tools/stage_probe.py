@@ -24,9 +24,10 @@ ap.add_argument("--nvars", type=int, default=1_000_000)
 ap.add_argument("--accesses", action="store_true")
 ap.add_argument("--oracle", action="store_true")
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--max-size", type=int, default=64 << 20, help="largest variable size (bytes)")
 a = ap.parse_args()
 t0 = time.time()
-arrays, window = workloads.interval_trace(a.nvars, seed=0, accesses=a.accesses)
+arrays, window = workloads.interval_trace(a.nvars, seed=0, accesses=a.accesses, max_size=a.max_size)
 print(f"trace n={len(arrays)} window={window} built in {time.time() - t0:.1f}s", flush=True)
 for _ in range(2):
     plan = plan_arrays(arrays)
