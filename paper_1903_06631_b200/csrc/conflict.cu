@@ -485,7 +485,17 @@ __global__ void k_prof_intervals(int64_t nv, const int32_t *nseg, const int32_t 
     lmn = x < lmn ? x : lmn;
     lmx = y > lmx ? y : lmx;
   }
-  if ((threadIdx.x & 31) == 0) {
+  // one pair of global atomics per block (every warp on the same two
+  // addresses serialises in L2)
+  __shared__ unsigned long long smn[32], smx[32];
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if ((threadIdx.x & 31) == 0) { smn[w] = lmn; smx[w] = lmx; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < nw; i++) {
+      lmn = smn[i] < lmn ? smn[i] : lmn;
+      lmx = smx[i] > lmx ? smx[i] : lmx;
+    }
     atomicMin(&kmm[0], lmn);
     atomicMax(&kmm[1], lmx);
   }
@@ -554,8 +564,8 @@ static int build_csr_profile(mp_ctx *ctx, mp_dprofile *P, mp_dgraph *g, mp_err *
   int32_t *d_ni = (int32_t *)(ctx->d_small + 2);
   CUDA_TRY(cudaMemsetAsync(d_kmm, 0xff, 8, st));
   CUDA_TRY(cudaMemsetAsync(d_kmm + 1, 0, 8, st));
-  LAUNCH(ctx, k_prof_intervals, grid_for(nv, 256), 256, 0, nv, P->nseg.p, P->seg.p, P->size.p, ea.p, eb.p, cnt.p,
-         hs.p, he.p, d_kmm);
+  LAUNCH(ctx, k_prof_intervals, grid_for(nv, 256, (int64_t)ctx->num_sms * 8), 256, 0, nv, P->nseg.p, P->seg.p,
+         P->size.p, ea.p, eb.p, cnt.p, hs.p, he.p, d_kmm);
   int rc = dev_exclusive_scan<int32_t>(ctx, hs.p, offs_s.p, p + 1, d_ni, err);
   if (rc) return rc;
   rc = dev_exclusive_scan<int32_t>(ctx, he.p, cum_e.p, p + 2, nullptr, err);

@@ -468,7 +468,14 @@ __global__ void k_load_peak(const int64_t *loads, int64_t p, long long *peak) {
     long long u = __shfl_xor_sync(FULL_MASK, m, o);
     if (u > m) m = u;
   }
-  if ((threadIdx.x & 31) == 0) atomicMax(peak, m);
+  // one global atomic per block: per-warp atomics on one address serialise
+  __shared__ long long sm[32];
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); w++) m = sm[w] > m ? sm[w] : m;
+    atomicMax(peak, m);
+  }
 }
 
 __global__ void k_load_argmax(const int64_t *loads, int64_t p, const long long *peak, unsigned long long *idx) {
@@ -497,7 +504,7 @@ int profile_loads_async(mp_ctx *ctx, mp_dprofile *P, mp_err *err) {
   const long long lmin = LLONG_MIN;
   CUDA_TRY(cudaMemcpyAsync(d_peak, &lmin, 8, cudaMemcpyHostToDevice, ctx->stream));
   CUDA_TRY(cudaMemsetAsync(d_idx, 0xff, 8, ctx->stream));
-  LAUNCH(ctx, k_load_peak, grid_for(p, 256, 2048), 256, 0, P->loads.p, p, d_peak);
+  LAUNCH(ctx, k_load_peak, grid_for(p, 256, (int64_t)ctx->num_sms * 8), 256, 0, P->loads.p, p, d_peak);
   LAUNCH(ctx, k_load_argmax, grid_for(p, 256, 2048), 256, 0, P->loads.p, p, d_peak, d_idx);
   return MP_OK;
 }

@@ -75,10 +75,14 @@ __device__ T block_excl_scan(T v, T *total) {
 // posted first) and post their own inclusive prefix.
 template <typename T>
 __global__ void __launch_bounds__(SCAN_THREADS) k_scan_onepass(const T *in, T *out, int64_t n, int32_t *flags,
-                                                               T *agg, T *incl, int32_t *tile_ctr, T *total) {
+                                                               T *agg, T *incl, int32_t *tile_ctr, T *total,
+                                                               int32_t epoch, uint32_t tile_base) {
   __shared__ int32_t s_tile;
   __shared__ T s_excl, s_tot;
-  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1);
+  // flags hold (epoch << 2) | status: a value from an earlier scan reads as
+  // "not posted", so the flags never need clearing
+  const int32_t F_AGG = (epoch << 2) | 1, F_PFX = (epoch << 2) | 2;
+  if (threadIdx.x == 0) s_tile = (int32_t)((uint32_t)atomicAdd(tile_ctr, 1) - tile_base);
   __syncthreads();
   const int64_t tile = s_tile;
   const int64_t base = tile * SCAN_TILE;
@@ -116,31 +120,35 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_onepass(const T *in, T *o
       if (lane == 0) {
         incl[0] = sum;
         __threadfence();
-        atomicExch(&flags[0], 2);
+        atomicExch(&flags[0], F_PFX);
       }
     } else {
       if (lane == 0) {
         agg[tile] = sum;
         __threadfence();
-        atomicExch(&flags[tile], 1);
+        atomicExch(&flags[tile], F_AGG);
       }
       for (int64_t p = tile - 1;; p -= 32) {
         int64_t q = p - lane;
-        int f = q >= 0 ? *(volatile int32_t *)&flags[q] : 2;
+        int f = q >= 0 ? *(volatile int32_t *)&flags[q] : F_PFX;
+        if (f != F_AGG && f != F_PFX) f = 0;
         while (__any_sync(FULL_MASK, f == 0))
-          if (f == 0) f = *(volatile int32_t *)&flags[q];
+          if (f == 0) {
+            f = *(volatile int32_t *)&flags[q];
+            if (f != F_AGG && f != F_PFX) f = 0;
+          }
         __threadfence();
-        unsigned pfx = __ballot_sync(FULL_MASK, f == 2);
+        unsigned pfx = __ballot_sync(FULL_MASK, f == F_PFX);
         int stop = pfx ? __ffs(pfx) - 1 : 31;
         T val = 0;
-        if (lane <= stop && q >= 0) val = f == 2 ? *(volatile T *)&incl[q] : *(volatile T *)&agg[q];
+        if (lane <= stop && q >= 0) val = f == F_PFX ? *(volatile T *)&incl[q] : *(volatile T *)&agg[q];
         excl += warp_sum(val);
         if (pfx) break;
       }
       if (lane == 0) {
         incl[tile] = excl + sum;
         __threadfence();
-        atomicExch(&flags[tile], 2);
+        atomicExch(&flags[tile], F_PFX);
       }
     }
     if (lane == 0) {
@@ -177,14 +185,27 @@ int dev_exclusive_scan(mp_ctx *ctx, const T *in, T *out, int64_t n, T *total, mp
     return MP_OK;
   }
   int64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
-  // flags + tile counter in one zeroed block, per-tile values after it
-  DBuf<unsigned char> st;
-  size_t fbytes = ((size_t)(nb + 1) * 4 + 15) & ~(size_t)15;
-  CUDA_TRY(st.alloc((int64_t)(fbytes + 2 * (size_t)nb * sizeof(T)), ctx->stream));
-  CUDA_TRY(cudaMemsetAsync(st.p, 0, fbytes, ctx->stream));
-  int32_t *flags = (int32_t *)st.p;
-  T *agg = (T *)(st.p + fbytes), *incl = agg + nb;
-  LAUNCH(ctx, k_scan_onepass<T>, (unsigned)nb, SCAN_THREADS, 0, in, out, n, flags, agg, incl, flags + nb, total);
+  // persistent per-context flags / values / tile counter (see mp_ctx)
+  if (nb > ctx->scan_cap || ctx->scan_epoch >= (1u << 28)) {
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (ctx->scan_flags) cudaFree(ctx->scan_flags);
+    if (ctx->scan_vals) cudaFree(ctx->scan_vals);
+    if (!ctx->scan_ctr) CUDA_TRY(cudaMalloc((void **)&ctx->scan_ctr, 16));
+    int64_t cap = nb < 4096 ? 4096 : nb;
+    CUDA_TRY(cudaMalloc((void **)&ctx->scan_flags, cap * 4));
+    CUDA_TRY(cudaMalloc((void **)&ctx->scan_vals, 2 * cap * 8));
+    CUDA_TRY(cudaMemsetAsync(ctx->scan_flags, 0, cap * 4, ctx->stream));
+    CUDA_TRY(cudaMemsetAsync(ctx->scan_ctr, 0, 16, ctx->stream));
+    ctx->scan_cap = cap;
+    ctx->scan_epoch = 0;
+    ctx->scan_base = 0;
+  }
+  const int32_t epoch = (int32_t)++ctx->scan_epoch;
+  const uint32_t base = ctx->scan_base;
+  ctx->scan_base += (uint32_t)nb;
+  T *agg = (T *)ctx->scan_vals, *incl = (T *)(ctx->scan_vals + ctx->scan_cap);
+  LAUNCH(ctx, k_scan_onepass<T>, (unsigned)nb, SCAN_THREADS, 0, in, out, n, ctx->scan_flags, agg, incl,
+         ctx->scan_ctr, total, epoch, base);
   return MP_OK;
 }
 

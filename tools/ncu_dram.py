@@ -3,8 +3,8 @@ with --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
 
   python tools/ncu_dram.py <csv> [first-kernel-prefix] [--json out.json] [--peak GBps]
 
-Keeps the launches from the last one whose name starts with the prefix (the
-last pipeline pass), groups by kernel name, and prints per kernel: launches,
+With a prefix naming a kernel launched once per pass, keeps the last pass
+(as many launches as separate the prefix kernel's last two launches), groups by kernel name, and prints per kernel: launches,
 total us, DRAM read/write MB, DRAM GB/s (measured bytes / duration) and the
 fraction of the HBM peak.  ncu serialises launches and runs them cold-cache,
 so the absolute times are upper bounds; shares and bytes are what count."""
@@ -39,8 +39,11 @@ for r in rows[hi + 1:]:
 L = list(launch.values())
 pre = args[1] if len(args) > 1 else None
 if pre:
-    first = max(i for i, d in enumerate(L) if d["name"].startswith(pre) or d["name"].split(" ")[-1].startswith(pre))
-    L = L[first:]
+    # the prefix names a kernel launched once per pass: the last pass is the
+    # last (distance between its last two launches) launches of the list
+    hits = [i for i, d in enumerate(L) if d["name"].startswith(pre) or d["name"].startswith("void " + pre)]
+    per = hits[-1] - hits[-2] if len(hits) > 1 else len(L) - hits[-1]
+    L = L[len(L) - per:] if len(hits) > 1 else L[hits[-1]:]
 agg = collections.OrderedDict()
 for d in L:
     a = agg.setdefault(d["name"], {"launches": 0, "us": 0.0, "rd": 0.0, "wr": 0.0})
@@ -59,7 +62,7 @@ print(f"total {tot:.1f} us in {len(L)} launches")
 if out_json:
     kern = {}
     for n, a in agg.items():
-        short = n.split(" ")[-1].split("<")[0]
+        short = (n[5:] if n.startswith("void ") else n).split("<")[0]
         k = kern.setdefault(short, {"launches": 0, "us": 0.0, "dram_read_bytes": 0.0, "dram_write_bytes": 0.0})
         k["launches"] += a["launches"]; k["us"] += a["us"]; k["dram_read_bytes"] += a["rd"]; k["dram_write_bytes"] += a["wr"]
     for k in kern.values():
