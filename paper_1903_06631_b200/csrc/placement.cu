@@ -550,7 +550,17 @@ __global__ void k_ready_init(int64_t V, const int32_t *pcnt, int32_t *remaining,
       while (n2 < (unsigned long long)c) n2 <<= 1;
       need += n2;
     }
-    if (c == 0) queue[atomicAdd(tail, 1)] = (int32_t)(v + 1);
+    // one tail atomic per warp (thousands of single increments on one
+    // address serialise in L2)
+    const unsigned am = __activemask();
+    const unsigned z = __ballot_sync(am, c == 0);
+    if (z) {
+      const int lead = __ffs(z) - 1;
+      int qb = 0;
+      if ((int)(threadIdx.x & 31) == lead) qb = atomicAdd(tail, __popc(z));
+      qb = __shfl_sync(am, qb, lead);
+      if (c == 0) queue[qb + __popc(z & lanemask_lt())] = (int32_t)(v + 1);
+    }
   }
   need = warp_sum(need);
   if ((threadIdx.x & 31) == 0 && need) atomicAdd(arena_need, need);
