@@ -60,6 +60,9 @@
 #ifndef PLACE_HOLE32
 #define PLACE_HOLE32 1  // 32-bit hole scan when every end is below 2^31
 #endif
+#ifndef PLACE_SE_KEYS
+#define PLACE_SE_KEYS 1  // narrow variables sort (start << 32 | end) keys
+#endif
 #ifndef PLACE_SHORT_NETS
 #define PLACE_SHORT_NETS 1  // rows of <= 8 / 16 predecessors sort with an 8 / 16-wide network
 #endif
@@ -189,6 +192,13 @@ __device__ __forceinline__ int64_t place_reg(const PlaceArgs &a, int64_t rb, int
   if (lane == 0) PT_STAMP(3, a.dbg_v);
   if constexpr ((PLACE_LANE_MAJOR && K >= PLACE_LM_KMIN) || (K == 1 && NARROW)) {
     // lane-major network and one-pass hole scan (place_dev.cuh)
+    if (PLACE_SE_KEYS && NARROW && narrow) {
+      // starts and ends both fit 31 bits: the key is (start << 32 | end),
+      // so the sorted keys carry the ends and no lookup by slot follows
+#pragma unroll
+      for (int r = 0; r < K; r++)
+        if (x[r] != ~0ull) x[r] = ((x[r] >> IB) << 32) | (uint64_t)(uint32_t)e[r];
+    }
     if constexpr (K == 1) {
       if (m <= 8) warp_bitonic_keys_first<8>(x[0]);
       else if (m <= 16) warp_bitonic_keys_first<16>(x[0]);
@@ -199,6 +209,12 @@ __device__ __forceinline__ int64_t place_reg(const PlaceArgs &a, int64_t rb, int
       warp_bitonic_keys_lm<K>(x);
     }
     if (lane == 0) PT_STAMP(4, a.dbg_v);
+    if (PLACE_SE_KEYS && NARROW && narrow) {
+      int32_t s32[K], e32[K];
+#pragma unroll
+      for (int r = 0; r < K; r++) { s32[r] = (int32_t)(x[r] >> 32); e32[r] = (int32_t)(uint32_t)x[r]; }
+      return hole_lm32<K>(s32, e32, m, (int32_t)need, a.policy);
+    }
     int64_t ss[K], es[K];
 #pragma unroll
     for (int r = 0; r < K; r++) {
