@@ -246,17 +246,9 @@ __global__ void __launch_bounds__(RS_THREADS) k_os_hist(const K *keys, int64_t n
   __shared__ int32_t h[OS_MAX_PASSES][RS_BINS];
   for (int i = threadIdx.x; i < passes * RS_BINS; i += RS_THREADS) h[i / RS_BINS][i % RS_BINS] = 0;
   __syncthreads();
-  // warp-aggregated increments: the top digits of a narrow key range take
-  // few values, and 32 lanes on one counter serialise
-  for (int64_t j0 = blockIdx.x * (int64_t)RS_THREADS; j0 < n; j0 += (int64_t)gridDim.x * RS_THREADS) {
-    const int64_t j = j0 + threadIdx.x;
-    const bool ok = j < n;
-    const K k = ok ? keys[j] : K(0);
-    for (int p = 0; p < passes; p++) {
-      const unsigned d = ok ? (unsigned)((k >> (8 * p)) & 0xff) : 0x100u + (threadIdx.x & 31);
-      const unsigned peers = __match_any_sync(FULL_MASK, d);
-      if (ok && (peers & lanemask_lt()) == 0) atomicAdd(&h[p][d], __popc(peers));
-    }
+  for (int64_t j = blockIdx.x * (int64_t)RS_THREADS + threadIdx.x; j < n; j += (int64_t)gridDim.x * RS_THREADS) {
+    K k = keys[j];
+    for (int p = 0; p < passes; p++) atomicAdd(&h[p][(unsigned)((k >> (8 * p)) & 0xff)], 1);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < passes * RS_BINS; i += RS_THREADS) {
@@ -682,7 +674,7 @@ static int radix_sort_impl(mp_ctx *ctx, K *keys, uint32_t *vals, int64_t n, int 
     cudaFuncSetAttribute(k_os_pass<K, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr_set = true;
   }
-  unsigned hgrid = grid_for(n, RS_THREADS, (int64_t)ctx->num_sms * 2);
+  unsigned hgrid = grid_for(n, RS_THREADS, (int64_t)ctx->num_sms * 8);
   LAUNCH(ctx, k_os_hist<K>, hgrid, RS_THREADS, 0, keys, n, passes, meta.p);
   LAUNCH(ctx, k_os_prefix, 1, 32 * passes, 0, meta.p, passes);
   // buffers: the caller's (0) and scratch (1, 2); the last pass always writes
