@@ -378,31 +378,26 @@ __global__ void k_ex_var(const uint8_t *kind, const int64_t *size, const uint32_
   }
 }
 
-__global__ void k_ex_marks(const uint8_t *kind, int64_t start, int64_t p, int32_t *is_malloc) {
+// twin pairing, iteration.py:193-225, and the window's malloc marks (one
+// launch: both only read k_ex_var's output or the trace)
+__global__ void k_ex_twin(const uint8_t *kind, const int64_t *size, int32_t nvars, int64_t start,
+                          int64_t p, ExScratch s, int32_t *is_malloc) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvars; v += (int64_t)gridDim.x * blockDim.x)
+    ex_twin_item(kind, size, v, start, p, s);
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < p; r += (int64_t)gridDim.x * blockDim.x)
     is_malloc[r] = kind[start + r] == MP_MALLOC;
 }
 
-// twin pairing, iteration.py:193-225
-__global__ void k_ex_twin(const uint8_t *kind, const int64_t *size, int32_t nvars, int64_t start,
-                          int64_t p, ExScratch s) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvars; v += (int64_t)gridDim.x * blockDim.x)
-    ex_twin_item(kind, size, v, start, p, s);
-}
-
-// final per-variable records (carry-ins)
-__global__ void k_ex_fill_carry(int32_t nvars, int64_t p, ExScratch s, const int32_t *carry_ord, ProfOut o,
-                                int64_t *acc_cnt) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvars; v += (int64_t)gridDim.x * blockDim.x)
-    ex_fill_carry_item(v, p, s, carry_ord, o, acc_cnt);
-}
-
-// final per-variable records (window instances, alloc order)
+// final per-variable records (window instances, alloc order), and the
+// carry-ins' (disjoint records and access counts: one launch)
 __global__ void k_ex_fill_window(const int32_t *var, const int64_t *size, int64_t start, int64_t p,
                                  int64_t ncarry, ExScratch s, const int32_t *win_ord,
-                                 const int32_t *carry_survive, ProfOut o, int64_t *acc_cnt) {
+                                 const int32_t *carry_survive, ProfOut o, int64_t *acc_cnt, int32_t nvars,
+                                 const int32_t *carry_ord) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < p; r += (int64_t)gridDim.x * blockDim.x)
     ex_fill_window_item(var, size, start, r, p, ncarry, s, win_ord, carry_survive, o, acc_cnt);
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvars; v += (int64_t)gridDim.x * blockDim.x)
+    ex_fill_carry_item(v, p, s, carry_ord, o, acc_cnt);
 }
 
 // second walk: accesses into the final CSR, owners into op_owner
@@ -573,10 +568,10 @@ extern "C" int mp_extract(mp_ctx *ctx, mp_dtrace *t, int64_t start, int64_t end,
   CUDA_TRY(cudaMemsetAsync(d_first, 0xff, 8, st));
   LAUNCH(ctx, k_ex_var, grid_for(nv, 128), 128, 0, t->kind.p, t->size.p, t->perm.p, t->gstart.p, nv,
          start, end, s, d_first);
-  LAUNCH(ctx, k_ex_marks, grid_for(p, 256), 256, 0, t->kind.p, start, p, is_malloc.p);
   // twins and ordinals run before the violation check so one readback
   // returns both (on a violation their output is simply discarded)
-  LAUNCH(ctx, k_ex_twin, grid_for(nv, 256), 256, 0, t->kind.p, t->size.p, nv, start, p, s);
+  LAUNCH(ctx, k_ex_twin, grid_for(nv > p ? nv : p, 256), 256, 0, t->kind.p, t->size.p, nv, start, p, s,
+         is_malloc.p);
   // carry ordinals (surviving carry-ins, by name = var id) and window ordinals
   int32_t *d_tot = (int32_t *)(ctx->d_small + 1);
   rc = dev_exclusive_scan<int32_t>(ctx, c_surv.p, carry_ord.p, nv, d_tot, err);
@@ -619,9 +614,8 @@ extern "C" int mp_extract(mp_ctx *ctx, mp_dtrace *t, int64_t start, int64_t end,
   }
   ProfOut o = prof_out(P);
   // c_surv still holds the 0/1 flags (scan wrote carry_ord)
-  LAUNCH(ctx, k_ex_fill_carry, grid_for(nv, 256), 256, 0, nv, p, s, carry_ord.p, o, acc_cnt.p);
-  LAUNCH(ctx, k_ex_fill_window, grid_for(p, 256), 256, 0, t->var.p, t->size.p, start, p, ncarry, s,
-         win_ord.p, c_surv.p, o, acc_cnt.p);
+  LAUNCH(ctx, k_ex_fill_window, grid_for(nv > p ? nv : p, 256), 256, 0, t->var.p, t->size.p, start, p, ncarry, s,
+         win_ord.p, c_surv.p, o, acc_cnt.p, nv, carry_ord.p);
   int64_t *d_atot = ctx->d_small + 2;
   rc = dev_exclusive_scan<int64_t>(ctx, acc_cnt.p, P->acc_off.p, V, d_atot, err);
   if (rc) return rc;
