@@ -461,8 +461,11 @@ __device__ __forceinline__ int prof_effective(int ns, int4 sg, int32_t &a0, int3
   return c;
 }
 
+// hse[x]: starts at x in the low 32 bits, ends at x in the high 32 bits, so
+// ONE 64-bit scan gives both prefix counts (the low sum never carries: fewer
+// than 2^31 intervals)
 __global__ void k_prof_intervals(int64_t nv, const int32_t *nseg, const int32_t *seg, const int64_t *size,
-                                 int32_t *ea, int32_t *eb, int64_t *cnt, int32_t *hs, int32_t *he,
+                                 int32_t *ea, int32_t *eb, int64_t *cnt, unsigned long long *hse,
                                  unsigned long long *kmm) {
   unsigned long long lmn = ~0ull, lmx = 0;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
@@ -471,8 +474,8 @@ __global__ void k_prof_intervals(int64_t nv, const int32_t *nseg, const int32_t 
     const int c = prof_effective(nseg[v], sg, a0, b0, a1, b1);
     reinterpret_cast<int2 *>(ea)[v] = make_int2(c > 0 ? a0 : -1, c > 1 ? a1 : -1);
     reinterpret_cast<int2 *>(eb)[v] = make_int2(b0, b1);
-    if (c > 0) { atomicAdd(&hs[a0], 1); atomicAdd(&he[b0], 1); }
-    if (c > 1) { atomicAdd(&hs[a1], 1); atomicAdd(&he[b1], 1); }
+    if (c > 0) { atomicAdd(&hse[a0], 1ull); atomicAdd(&hse[b0], 1ull << 32); }
+    if (c > 1) { atomicAdd(&hse[a1], 1ull); atomicAdd(&hse[b1], 1ull << 32); }
     cnt[2 * v] = 0;
     cnt[2 * v + 1] = 0;
     const uint64_t k = desc_size_key(size[v]);
@@ -502,21 +505,20 @@ __global__ void k_prof_intervals(int64_t nv, const int32_t *nseg, const int32_t 
 }
 
 // slots in start order (counting sort; order among equal starts is free)
-__global__ void k_prof_scatter(int64_t nslots, const int32_t *ea, const int32_t *offs, int32_t *cur, uint32_t *perm) {
+__global__ void k_prof_scatter(int64_t nslots, const int32_t *ea, const int64_t *pref, int32_t *cur, uint32_t *perm) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nslots; i += (int64_t)gridDim.x * blockDim.x) {
     const int32_t x = ea[i];
-    if (x >= 0) perm[offs[x] + atomicAdd(&cur[x], 1)] = (uint32_t)i;
+    if (x >= 0) perm[(int32_t)(uint32_t)pref[x] + atomicAdd(&cur[x], 1)] = (uint32_t)i;
   }
 }
 
 // k_iv_counts_dense with the slot's variable implicit (slot >> 1)
 __global__ void k_prof_counts(int64_t n, const uint32_t *perm, const int32_t *ea, const int32_t *eb,
-                              const int32_t *offs, const int32_t *cum_e, int64_t *cnt, const int32_t *rank,
-                              int32_t *sv) {
+                              const int64_t *pref, int64_t *cnt, const int32_t *rank, int32_t *sv) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t iid = perm[k];
-    const int64_t f = (int64_t)offs[eb[iid]] - k - 1;
-    const int64_t bw = k - cum_e[ea[iid] + 1];
+    const int64_t f = (int64_t)(uint32_t)pref[eb[iid]] - k - 1;       // starts before the end
+    const int64_t bw = k - (int64_t)(pref[ea[iid] + 1] >> 32);         // ends at or before the start
     cnt[iid] = f + bw;
     const int32_t v = (int32_t)(iid >> 1);
     sv[3 * k] = v;
@@ -550,39 +552,34 @@ static int build_csr_profile(mp_ctx *ctx, mp_dprofile *P, mp_dgraph *g, mp_err *
   CUDA_TRY(g->rank.alloc(nv, st));
   CUDA_TRY(g->pcnt.alloc(nv, st));
   StageTimer *tm = new StageTimer(ctx, MP_ST_CONFLICT_PREP);
-  DBuf<int32_t> ea, eb, hs, he, offs_s, cum_e, curs, sv, scur;
-  DBuf<int64_t> cnt, sub_off;
+  DBuf<int32_t> ea, eb, curs, sv, scur;
+  DBuf<int64_t> cnt, sub_off, hse, pref;
   CUDA_TRY(ea.alloc(ns, st)); CUDA_TRY(eb.alloc(ns, st));
-  CUDA_TRY(hs.alloc(p + 2, st)); CUDA_TRY(he.alloc(p + 2, st));
-  CUDA_TRY(offs_s.alloc(p + 2, st)); CUDA_TRY(cum_e.alloc(p + 2, st)); CUDA_TRY(curs.alloc(p + 1, st));
+  CUDA_TRY(hse.alloc(p + 2, st)); CUDA_TRY(pref.alloc(p + 2, st)); CUDA_TRY(curs.alloc(p + 1, st));
   CUDA_TRY(cnt.alloc(ns + 1, st)); CUDA_TRY(sub_off.alloc(ns + 1, st));
-  CUDA_TRY(cudaMemsetAsync(hs.p, 0, (p + 2) * 4, st));
-  CUDA_TRY(cudaMemsetAsync(he.p, 0, (p + 2) * 4, st));
+  CUDA_TRY(cudaMemsetAsync(hse.p, 0, (p + 2) * 8, st));
   CUDA_TRY(cudaMemsetAsync(curs.p, 0, (p + 1) * 4, st));
   // d_small: [0..1] size-key range, [2] interval count, [3] arena need, [4] nnz
   unsigned long long *d_kmm = (unsigned long long *)ctx->d_small;
-  int32_t *d_ni = (int32_t *)(ctx->d_small + 2);
+  int64_t *d_ni = ctx->d_small + 2;
   CUDA_TRY(cudaMemsetAsync(d_kmm, 0xff, 8, st));
   CUDA_TRY(cudaMemsetAsync(d_kmm + 1, 0, 8, st));
   LAUNCH(ctx, k_prof_intervals, grid_for(nv, 256, (int64_t)ctx->num_sms * 8), 256, 0, nv, P->nseg.p, P->seg.p,
-         P->size.p, ea.p, eb.p, cnt.p, hs.p, he.p, d_kmm);
-  int rc = dev_exclusive_scan<int32_t>(ctx, hs.p, offs_s.p, p + 1, d_ni, err);
-  if (rc) return rc;
-  rc = dev_exclusive_scan<int32_t>(ctx, he.p, cum_e.p, p + 2, nullptr, err);
+         P->size.p, ea.p, eb.p, cnt.p, (unsigned long long *)hse.p, d_kmm);
+  int rc = dev_exclusive_scan<int64_t>(ctx, hse.p, pref.p, p + 2, d_ni, err);
   if (rc) return rc;
   int64_t h[3];
   rc = dev_read_n(ctx, ctx->d_small, h, 24, err);
   if (rc) return rc;
-  const int64_t ni = (int32_t)h[2];
+  const int64_t ni = (int64_t)(uint32_t)h[2];  // low half of the packed total: the interval count
   g->size_hi = (int64_t)(~(uint64_t)h[0] ^ 0x8000000000000000ull);
   g->size_lo = (int64_t)(~(uint64_t)h[1] ^ 0x8000000000000000ull);
   rc = placement_rank_sort(ctx, nv, g->size.p, nullptr, g->rank.p, (uint64_t)h[0], (uint64_t)h[1], err);
   if (rc) return rc;
   DBuf<uint32_t> perm;
   CUDA_TRY(perm.alloc(ni, st)); CUDA_TRY(sv.alloc(3 * ni, st)); CUDA_TRY(scur.alloc(nv, st));
-  LAUNCH(ctx, k_prof_scatter, grid_for(ns, 256), 256, 0, ns, ea.p, offs_s.p, curs.p, perm.p);
-  LAUNCH(ctx, k_prof_counts, grid_for(ni, 256), 256, 0, ni, perm.p, ea.p, eb.p, offs_s.p, cum_e.p, cnt.p, g->rank.p,
-         sv.p);
+  LAUNCH(ctx, k_prof_scatter, grid_for(ns, 256), 256, 0, ns, ea.p, pref.p, curs.p, perm.p);
+  LAUNCH(ctx, k_prof_counts, grid_for(ni, 256), 256, 0, ni, perm.p, ea.p, eb.p, pref.p, cnt.p, g->rank.p, sv.p);
   int64_t *d_tot = ctx->d_small + 4;
   rc = dev_exclusive_scan<int64_t>(ctx, cnt.p, sub_off.p, ns, d_tot, err);
   if (rc) return rc;
