@@ -210,6 +210,9 @@ __host__ __device__ inline int name_cmp(NameTable nm, int32_t ab, int32_t ar, in
 // device pointer receiving the sum.  T in {int32_t, int64_t}.
 template <typename T>
 int dev_exclusive_scan(mp_ctx *ctx, const T *in, T *out, int64_t n, T *total, mp_err *err);
+// out[i] = in[0] + ... + in[i] (T = int64_t)
+template <typename T>
+int dev_inclusive_scan(mp_ctx *ctx, const T *in, T *out, int64_t n, T *total, mp_err *err);
 
 // stable LSD radix sort of (key, value) pairs on bits [0, bits)
 int dev_radix_sort_u32(mp_ctx *ctx, uint32_t *keys, uint32_t *vals, int64_t n, int bits,

@@ -488,12 +488,9 @@ int profile_loads_async(mp_ctx *ctx, mp_dprofile *P, mp_err *err) {
   CUDA_TRY(cudaMemsetAsync(diff.p, 0, (p + 1) * 8, ctx->stream));
   LAUNCH(ctx, k_load_diff, grid_for(V, 256), 256, 0, V, P->nseg.p, P->seg.p, P->size.p,
          (unsigned long long *)diff.p);
-  // loads[r] = sum diff[0..r]: exclusive scan of p+1 entries, shifted by one
-  DBuf<int64_t> ex;
-  CUDA_TRY(ex.alloc(p + 1, ctx->stream));
-  int rc = dev_exclusive_scan<int64_t>(ctx, diff.p, ex.p, p + 1, nullptr, err);
+  // loads[r] = sum diff[0..r]: inclusive scan straight into the profile
+  int rc = dev_inclusive_scan<int64_t>(ctx, diff.p, P->loads.p, p, nullptr, err);
   if (rc) return rc;
-  CUDA_TRY(cudaMemcpyAsync(P->loads.p, ex.p + 1, p * 8, cudaMemcpyDeviceToDevice, ctx->stream));
   long long *d_peak = (long long *)ctx->d_small;
   unsigned long long *d_idx = (unsigned long long *)(ctx->d_small + 1);
   const long long lmin = LLONG_MIN;

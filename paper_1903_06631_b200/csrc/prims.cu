@@ -73,7 +73,7 @@ __device__ T block_excl_scan(T v, T *total) {
 // from a counter, publish their aggregate, then resolve their exclusive
 // prefix from predecessors (aggregate or inclusive prefix, whichever is
 // posted first) and post their own inclusive prefix.
-template <typename T>
+template <typename T, bool INCL>
 __global__ void __launch_bounds__(SCAN_THREADS) k_scan_onepass(const T *in, T *out, int64_t n, int32_t *flags,
                                                                T *agg, T *incl, int32_t *tile_ctr, T *total,
                                                                int32_t epoch, uint32_t tile_base) {
@@ -162,8 +162,13 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_onepass(const T *in, T *o
 #pragma unroll
     for (int i = 0; i < SCAN_ITEMS; i++) {
       T x = v[i];
-      v[i] = run;
-      run += x;
+      if (INCL) {
+        run += x;
+        v[i] = run;
+      } else {
+        v[i] = run;
+        run += x;
+      }
     }
     uint4 *dst = (uint4 *)(out + base + (int64_t)threadIdx.x * SCAN_ITEMS);
 #pragma unroll
@@ -173,13 +178,14 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_onepass(const T *in, T *o
 #pragma unroll
   for (int i = 0; i < SCAN_ITEMS; i++) {
     int64_t j = base + (int64_t)threadIdx.x * SCAN_ITEMS + i;
+    if (INCL) run += v[i];
     if (j < n) out[j] = run;
-    run += v[i];
+    if (!INCL) run += v[i];
   }
 }
 
-template <typename T>
-int dev_exclusive_scan(mp_ctx *ctx, const T *in, T *out, int64_t n, T *total, mp_err *err) {
+template <typename T, bool INCL>
+static int dev_scan(mp_ctx *ctx, const T *in, T *out, int64_t n, T *total, mp_err *err) {
   if (n <= 0) {
     if (total) CUDA_TRY(cudaMemsetAsync(total, 0, sizeof(T), ctx->stream));
     return MP_OK;
@@ -204,13 +210,23 @@ int dev_exclusive_scan(mp_ctx *ctx, const T *in, T *out, int64_t n, T *total, mp
   const uint32_t base = ctx->scan_base;
   ctx->scan_base += (uint32_t)nb;
   T *agg = (T *)ctx->scan_vals, *incl = (T *)(ctx->scan_vals + ctx->scan_cap);
-  LAUNCH(ctx, k_scan_onepass<T>, (unsigned)nb, SCAN_THREADS, 0, in, out, n, ctx->scan_flags, agg, incl,
+  LAUNCH(ctx, (k_scan_onepass<T, INCL>), (unsigned)nb, SCAN_THREADS, 0, in, out, n, ctx->scan_flags, agg, incl,
          ctx->scan_ctr, total, epoch, base);
   return MP_OK;
 }
 
+template <typename T>
+int dev_exclusive_scan(mp_ctx *ctx, const T *in, T *out, int64_t n, T *total, mp_err *err) {
+  return dev_scan<T, false>(ctx, in, out, n, total, err);
+}
+template <typename T>
+int dev_inclusive_scan(mp_ctx *ctx, const T *in, T *out, int64_t n, T *total, mp_err *err) {
+  return dev_scan<T, true>(ctx, in, out, n, total, err);
+}
+
 template int dev_exclusive_scan<int32_t>(mp_ctx *, const int32_t *, int32_t *, int64_t, int32_t *, mp_err *);
 template int dev_exclusive_scan<int64_t>(mp_ctx *, const int64_t *, int64_t *, int64_t, int64_t *, mp_err *);
+template int dev_inclusive_scan<int64_t>(mp_ctx *, const int64_t *, int64_t *, int64_t, int64_t *, mp_err *);
 
 // ----------------------------------------------------------------------------
 // radix sort
