@@ -21,6 +21,7 @@ extern "C" int mp_ctx_create(int device, mp_ctx **out, mp_err *err) {
   CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   CUDA_TRY(cudaMallocHost((void **)&c->h_small, 64 * sizeof(int64_t)));
   CUDA_TRY(cudaMalloc((void **)&c->d_small, 64 * sizeof(int64_t)));
+  CUDA_TRY(cudaMemset(c->d_small, 0, 64 * sizeof(int64_t)));  // [63]: k_load_peak_idx's finish counter
   // keep freed scratch in the pool instead of returning it to the driver
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {

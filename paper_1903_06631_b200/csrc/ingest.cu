@@ -455,28 +455,56 @@ __global__ void k_load_diff(int64_t nv, const int32_t *nseg, const int32_t *seg,
   }
 }
 
-__global__ void k_load_peak(const int64_t *loads, int64_t p, long long *peak) {
-  long long m = LLONG_MIN;
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < p; r += (int64_t)gridDim.x * blockDim.x)
-    if (loads[r] > m) m = loads[r];
-  for (int o = 16; o; o >>= 1) {
-    long long u = __shfl_xor_sync(FULL_MASK, m, o);
-    if (u > m) m = u;
+// peak and its earliest index in one pass: each block reduces its share to
+// (max, first index of it); the last block to finish reduces the blocks'
+// pairs (per-block cells, a finish counter it resets for the next call)
+__global__ void k_load_peak_idx(const int64_t *loads, int64_t p, long long *bmax, long long *bidx,
+                                unsigned int *finished, long long *peak, unsigned long long *idx) {
+  long long m = LLONG_MIN, mi = LLONG_MAX;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < p; r += (int64_t)gridDim.x * blockDim.x) {
+    const long long x = loads[r];
+    if (x > m) { m = x; mi = r; }  // r increases along a thread's stride: the first wins ties
   }
-  // one global atomic per block: per-warp atomics on one address serialise
-  __shared__ long long sm[32];
-  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
+  for (int o = 16; o; o >>= 1) {
+    const long long um = __shfl_xor_sync(FULL_MASK, m, o), ui = __shfl_xor_sync(FULL_MASK, mi, o);
+    if (um > m || (um == m && ui < mi)) { m = um; mi = ui; }
+  }
+  __shared__ long long sm[32], si[32];
+  __shared__ bool last;
+  if ((threadIdx.x & 31) == 0) { sm[threadIdx.x >> 5] = m; si[threadIdx.x >> 5] = mi; }
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int w = 1; w < (int)(blockDim.x >> 5); w++) m = sm[w] > m ? sm[w] : m;
-    atomicMax(peak, m);
+    for (int w = 1; w < (int)(blockDim.x >> 5); w++)
+      if (sm[w] > m || (sm[w] == m && si[w] < mi)) { m = sm[w]; mi = si[w]; }
+    bmax[blockIdx.x] = m;
+    bidx[blockIdx.x] = mi;
+    __threadfence();
+    last = atomicAdd(finished, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  m = LLONG_MIN;
+  mi = LLONG_MAX;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+    const long long bm = *(volatile long long *)&bmax[b], bi = *(volatile long long *)&bidx[b];
+    if (bm > m || (bm == m && bi < mi)) { m = bm; mi = bi; }
+  }
+  for (int o = 16; o; o >>= 1) {
+    const long long um = __shfl_xor_sync(FULL_MASK, m, o), ui = __shfl_xor_sync(FULL_MASK, mi, o);
+    if (um > m || (um == m && ui < mi)) { m = um; mi = ui; }
+  }
+  if ((threadIdx.x & 31) == 0) { sm[threadIdx.x >> 5] = m; si[threadIdx.x >> 5] = mi; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); w++)
+      if (sm[w] > m || (sm[w] == m && si[w] < mi)) { m = sm[w]; mi = si[w]; }
+    *peak = m;
+    *idx = (unsigned long long)mi;
+    *finished = 0;
   }
 }
 
-__global__ void k_load_argmax(const int64_t *loads, int64_t p, const long long *peak, unsigned long long *idx) {
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < p; r += (int64_t)gridDim.x * blockDim.x)
-    if (loads[r] == *peak) atomicMin(idx, (unsigned long long)r);
-}
 
 // loads + peak for any device profile (also used after uploads)
 // loads + peak (left in ctx->d_small[0..1] = peak, earliest argmax)
@@ -493,11 +521,19 @@ int profile_loads_async(mp_ctx *ctx, mp_dprofile *P, mp_err *err) {
   if (rc) return rc;
   long long *d_peak = (long long *)ctx->d_small;
   unsigned long long *d_idx = (unsigned long long *)(ctx->d_small + 1);
-  const long long lmin = LLONG_MIN;
-  CUDA_TRY(cudaMemcpyAsync(d_peak, &lmin, 8, cudaMemcpyHostToDevice, ctx->stream));
-  CUDA_TRY(cudaMemsetAsync(d_idx, 0xff, 8, ctx->stream));
-  LAUNCH(ctx, k_load_peak, grid_for(p, 256, (int64_t)ctx->num_sms * 8), 256, 0, P->loads.p, p, d_peak);
-  LAUNCH(ctx, k_load_argmax, grid_for(p, 256, 2048), 256, 0, P->loads.p, p, d_peak, d_idx);
+  if (p == 0) {
+    const long long lmin = LLONG_MIN;
+    CUDA_TRY(cudaMemcpyAsync(d_peak, &lmin, 8, cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(cudaMemsetAsync(d_idx, 0xff, 8, ctx->stream));
+    return MP_OK;
+  }
+  // per-block cells and the finish counter live in the context's small
+  // scratch tail (the counter is left at zero by the last block)
+  const unsigned nb = grid_for(p, 256, 1024);
+  DBuf<long long> cells;
+  CUDA_TRY(cells.alloc(2 * (int64_t)nb, ctx->stream));
+  unsigned int *fin = (unsigned int *)(ctx->d_small + 63);
+  LAUNCH(ctx, k_load_peak_idx, nb, 256, 0, P->loads.p, p, cells.p, cells.p + nb, fin, d_peak, d_idx);
   return MP_OK;
 }
 
