@@ -341,7 +341,9 @@ __device__ __forceinline__ void warp_bitonic_keys_first(uint64_t &x) {
 
 // hole_lm on 32-bit values (every end below 2^31): one shuffle per scan
 // level and redux reductions
-template <int K>
+// L = the lanes that can hold ranges (m <= L * K): a row of at most 8 / 16
+// ranges needs 3 / 4 scan levels, and the top is lane L - 1's prefix
+template <int K, int L = 32>
 __device__ __forceinline__ int64_t hole_lm32(const int32_t (&s)[K], const int32_t (&e)[K], int m, int32_t need,
                                              int policy) {
   const int lane = threadIdx.x & 31;
@@ -351,7 +353,7 @@ __device__ __forceinline__ int64_t hole_lm32(const int32_t (&s)[K], const int32_
     if (lane * K + r < m && e[r] > lmax) lmax = e[r];
   int32_t incl = lmax;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
+  for (int o = 1; o < L; o <<= 1) {
     const int32_t u = __shfl_up_sync(FULL_MASK, incl, o);
     if (lane >= o && u > incl) incl = u;
   }
@@ -370,7 +372,7 @@ __device__ __forceinline__ int64_t hole_lm32(const int32_t (&s)[K], const int32_
     }
     if (e[r] > run) run = e[r];
   }
-  const int32_t cmax = __shfl_sync(FULL_MASK, incl, 31);
+  const int32_t cmax = __shfl_sync(FULL_MASK, incl, L - 1);
   const int32_t top = cmax > 0 ? cmax : 0;
   if (policy == 0) {
     const unsigned bal = __ballot_sync(FULL_MASK, mine);

@@ -63,6 +63,9 @@
 #ifndef PLACE_SE_KEYS
 #define PLACE_SE_KEYS 1  // narrow variables sort (start << 32 | end) keys
 #endif
+#ifndef PLACE_SHORT_SCANS
+#define PLACE_SHORT_SCANS 1  // rows of <= 8 / 16 ranges: 3 / 4-level hole scans
+#endif
 #ifndef PLACE_SHORT_NETS
 #define PLACE_SHORT_NETS 1  // rows of <= 8 / 16 predecessors sort with an 8 / 16-wide network
 #endif
@@ -188,7 +191,7 @@ __device__ __forceinline__ int64_t place_reg(const PlaceArgs &a, int64_t rb, int
     for (int r = 0; r < K; r++) wide |= e[r] >= (int64_t)INT32_MAX;
     narrow = !__any_sync(FULL_MASK, wide);
   }
-  lvl = warp_max_i32(lv) + 1;
+  lvl = (int)__reduce_max_sync(FULL_MASK, (unsigned)lv) + 1;
   if (lane == 0) PT_STAMP(3, a.dbg_v);
   if constexpr ((PLACE_LANE_MAJOR && K >= PLACE_LM_KMIN) || (K == 1 && NARROW)) {
     // lane-major network and one-pass hole scan (place_dev.cuh)
@@ -213,6 +216,10 @@ __device__ __forceinline__ int64_t place_reg(const PlaceArgs &a, int64_t rb, int
       int32_t s32[K], e32[K];
 #pragma unroll
       for (int r = 0; r < K; r++) { s32[r] = (int32_t)(x[r] >> 32); e32[r] = (int32_t)(uint32_t)x[r]; }
+      if constexpr (K == 1 && PLACE_SHORT_SCANS) {
+        if (m <= 8) return hole_lm32<1, 8>(s32, e32, m, (int32_t)need, a.policy);
+        if (m <= 16) return hole_lm32<1, 16>(s32, e32, m, (int32_t)need, a.policy);
+      }
       return hole_lm32<K>(s32, e32, m, (int32_t)need, a.policy);
     }
     int64_t ss[K], es[K];
@@ -281,7 +288,7 @@ __device__ int64_t place_mem(const PlaceArgs &a, P buf, int64_t rb, int m, int64
     }
     buf[i] = x;
   }
-  lvl = warp_max_i32(lv) + 1;
+  lvl = (int)__reduce_max_sync(FULL_MASK, (unsigned)lv) + 1;
   __syncwarp();
   warp_bitonic_mem(buf, n2);
   HoleState h{0, 0, 0, false};
