@@ -99,12 +99,35 @@ void mp_set_err(mp_err *e, int32_t code, int64_t index, int64_t a0, int64_t a1, 
     }                                                                                   \
   } while (0)
 
+// Programmatic dependent launch: a kernel may be scheduled while the one
+// before it on the stream drains, and waits (griddepcontrol.wait, the first
+// statement of every kernel here) until that one has completed and its
+// writes are visible — the launch latency and block ramp-up of each kernel
+// overlap its predecessor's tail.  Every __global__ function in csrc/ starts
+// with PDL_WAIT() (tests/test_cpu_host.py checks it): a kernel that returned
+// before waiting could complete ahead of its predecessor and let the next
+// kernel read unfinished data.
+#ifndef MP_PDL
+#define MP_PDL 1
+#endif
+#define PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+
 // launch wrapper: counts launches on the context and checks the config
 #define LAUNCH(ctx, kernel, grid, block, smem, ...)                                      \
   do {                                                                                  \
     (ctx)->launches++;                                                                  \
-    kernel<<<(grid), (block), (smem), (ctx)->stream>>>(__VA_ARGS__);                    \
-    cudaError_t _le = cudaGetLastError();                                               \
+    cudaLaunchConfig_t _cfg = {};                                                       \
+    _cfg.gridDim = dim3(grid);                                                          \
+    _cfg.blockDim = dim3(block);                                                        \
+    _cfg.dynamicSmemBytes = (smem);                                                     \
+    _cfg.stream = (ctx)->stream;                                                        \
+    cudaLaunchAttribute _at[1];                                                         \
+    _at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;                     \
+    _at[0].val.programmaticStreamSerializationAllowed = MP_PDL;                         \
+    _cfg.attrs = _at;                                                                   \
+    _cfg.numAttrs = 1;                                                                  \
+    cudaError_t _le = cudaLaunchKernelEx(&_cfg, kernel, __VA_ARGS__);                   \
+    if (_le == cudaSuccess) _le = cudaGetLastError();                                   \
     if (_le != cudaSuccess) {                                                           \
       mp_set_err(err, MP_E_CUDA, 0, (int64_t)_le, __LINE__, cudaGetErrorString(_le));   \
       return MP_E_CUDA;                                                                 \

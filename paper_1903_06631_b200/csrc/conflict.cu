@@ -28,6 +28,7 @@ template <bool GENERAL>
 __global__ void k_norm_count(int64_t nv, const int64_t *seg_off, const int32_t *lo, const int32_t *hi,
                              int64_t *ecnt, int32_t *ea, int32_t *eb, int *overflow, int write,
                              const int64_t *eoff, int32_t *ivar) {
+  PDL_WAIT();
   // counting pass (write == 0): eb doubles as the (min start, max end) cell
   int32_t lmin = INT32_MAX, lmax = INT32_MIN;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
@@ -140,6 +141,7 @@ __global__ void k_norm_count(int64_t nv, const int64_t *seg_off, const int32_t *
 }
 
 __global__ void k_iv_keys(int64_t n, const int32_t *a, uint32_t *keys, uint32_t *vals) {
+  PDL_WAIT();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     keys[i] = (uint32_t)a[i] ^ 0x80000000u;  // order-preserving for signed bounds
     vals[i] = (uint32_t)i;
@@ -153,6 +155,7 @@ __global__ void k_iv_keys(int64_t n, const int32_t *a, uint32_t *keys, uint32_t 
 __global__ void k_iv_counts(int64_t n, const uint32_t *sstart, const uint32_t *perm, const uint32_t *send,
                             const int32_t *eb, int64_t *cnt, const int32_t *ivar, const int32_t *rank,
                             int32_t *sv) {
+  PDL_WAIT();
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
     uint32_t iid = perm[k];
     uint32_t a = sstart[k], b = (uint32_t)eb[iid] ^ 0x80000000u;
@@ -177,6 +180,7 @@ __global__ void k_iv_counts(int64_t n, const uint32_t *sstart, const uint32_t *p
 }
 
 __global__ void k_arena_need(int64_t V, const int64_t *row_off, unsigned long long *need) {
+  PDL_WAIT();
   unsigned long long s = 0;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
     int64_t d = row_off[v + 1] - row_off[v];
@@ -191,6 +195,7 @@ __global__ void k_arena_need(int64_t V, const int64_t *row_off, unsigned long lo
 }
 
 __global__ void k_iv_minmax(int64_t n, const int32_t *ea, const int32_t *eb, int *mm) {
+  PDL_WAIT();
   int lo = INT32_MAX, hi = INT32_MIN;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     lo = min(lo, ea[i]);
@@ -208,6 +213,7 @@ __global__ void k_iv_minmax(int64_t n, const int32_t *ea, const int32_t *eb, int
 }
 
 __global__ void k_iv_hist(int64_t n, const int32_t *ea, const int32_t *eb, int32_t base, int32_t *hs, int32_t *he) {
+  PDL_WAIT();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     atomicAdd(&hs[ea[i] - base], 1);
     atomicAdd(&he[eb[i] - base], 1);  // exclusive scan: cum_e[x - base + 1] = #ends <= x
@@ -216,6 +222,7 @@ __global__ void k_iv_hist(int64_t n, const int32_t *ea, const int32_t *eb, int32
 
 __global__ void k_iv_scatter(int64_t n, const int32_t *ea, int32_t base, const int32_t *offs, int32_t *cur,
                              uint32_t *perm) {
+  PDL_WAIT();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     int32_t x = ea[i] - base;
     perm[offs[x] + atomicAdd(&cur[x], 1)] = (uint32_t)i;
@@ -226,6 +233,7 @@ __global__ void k_iv_scatter(int64_t n, const int32_t *ea, int32_t base, const i
 __global__ void k_iv_counts_dense(int64_t n, const uint32_t *perm, const int32_t *ea, const int32_t *eb, int32_t base,
                                   const int32_t *offs, const int32_t *cum_e, int64_t *cnt, const int32_t *ivar,
                                   const int32_t *rank, int32_t *sv) {
+  PDL_WAIT();
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
     uint32_t iid = perm[k];
     int64_t f = (int64_t)offs[eb[iid] - base] - k - 1;
@@ -239,6 +247,7 @@ __global__ void k_iv_counts_dense(int64_t n, const uint32_t *perm, const int32_t
 }
 
 __global__ void k_row_off(int64_t nv, const int64_t *eoff, const int64_t *sub_off, int64_t *row_off) {
+  PDL_WAIT();
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v <= nv; v += (int64_t)gridDim.x * blockDim.x)
     row_off[v] = sub_off[eoff[v]];
 }
@@ -248,6 +257,7 @@ __global__ void k_row_off(int64_t nv, const int64_t *eoff, const int64_t *sub_of
 // successors from the row end) so plan_pool needs no separate split pass
 __global__ void k_iv_fill(int64_t n, const int32_t *sv, const int64_t *row_off, int32_t *pc, int32_t *sc,
                           int32_t *col) {
+  PDL_WAIT();
   const int lane = threadIdx.x & 31;
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -414,6 +424,7 @@ static int build_csr(mp_ctx *ctx, int64_t nv, const int64_t *seg_off_d, const in
 
 __global__ void k_prof_segs(int64_t nv, const int32_t *nseg, const int32_t *seg, int64_t *seg_off,
                             int32_t *lo, int32_t *hi) {
+  PDL_WAIT();
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
     seg_off[v] = 2 * v;
     int ns = nseg[v];
@@ -467,6 +478,7 @@ __device__ __forceinline__ int prof_effective(int ns, int4 sg, int32_t &a0, int3
 __global__ void k_prof_intervals(int64_t nv, const int32_t *nseg, const int32_t *seg, const int64_t *size,
                                  int32_t *ea, int32_t *eb, int64_t *cnt, unsigned long long *hse,
                                  unsigned long long *kmm) {
+  PDL_WAIT();
   unsigned long long lmn = ~0ull, lmx = 0;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
     const int4 sg = reinterpret_cast<const int4 *>(seg)[v];
@@ -506,6 +518,7 @@ __global__ void k_prof_intervals(int64_t nv, const int32_t *nseg, const int32_t 
 
 // slots in start order (counting sort; order among equal starts is free)
 __global__ void k_prof_scatter(int64_t nslots, const int32_t *ea, const int64_t *pref, int32_t *cur, uint32_t *perm) {
+  PDL_WAIT();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nslots; i += (int64_t)gridDim.x * blockDim.x) {
     const int32_t x = ea[i];
     if (x >= 0) perm[(int32_t)(uint32_t)pref[x] + atomicAdd(&cur[x], 1)] = (uint32_t)i;
@@ -515,6 +528,7 @@ __global__ void k_prof_scatter(int64_t nslots, const int32_t *ea, const int64_t 
 // k_iv_counts_dense with the slot's variable implicit (slot >> 1)
 __global__ void k_prof_counts(int64_t n, const uint32_t *perm, const int32_t *ea, const int32_t *eb,
                               const int64_t *pref, int64_t *cnt, const int32_t *rank, int32_t *sv) {
+  PDL_WAIT();
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t iid = perm[k];
     const int64_t f = (int64_t)(uint32_t)pref[eb[iid]] - k - 1;       // starts before the end
@@ -529,6 +543,7 @@ __global__ void k_prof_counts(int64_t n, const uint32_t *perm, const int32_t *ea
 
 // row bounds from the slot scan, and the long-row scratch bound
 __global__ void k_prof_rows(int64_t nv, const int64_t *sub_off, int64_t *row_off, unsigned long long *need) {
+  PDL_WAIT();
   unsigned long long s = 0;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v <= nv; v += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r0 = sub_off[2 * v];
@@ -694,6 +709,7 @@ extern "C" int mp_graph_free(mp_dgraph *g) {
 // rows of a host CSR split by placement order (warp per row)
 __global__ void k_partition_rows(int64_t V, const int64_t *row_off, const int32_t *col_in, const int32_t *rank,
                                  int32_t *col, int32_t *pcnt) {
+  PDL_WAIT();
   const int lane = threadIdx.x & 31;
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;

@@ -27,6 +27,7 @@
 // its own (ids without events get an empty run); the last position closes
 // the ids after the largest key.  n >= 1.
 __global__ void k_group_bounds(const uint32_t *skeys, int64_t n, int32_t nvars, int64_t *gstart) {
+  PDL_WAIT();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t cur = skeys[i];
     const int64_t prev = i ? (int64_t)skeys[i - 1] : -1;
@@ -61,6 +62,7 @@ int build_groups(mp_ctx *ctx, mp_dtrace *t, mp_err *err) {
 
 __global__ void k_validate_elem(const uint8_t *kind, const int64_t *size, const int64_t *t_us,
                                 const int64_t *index, int64_t n, int checks, unsigned long long *first) {
+  PDL_WAIT();
   for (int64_t pos = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; pos < n; pos += (int64_t)gridDim.x * blockDim.x) {
     int code = validate_elem_code(kind, size, t_us, index, pos, checks);
     if (code) atomicMin(first, ((unsigned long long)pos << 4) | (unsigned)code);
@@ -69,6 +71,7 @@ __global__ void k_validate_elem(const uint8_t *kind, const int64_t *size, const 
 
 __global__ void k_validate_var(const uint8_t *kind, const uint32_t *perm, const int64_t *gstart,
                                int32_t nvars, unsigned long long *first) {
+  PDL_WAIT();
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvars; v += (int64_t)gridDim.x * blockDim.x) {
     unsigned long long f = validate_var_first(kind, perm, gstart[v], gstart[v + 1]);
     if (f != NO_VIOLATION) atomicMin(first, f);
@@ -198,6 +201,7 @@ __device__ HPair block_scan_hash(HPair v, HPair *total) {
 }
 
 __global__ void __launch_bounds__(DT_THREADS) k_hash_tiles(const uint8_t *kind, const int64_t *size, int64_t n, HPair *tile_agg) {
+  PDL_WAIT();
   int64_t base = (int64_t)blockIdx.x * DT_TILE + (int64_t)threadIdx.x * DT_ITEMS;
   HPair a{0, 1};
   for (int i = 0; i < DT_ITEMS; i++) {
@@ -211,6 +215,7 @@ __global__ void __launch_bounds__(DT_THREADS) k_hash_tiles(const uint8_t *kind, 
 
 // exclusive prefix of the tile aggregates, one CTA in chunks of DT_THREADS
 __global__ void __launch_bounds__(DT_THREADS) k_hash_tile_prefix(HPair *agg, int64_t ntiles) {
+  PDL_WAIT();
   __shared__ HPair tot;
   HPair carry{0, 1};
   for (int64_t base = 0; base < ntiles; base += DT_THREADS) {
@@ -227,6 +232,7 @@ __global__ void __launch_bounds__(DT_THREADS) k_hash_tile_prefix(HPair *agg, int
 // P[i] = hash of events [0, i) for i in [0, n]
 __global__ void __launch_bounds__(DT_THREADS) k_hash_prefix(const uint8_t *kind, const int64_t *size, int64_t n,
                                                             const HPair *tile_pre, uint64_t *P) {
+  PDL_WAIT();
   int64_t base = (int64_t)blockIdx.x * DT_TILE + (int64_t)threadIdx.x * DT_ITEMS;
   HPair a{0, 1};
   uint64_t f[DT_ITEMS];
@@ -250,6 +256,7 @@ __global__ void __launch_bounds__(DT_THREADS) k_hash_prefix(const uint8_t *kind,
 // each thread tests a run of PC_RUN consecutive periods, carrying B^p along
 constexpr int PC_RUN = 32;
 __global__ void k_period_candidates(const uint64_t *P, int64_t n, int64_t pmin, unsigned long long *best) {
+  PDL_WAIT();
   int64_t nruns = (n / 2 - pmin + PC_RUN) / PC_RUN;
   for (int64_t run = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; run < nruns; run += (int64_t)gridDim.x * blockDim.x) {
     int64_t p0 = pmin + run * PC_RUN;
@@ -269,6 +276,7 @@ __global__ void k_period_candidates(const uint64_t *P, int64_t n, int64_t pmin, 
 
 __global__ void k_period_verify(const uint8_t *kind, const int64_t *size, int64_t n, const unsigned long long *pbest,
                                 int *bad) {
+  PDL_WAIT();
   unsigned long long pb = *pbest;
   if (pb == ~0ull) return;
   int64_t p = (int64_t)pb;
@@ -284,6 +292,7 @@ __global__ void k_period_verify(const uint8_t *kind, const int64_t *size, int64_
 // pairs, so the prefix hashes are only needed when that survivor fails.
 constexpr int DT_QUICK = 32;
 __global__ void k_period_quick(const uint8_t *kind, const int64_t *size, int64_t n, unsigned long long *best) {
+  PDL_WAIT();
   for (int64_t p = 1 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p <= n / 2;
        p += (int64_t)gridDim.x * blockDim.x) {
     const int64_t q = p < DT_QUICK ? p : DT_QUICK;
@@ -372,6 +381,7 @@ extern "C" int mp_detect(mp_ctx *ctx, mp_dtrace *t, int64_t *period, mp_err *err
 __global__ void k_ex_var(const uint8_t *kind, const int64_t *size, const uint32_t *perm,
                          const int64_t *gstart, int32_t nvars, int64_t start, int64_t end,
                          ExScratch s, unsigned long long *first) {
+  PDL_WAIT();
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvars; v += (int64_t)gridDim.x * blockDim.x) {
     unsigned long long f = ex_var_item(kind, size, perm, gstart, v, start, end, s);
     if (f != NO_VIOLATION) atomicMin(first, f);
@@ -382,6 +392,7 @@ __global__ void k_ex_var(const uint8_t *kind, const int64_t *size, const uint32_
 // launch: both only read k_ex_var's output or the trace)
 __global__ void k_ex_twin(const uint8_t *kind, const int64_t *size, int32_t nvars, int64_t start,
                           int64_t p, ExScratch s, int32_t *is_malloc) {
+  PDL_WAIT();
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvars; v += (int64_t)gridDim.x * blockDim.x)
     ex_twin_item(kind, size, v, start, p, s);
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < p; r += (int64_t)gridDim.x * blockDim.x)
@@ -394,6 +405,7 @@ __global__ void k_ex_fill_window(const int32_t *var, const int64_t *size, int64_
                                  int64_t ncarry, ExScratch s, const int32_t *win_ord,
                                  const int32_t *carry_survive, ProfOut o, int64_t *acc_cnt, int32_t nvars,
                                  const int32_t *carry_ord) {
+  PDL_WAIT();
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < p; r += (int64_t)gridDim.x * blockDim.x)
     ex_fill_window_item(var, size, start, r, p, ncarry, s, win_ord, carry_survive, o, acc_cnt);
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvars; v += (int64_t)gridDim.x * blockDim.x)
@@ -404,11 +416,13 @@ __global__ void k_ex_fill_window(const int32_t *var, const int64_t *size, int64_
 __global__ void k_ex_access(const uint8_t *kind, const uint32_t *perm, const int64_t *gstart,
                             int32_t nvars, int64_t start, int64_t end, int64_t ncarry, ExScratch s,
                             const int32_t *carry_ord, const int32_t *win_ord, ProfOut o) {
+  PDL_WAIT();
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvars; v += (int64_t)gridDim.x * blockDim.x)
     ex_access_item(kind, perm, gstart, v, start, end, ncarry, s, carry_ord, win_ord, o);
 }
 
 __global__ void k_ex_times(const int64_t *t_us, int64_t start, int64_t end, double *op_times, double *dur) {
+  PDL_WAIT();
   int64_t p = end - start;
   int64_t t0 = t_us[start];
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < p; r += (int64_t)gridDim.x * blockDim.x)
@@ -447,6 +461,7 @@ int trace_flush_tus(mp_ctx *ctx, mp_dtrace *t, mp_err *err) {
 
 __global__ void k_load_diff(int64_t nv, const int32_t *nseg, const int32_t *seg, const int64_t *size,
                             unsigned long long *diff) {
+  PDL_WAIT();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
     for (int s = 0; s < nseg[i]; s++) {
       atomicAdd(&diff[seg[4 * i + 2 * s]], (unsigned long long)size[i]);
@@ -460,6 +475,7 @@ __global__ void k_load_diff(int64_t nv, const int32_t *nseg, const int32_t *seg,
 // pairs (per-block cells, a finish counter it resets for the next call)
 __global__ void k_load_peak_idx(const int64_t *loads, int64_t p, long long *bmax, long long *bidx,
                                 unsigned int *finished, long long *peak, unsigned long long *idx) {
+  PDL_WAIT();
   long long m = LLONG_MIN, mi = LLONG_MAX;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < p; r += (int64_t)gridDim.x * blockDim.x) {
     const long long x = loads[r];

@@ -362,6 +362,7 @@ __device__ __forceinline__ int64_t place_var(const PlaceArgs &a, int32_t v, int6
 // barrier: a variable starts the moment its last predecessor is placed.
 template <bool REC, bool NARROW>
 __global__ void __launch_bounds__(PLACE_THREADS, PLACE_MIN_BLOCKS) k_place_async(PlaceArgs a) {
+  PDL_WAIT();
   const int lane = threadIdx.x & 31;
   int64_t gwarp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   long long fp = LLONG_MIN;
@@ -518,6 +519,7 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_MIN_BLOCKS) k_place_async
 // placement order and row partition
 
 __global__ void k_tie_keys(int64_t V, const int64_t *tiekey, uint64_t *keys, uint32_t *vals) {
+  PDL_WAIT();
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
     keys[v] = (uint64_t)tiekey[v] ^ 0x8000000000000000ull;
     vals[v] = (uint32_t)v;
@@ -527,6 +529,7 @@ __global__ void k_tie_keys(int64_t V, const int64_t *tiekey, uint64_t *keys, uin
 
 __global__ void k_size_keys(int64_t V, const int64_t *size, const uint32_t *vals, uint64_t *keys,
                             unsigned long long *mn, unsigned long long *mx) {
+  PDL_WAIT();
   unsigned long long lmn = ~0ull, lmx = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V; i += (int64_t)gridDim.x * blockDim.x) {
     uint64_t k = desc_size_key(size[vals[i]]);
@@ -547,23 +550,27 @@ __global__ void k_size_keys(int64_t V, const int64_t *size, const uint32_t *vals
 }
 
 __global__ void k_sub_keys(int64_t V, uint64_t *keys, const unsigned long long *mn) {
+  PDL_WAIT();
   uint64_t m = *mn;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V; i += (int64_t)gridDim.x * blockDim.x)
     keys[i] -= m;
 }
 
 __global__ void k_iota(int64_t V, uint32_t *vals) {
+  PDL_WAIT();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V; i += (int64_t)gridDim.x * blockDim.x)
     vals[i] = (uint32_t)i;
 }
 
 __global__ void k_rank(int64_t V, const uint32_t *order, int32_t *rank) {
+  PDL_WAIT();
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < V; q += (int64_t)gridDim.x * blockDim.x)
     rank[order[q]] = (int32_t)q;
 }
 
 __global__ void k_ready_init(int64_t V, const int32_t *pcnt, int32_t *remaining, int32_t *queue, int32_t *tail,
                              unsigned long long *arena_need) {
+  PDL_WAIT();
   unsigned long long need = 0;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
     int c = pcnt[v];
@@ -591,6 +598,7 @@ __global__ void k_ready_init(int64_t V, const int32_t *pcnt, int32_t *remaining,
 
 // placement rank of every vertex: (-size, tiekey or vertex index)
 __global__ void k_size_range(int64_t V, const int64_t *size, unsigned long long *mm) {
+  PDL_WAIT();
   unsigned long long lmn = ~0ull, lmx = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V; i += (int64_t)gridDim.x * blockDim.x) {
     uint64_t k = desc_size_key(size[i]);
@@ -620,6 +628,7 @@ int placement_rank_keys(mp_ctx *ctx, int64_t V, const int64_t *size, unsigned lo
 
 // rank[v] = position in (-size, tiekey or vertex) order, size keys in [kmin, kmax]
 __global__ void k_size_keys32(int64_t V, const int64_t *size, uint64_t kmin, uint32_t *keys, uint32_t *vals) {
+  PDL_WAIT();
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
     keys[v] = (uint32_t)(desc_size_key(size[v]) - kmin);
     vals[v] = (uint32_t)v;

@@ -77,6 +77,7 @@ template <typename T, bool INCL>
 __global__ void __launch_bounds__(SCAN_THREADS) k_scan_onepass(const T *in, T *out, int64_t n, int32_t *flags,
                                                                T *agg, T *incl, int32_t *tile_ctr, T *total,
                                                                int32_t epoch, uint32_t tile_base) {
+  PDL_WAIT();
   __shared__ int32_t s_tile;
   __shared__ T s_excl, s_tot;
   // flags hold (epoch << 2) | status: a value from an earlier scan reads as
@@ -259,6 +260,7 @@ constexpr int OS_MAX_PASSES = 8;
 
 template <typename K>
 __global__ void __launch_bounds__(RS_THREADS) k_os_hist(const K *keys, int64_t n, int passes, int32_t *ghist) {
+  PDL_WAIT();
   __shared__ int32_t h[OS_MAX_PASSES][RS_BINS];
   for (int i = threadIdx.x; i < passes * RS_BINS; i += RS_THREADS) h[i / RS_BINS][i % RS_BINS] = 0;
   __syncthreads();
@@ -275,6 +277,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_os_hist(const K *keys, int64_t n
 
 // per pass: exclusive prefix of the 256 digit counts (one warp per pass)
 __global__ void k_os_prefix(int32_t *ghist, int passes) {
+  PDL_WAIT();
   const int lane = threadIdx.x & 31, p = threadIdx.x >> 5;
   if (p >= passes) return;
   int32_t c = 0;
@@ -291,6 +294,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_os_pass(const K *keys, const uin
                                                          uint32_t *ovals, int64_t n, int shift,
                                                          const int32_t *gstart, uint32_t *look,
                                                          int32_t *tile_ctr) {
+  PDL_WAIT();
   constexpr int TILE = RS_THREADS * ITEMS;
   constexpr int PER_WARP = 32 * ITEMS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -447,6 +451,7 @@ __device__ __forceinline__ unsigned multisplit_peers(unsigned d, unsigned valid)
 template <typename K, int RB, int ITEMS>
 __global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const K *keys, int64_t n, int shift, int32_t ntiles,
                                                         int32_t *mat) {
+  PDL_WAIT();
   constexpr int BINS = 1 << RB;
   constexpr int TILE = RS_THREADS * ITEMS;
   constexpr int VK = 16 / sizeof(K);  // keys per 16-byte vector
@@ -492,6 +497,7 @@ template <typename K, int RB, int ITEMS>
 __global__ void __launch_bounds__(RS_THREADS, RS_MINB) k_rs_scatter(const K *keys, const uint32_t *vals, K *okeys,
                                                            uint32_t *ovals, int64_t n, int shift, int32_t ntiles,
                                                            const int32_t *offs) {
+  PDL_WAIT();
   constexpr int BINS = 1 << RB;
   constexpr int TILE = RS_THREADS * ITEMS;
   constexpr int PER_WARP = 32 * ITEMS;
@@ -591,6 +597,7 @@ __global__ void __launch_bounds__(RS_THREADS, RS_MINB) k_rs_scatter(const K *key
 }
 
 __global__ void k_rs_iota(uint32_t *v, int64_t n) {
+  PDL_WAIT();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     v[i] = (uint32_t)i;
 }

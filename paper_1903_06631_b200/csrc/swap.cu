@@ -60,6 +60,7 @@ __global__ void k_swap_candidates(int64_t V, int64_t p, int64_t peak, const int6
                                   const int64_t *acc_off, const int32_t *acc_index, const uint8_t *acc_next,
                                   const double *op_times, double duration, int64_t threshold, double bw, double lat,
                                   int32_t *flag, CandOut o) {
+  PDL_WAIT();
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x)
     flag[v] = cand_item(v, v, p, peak, size, flags, acc_off, acc_index, acc_next, op_times, duration, threshold, bw,
                         lat, o);
@@ -67,6 +68,7 @@ __global__ void k_swap_candidates(int64_t V, int64_t p, int64_t peak, const int6
 
 template <typename T>
 __global__ void k_compact(int64_t V, const int32_t *flag, const int32_t *pos, const T *src, T *dst) {
+  PDL_WAIT();
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x)
     if (flag[v]) dst[pos[v]] = src[v];
 }
@@ -134,6 +136,7 @@ extern "C" int mp_swap_candidates(mp_ctx *ctx, mp_dprofile *P, int64_t threshold
 // gap areas
 
 __global__ void k_gap_areas(LoadView L, CandView c, const double *cur, double *area) {
+  PDL_WAIT();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.k; i += (int64_t)gridDim.x * blockDim.x)
     area[i] = gap_area(L, cur, c.out_t[i], c.in_t[i]);
 }
@@ -143,6 +146,7 @@ __global__ void __launch_bounds__(512) k_swap_greedy(LoadView L, CandView c, dou
                                                      double *doa, double *aoa, double *wdoa, double *swdoa,
                                                      int32_t *order, double *peaks, int64_t *W, int32_t *jx,
                                                      int64_t *area) {
+  PDL_WAIT();
   __shared__ SwKey keys[33];
   __shared__ long long sm[PM_SMEM];
   swdoa_greedy_block(CtaGroup{}, L, c, cur, taken, doa, aoa, wdoa, swdoa, order, peaks, W, jx, keys, sm, -1, area);
@@ -225,6 +229,7 @@ extern "C" int mp_swap_gap_area(mp_ctx *ctx, mp_dprofile *P, const mp_cands_io *
 __global__ void __launch_bounds__(512) k_swap_static(LoadView L, CandView c, const double *ranked, int64_t limit,
                                                      double *cur, int32_t *ord, int32_t *sel, int64_t *nsel,
                                                      double *peak_out) {
+  PDL_WAIT();
   __shared__ double red[33];
   const int64_t p = L.p, k = c.k;
   // order by (-ranked, -size, name): rank_i = #keys smaller than key_i
@@ -305,6 +310,7 @@ __device__ __forceinline__ double dkey_inv(unsigned long long k) {
 
 __global__ void k_planned_peak(LoadView L, CandView c, const int32_t *subset, int64_t nsub,
                                unsigned long long *best) {
+  PDL_WAIT();
   const int64_t p = L.p;
   unsigned long long m = 0;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < p; r += (int64_t)gridDim.x * blockDim.x) {
@@ -364,6 +370,7 @@ extern "C" int mp_swap_planned_peak(mp_ctx *ctx, mp_dprofile *P, const mp_cands_
 
 __global__ void k_swap_schedule(CandView c, const int32_t *sel, int64_t n, const double *ready, const double *deadline,
                                 double *t_so, double *t_eo, double *t_si, double *t_ei, int32_t *eord, SimScratch S) {
+  PDL_WAIT();
   if (blockIdx.x || threadIdx.x >= 32) return;
   make_schedule(c, sel, n, ready, deadline, t_so, t_eo, t_si, t_ei, eord, S);
 }
@@ -410,6 +417,7 @@ struct SimOutDev {
 };
 
 __global__ void k_op_deltas(ProfView P, int64_t *delta, unsigned long long *live0) {
+  PDL_WAIT();
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < P.V; v += (int64_t)gridDim.x * blockDim.x) {
     for (int s = 0; s < P.nseg[v]; s++) {
       int64_t lo = P.seg[4 * v + 2 * s], hi = P.seg[4 * v + 2 * s + 1];
@@ -422,6 +430,7 @@ __global__ void k_op_deltas(ProfView P, int64_t *delta, unsigned long long *live
 
 __global__ void k_swap_simulate(ProfView P, CandView c, const int32_t *sel, int64_t n, int64_t limit, int has_limit,
                                 int max_rounds, const unsigned long long *live0p, SimScratch S, SimOutDev O) {
+  PDL_WAIT();
   if (blockIdx.x || threadIdx.x >= 32) return;  // one warp
   const int lane = threadIdx.x;
   int64_t live0 = (int64_t)*live0p;
@@ -461,6 +470,7 @@ __global__ void k_swap_simulate(ProfView P, CandView c, const int32_t *sel, int6
 // the delayed-op list of the last replay, recomputed from actual starts
 __global__ void k_sim_delays(ProfView P, const double *actual, double delay_total, int64_t *dl_idx, double *dl_us,
                              int64_t *ndl) {
+  PDL_WAIT();
   (void)delay_total;
   if (threadIdx.x || blockIdx.x) return;
   // a delayed op r adds (t - t0) where t0 = tau[r] + accumulated delay
@@ -651,11 +661,13 @@ __device__ __forceinline__ double warp_pymax_cur(const double *cur, int64_t p) {
 }
 
 __global__ void k_op_events(ProfView P, const int64_t *delta, double *ev_t, int64_t *ev_d, int64_t *na) {
+  PDL_WAIT();
   if (blockIdx.x || threadIdx.x) return;
   *na = sim_op_events(P, delta, ev_t, ev_d);
 }
 
 __global__ void __launch_bounds__(128) k_swap_eval_weights(EvalArgs a) {
+  PDL_WAIT();
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;

@@ -1048,6 +1048,7 @@ __device__ void sweep_one(const SweepArgs &a, int64_t t, char *slab, char *fast,
 }
 
 __global__ void __launch_bounds__(SW_THREADS) k_sweep(SweepArgs a, size_t fast_bytes) {
+  PDL_WAIT();
   __shared__ SweepShared sh;
   __shared__ int32_t s_item;
   extern __shared__ __align__(16) char s_fast[];

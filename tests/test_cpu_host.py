@@ -193,3 +193,24 @@ def test_brute_force_search_host_c_matches_python():
         N.lib().mp_brute_force_footprint(C.c_int32(n), N.ptr(sz), N.ptr(nb_off), N.ptr(nb), N.ptr(cd),
                                          C.c_int64(len(cands)), C.c_int64(lower), C.byref(out))
         assert out.value == py_search(sizes, earlier, cands, lower, start)
+
+
+def test_every_kernel_waits_for_its_predecessor_first():
+    """Kernels are launched with programmatic dependent launch (common.cuh
+    LAUNCH): each may be scheduled while the kernel before it drains, so each
+    must execute griddepcontrol.wait before anything else — a kernel that
+    returned (or read its inputs) before waiting could complete ahead of its
+    predecessor and let the next kernel read unfinished data."""
+    import glob
+    import re
+    csrc = os.path.join(ROOT, "paper_1903_06631_b200", "csrc")
+    bad, n = [], 0
+    for path in sorted(glob.glob(os.path.join(csrc, "*.cu")) + glob.glob(os.path.join(csrc, "*.cuh"))):
+        src = re.sub(r"//[^\n]*", "", open(path).read())
+        for m in re.finditer(r"__global__[^;{]*\{", src):
+            n += 1
+            body = src[m.end():m.end() + 200].lstrip()
+            if not body.startswith("PDL_WAIT();"):
+                bad.append(f"{os.path.basename(path)}: {m.group(0)[:80]}")
+    assert n > 40
+    assert not bad, bad
