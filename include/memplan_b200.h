@@ -197,6 +197,11 @@ int mp_validate_times(mp_ctx *ctx, mp_dtrace *t, mp_err *err);
 /* detect_iteration (iteration.py:93-105): smallest p with the last 2p
  * (kind, size) fingerprints equal pairwise; window = (n - p, n). */
 int mp_detect(mp_ctx *ctx, mp_dtrace *t, int64_t *period, mp_err *err);
+/* detect_iteration after validate_trace with one readback for both: a
+ * violation is reported first (structure_only: everything but timestamps, a
+ * violation then re-decided by the full pass, as mp_validate_structure);
+ * without a period the full validation runs before PeriodNotFound. */
+int mp_detect_validate(mp_ctx *ctx, mp_dtrace *t, int32_t structure_only, int64_t *period, mp_err *err);
 
 /* extract_lifetimes (iteration.py:275-301) incl. build_profile and
  * compute_load_profile (iteration.py:135-272, 304-320). */

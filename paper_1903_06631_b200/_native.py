@@ -167,6 +167,18 @@ def detect(arrays) -> int:
     return int(p.value)
 
 
+def detect_validate(arrays, checks: str = "all") -> int:
+    """validate_trace then detect_iteration with one device round trip
+    (mp_detect_validate); raises what validate, then detect, would."""
+    t = device_trace(arrays)
+    p = C.c_int64(0)
+    err = MpErr()
+    rc = lib().mp_detect_validate(ctx(), t.h, C.c_int32(1 if checks == "structure" else 0), C.byref(p),
+                                  C.byref(err))
+    raise_for(rc, err, arrays.names)
+    return int(p.value)
+
+
 def extract(arrays, start: int, end: int) -> DProfile:
     t = device_trace(arrays)
     h = C.c_void_p()

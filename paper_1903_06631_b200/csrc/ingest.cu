@@ -303,6 +303,48 @@ __global__ void k_period_quick(const uint8_t *kind, const int64_t *size, int64_t
   }
 }
 
+// the hash search above pmin (the quick filter's smallest survivor was not a
+// period): fingerprint hash tiles, prefix hashes, every candidate, exact check
+static int detect_hash(mp_ctx *ctx, mp_dtrace *t, int64_t pmin, int64_t *period, mp_err *err) {
+  const int64_t n = t->n;
+  unsigned long long *d_best = (unsigned long long *)ctx->d_small;
+  int *d_bad = (int *)(ctx->d_small + 1);
+  int64_t ntiles = (n + DT_TILE - 1) / DT_TILE;
+  DBuf<HPair> agg;
+  DBuf<uint64_t> P;
+  CUDA_TRY(agg.alloc(ntiles, ctx->stream));
+  CUDA_TRY(P.alloc(n + 1, ctx->stream));
+  LAUNCH(ctx, k_hash_tiles, (unsigned)ntiles, DT_THREADS, 0, t->kind.p, t->size.p, n, agg.p);
+  LAUNCH(ctx, k_hash_tile_prefix, 1, DT_THREADS, 0, agg.p, ntiles);
+  LAUNCH(ctx, k_hash_prefix, (unsigned)ntiles, DT_THREADS, 0, t->kind.p, t->size.p, n, agg.p, P.p);
+  for (;;) {
+    if (pmin > n / 2) {
+      mp_set_err(err, MP_E_PERIOD_NOT_FOUND, n, 0, 0, "no period");
+      return MP_E_PERIOD_NOT_FOUND;
+    }
+    CUDA_TRY(cudaMemsetAsync(d_best, 0xff, 8, ctx->stream));
+    CUDA_TRY(cudaMemsetAsync(d_bad, 0, 4, ctx->stream));
+    LAUNCH(ctx, k_period_candidates, grid_for((n / 2 - pmin + PC_RUN) / PC_RUN, 256, 8192), 256, 0, P.p, n, pmin,
+           d_best);
+    // exact check of the smallest hash match, read back together with it
+    LAUNCH(ctx, k_period_verify, grid_for(n / 2, 256, 4096), 256, 0, t->kind.p, t->size.p, n,
+           (const unsigned long long *)d_best, d_bad);
+    int64_t h[2];
+    int rc = dev_read_n(ctx, d_best, h, 16, err);
+    if (rc) return rc;
+    int64_t best = h[0];
+    if ((uint64_t)best == ~0ull) {
+      mp_set_err(err, MP_E_PERIOD_NOT_FOUND, n, 0, 0, "no period");
+      return MP_E_PERIOD_NOT_FOUND;
+    }
+    if (!(int)h[1]) {
+      *period = best;
+      return MP_OK;
+    }
+    pmin = best + 1;  // hash collision: keep searching above it
+  }
+}
+
 extern "C" int mp_detect(mp_ctx *ctx, mp_dtrace *t, int64_t *period, mp_err *err) {
   CTX_GUARD(ctx);
   int64_t n = t->n;
@@ -339,41 +381,73 @@ extern "C" int mp_detect(mp_ctx *ctx, mp_dtrace *t, int64_t *period, mp_err *err
     }
     pmin = h[0] + 1;  // the smallest survivor is not a period: hash search above it
   }
-  int64_t ntiles = (n + DT_TILE - 1) / DT_TILE;
-  DBuf<HPair> agg;
-  DBuf<uint64_t> P;
-  CUDA_TRY(agg.alloc(ntiles, ctx->stream));
-  CUDA_TRY(P.alloc(n + 1, ctx->stream));
-  LAUNCH(ctx, k_hash_tiles, (unsigned)ntiles, DT_THREADS, 0, t->kind.p, t->size.p, n, agg.p);
-  LAUNCH(ctx, k_hash_tile_prefix, 1, DT_THREADS, 0, agg.p, ntiles);
-  LAUNCH(ctx, k_hash_prefix, (unsigned)ntiles, DT_THREADS, 0, t->kind.p, t->size.p, n, agg.p, P.p);
-  for (;;) {
-    if (pmin > n / 2) {
-      mp_set_err(err, MP_E_PERIOD_NOT_FOUND, n, 0, 0, "no period");
-      return MP_E_PERIOD_NOT_FOUND;
-    }
+  return detect_hash(ctx, t, pmin, period, err);
+}
+
+// detect_iteration and validate_trace in one round trip: the quick period
+// filter + exact check and the validation kernels run back to back and one
+// readback returns both.  A violation takes precedence (the reference
+// validates first); a structural one is re-decided by the full pass, as
+// mp_validate_structure does.  No period: the full validation decides between
+// InvariantViolation and PeriodNotFound, as the pipeline's own fallback does.
+extern "C" int mp_detect_validate(mp_ctx *ctx, mp_dtrace *t, int32_t structure_only, int64_t *period,
+                                  mp_err *err) {
+  CTX_GUARD(ctx);
+  const int64_t n = t->n;
+  const int checks = structure_only ? VC_STRUCT : VC_ALL;
+  if (n < 2) {
+    int rc = validate_checks(ctx, t, VC_ALL, err);
+    if (rc) return rc;
+    mp_set_err(err, MP_E_PERIOD_NOT_FOUND, n, 0, 0, "no period");
+    return MP_E_PERIOD_NOT_FOUND;
+  }
+  int rc = build_groups(ctx, t, err);
+  if (rc) return rc;
+  rc = trace_need(ctx, t, checks == VC_ALL ? TC_ALL : TC_ALL & ~TC_TUS, err);
+  if (rc) return rc;
+  // d_small: [0] first violation, [2] best period, [3] its exact check
+  unsigned long long *d_first = (unsigned long long *)ctx->d_small;
+  unsigned long long *d_best = (unsigned long long *)(ctx->d_small + 2);
+  int *d_bad = (int *)(ctx->d_small + 3);
+  {
+    StageTimer tm(ctx, MP_ST_DETECT);
     CUDA_TRY(cudaMemsetAsync(d_best, 0xff, 8, ctx->stream));
     CUDA_TRY(cudaMemsetAsync(d_bad, 0, 4, ctx->stream));
-    LAUNCH(ctx, k_period_candidates, grid_for((n / 2 - pmin + PC_RUN) / PC_RUN, 256, 8192), 256, 0, P.p, n, pmin,
-           d_best);
-    // exact check of the smallest hash match, read back together with it
+    LAUNCH(ctx, k_period_quick, grid_for(n / 2, 256, 16384), 256, 0, t->kind.p, t->size.p, n, d_best);
     LAUNCH(ctx, k_period_verify, grid_for(n / 2, 256, 4096), 256, 0, t->kind.p, t->size.p, n,
            (const unsigned long long *)d_best, d_bad);
-    int64_t h[2];
-    int rc = dev_read_n(ctx, d_best, h, 16, err);
-    if (rc) return rc;
-    int64_t best = h[0];
-    if ((uint64_t)best == ~0ull) {
-      mp_set_err(err, MP_E_PERIOD_NOT_FOUND, n, 0, 0, "no period");
-      return MP_E_PERIOD_NOT_FOUND;
-    }
-    if (!(int)h[1]) {
-      *period = best;
-      return MP_OK;
-    }
-    pmin = best + 1;  // hash collision: keep searching above it
   }
+  {
+    StageTimer tm(ctx, MP_ST_VALIDATE);
+    CUDA_TRY(cudaMemsetAsync(d_first, 0xff, 8, ctx->stream));
+    LAUNCH(ctx, k_validate_elem, grid_for(n, 256, 4096), 256, 0, t->kind.p, t->size.p, t->t_us.p, t->index.p, n,
+           checks, d_first);
+    LAUNCH(ctx, k_validate_var, grid_for(t->nvars, 256), 256, 0, t->kind.p, t->perm.p, t->gstart.p, t->nvars,
+           d_first);
+  }
+  int64_t h[4];
+  rc = dev_read_n(ctx, ctx->d_small, h, 32, err);
+  if (rc) return rc;
+  if ((uint64_t)h[0] != ~0ull) return validate_checks(ctx, t, VC_ALL, err);  // names the first violation
+  if ((uint64_t)h[2] == ~0ull) {
+    rc = validate_checks(ctx, t, VC_ALL, err);
+    if (rc) return rc;
+    mp_set_err(err, MP_E_PERIOD_NOT_FOUND, n, 0, 0, "no period");
+    return MP_E_PERIOD_NOT_FOUND;
+  }
+  if (!(int)h[3]) {
+    *period = h[2];
+    return MP_OK;
+  }
+  rc = detect_hash(ctx, t, h[2] + 1, period, err);
+  if (rc == MP_E_PERIOD_NOT_FOUND) {
+    mp_err e2{};
+    const int vr = validate_checks(ctx, t, VC_ALL, &e2);
+    if (vr) { *err = e2; return vr; }
+  }
+  return rc;
 }
+
 
 // ---------------------------------------------------------------------------
 // extract_lifetimes

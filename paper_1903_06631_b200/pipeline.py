@@ -73,17 +73,23 @@ def plan_arrays(arrays: TraceArrays, window: tuple[int, int] | None = None,
     dev = N.device_trace(arrays, asynchronous=True)
     try:
         N.lib().mp_trace_reset(dev.h)
-        if window is None:
-            try:
-                p = N.detect(arrays)
-            except (MemplanError, ValueError):
-                if validate:
-                    N.validate(arrays)
-                raise
+        if window is None and validate:
+            # validation and period detection share one readback; a violation
+            # wins, and without a period the full validation decides first
+            p = N.detect_validate(arrays, "structure" if fresh else "all")
             window = (len(arrays) - p, len(arrays))
-        if validate:
-            # a resident trace has every column: one pass, one readback
-            N.validate(arrays, "structure" if fresh else "all")
+        else:
+            if window is None:
+                try:
+                    p = N.detect(arrays)
+                except (MemplanError, ValueError):
+                    if validate:
+                        N.validate(arrays)
+                    raise
+                window = (len(arrays) - p, len(arrays))
+            if validate:
+                # a resident trace has every column: one pass, one readback
+                N.validate(arrays, "structure" if fresh else "all")
         try:
             dp = N.extract(arrays, window[0], window[1])
             g = N.conflict_from_profile(dp)
