@@ -218,6 +218,7 @@ extern "C" int mp_profile_download(mp_ctx *ctx, mp_dprofile *P, mp_profile_out *
 
 extern "C" int mp_profile_free(mp_dprofile *p) {
   CTX_GUARD(p->ctx);
+  if (p->ctx->dims_owner == p) p->ctx->dims_owner = nullptr;
   if (p->times_src) {  // still registered with a deferred timestamp upload
     auto &w = p->times_src->tus_waiters;
     for (size_t i = 0; i < w.size(); i++)
@@ -317,7 +318,9 @@ extern "C" int mp_standardize(const double *x, int64_t n, double *out) {
 extern "C" int mp_profile_compute_loads(mp_ctx *ctx, mp_dprofile *P, int64_t *loads, int64_t *peak,
                                         int64_t *peak_index, mp_err *err) {
   CTX_GUARD(ctx);
-  int rc = profile_loads(ctx, P, err);
+  int rc = profile_dims(ctx, P, err);  // settle the extraction's values before recomputing
+  if (rc) return rc;
+  rc = profile_loads(ctx, P, err);
   if (rc) return rc;
   if (P->d.period) CUDA_TRY(cudaMemcpyAsync(loads, P->loads.p, P->d.period * 8, cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));

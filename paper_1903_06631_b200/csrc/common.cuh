@@ -47,6 +47,11 @@ struct mp_ctx {
   int64_t scan_cap = 0;
   uint32_t scan_epoch = 0;
   uint32_t scan_base = 0;
+  // the last extraction's final scalars (peak, peak index, access count,
+  // duration) travel to h_small[40..43] asynchronously; dims_owner is the
+  // profile they belong to until read (handles.cuh profile_dims)
+  struct mp_dprofile *dims_owner = nullptr;
+  cudaEvent_t dims_ev = nullptr;
   // stage timing (CUDA events on `stream`)
   bool timing = false;
   std::vector<mp_stage_rec> pending;

@@ -634,6 +634,8 @@ extern "C" int mp_conflict_from_profile(mp_ctx *ctx, mp_dprofile *P, mp_dgraph *
     CUDA_TRY(cudaMemcpyAsync(g->size.p, P->size.p, nv * 8, cudaMemcpyDeviceToDevice, st));
     int rc = build_csr_profile(ctx, P, g, err);
     if (rc) { delete g; return rc; }
+    rc = profile_dims(ctx, P, err);  // drained by the build's readbacks: no wait
+    if (rc) { delete g; return rc; }
     g->peak_hint = P->d.peak_bytes;
     *out = g;
     return MP_OK;
@@ -650,6 +652,8 @@ extern "C" int mp_conflict_from_profile(mp_ctx *ctx, mp_dprofile *P, mp_dgraph *
   // profile variables are already in (alloc or -1, name) order: the
   // placement tie-break is the vertex index
   int rc = build_csr(ctx, nv, so.p, lo.p, hi.p, false, g, err);
+  if (rc) { delete g; return rc; }
+  rc = profile_dims(ctx, P, err);
   if (rc) { delete g; return rc; }
   g->peak_hint = P->d.peak_bytes;
   *out = g;

@@ -70,14 +70,36 @@ struct mp_dprofile {
   // trace whose t_us column is still in flight): ready at times_ev
   cudaEvent_t times_ev = nullptr;
   bool times_pending = false;
+  // peak / peak index / access count (and the duration unless times are
+  // late) still on their way to ctx->h_small[40..43] (profile_dims)
+  bool dims_pending = false, dims_late_times = false;
   DBuf<double> dur;
   mp_dtrace *times_src = nullptr;  // registered with a deferred timestamp upload
   int64_t times_start = 0, times_end = 0;
 };
 
+// the extraction's final scalars, read back without a stream sync of its own
+inline int profile_dims(mp_ctx *ctx, mp_dprofile *P, mp_err *err) {
+  if (!P->dims_pending) return MP_OK;
+  CUDA_TRY(cudaEventSynchronize(ctx->dims_ev));
+  const int64_t *h = ctx->h_small + 40;
+  const int64_t p = P->d.period;
+  P->d.peak_bytes = p ? h[0] : 0;
+  P->d.peak_index = p ? h[1] : 0;
+  P->d.naccess = h[2];
+  if (!P->dims_late_times) memcpy(&P->d.duration_us, &h[3], 8);
+  P->dims_pending = false;
+  if (ctx->dims_owner == P) ctx->dims_owner = nullptr;
+  return MP_OK;
+}
+
 // wait for deferred op times (device order on the context stream, and the
-// period duration on the host)
+// period duration on the host); resolves the deferred dims first
 inline int profile_times(mp_ctx *ctx, mp_dprofile *P, mp_err *err) {
+  {
+    int rc = profile_dims(ctx, P, err);
+    if (rc) return rc;
+  }
   if (!P->times_pending) return MP_OK;
   if (P->times_src) {
     int rc = trace_flush_tus(ctx, P->times_src, err);

@@ -778,14 +778,19 @@ extern "C" int mp_extract(mp_ctx *ctx, mp_dtrace *t, int64_t start, int64_t end,
   delete tm;
   rc = profile_loads_async(ctx, P, err);
   if (rc) { delete P; return rc; }
-  // one readback: peak, peak index, access count, period duration
-  int64_t fin[4];
-  rc = dev_read_n(ctx, ctx->d_small, fin, 32, err);
-  if (rc) { delete P; return rc; }
-  P->d.peak_bytes = p ? fin[0] : 0;
-  P->d.peak_index = p ? fin[1] : 0;
-  P->d.naccess = fin[2];
-  if (!late_times) memcpy(&P->d.duration_us, &fin[3], 8);
+  // peak, peak index, access count, period duration: copied to pinned
+  // memory without waiting (whoever reads them first calls profile_dims —
+  // the conflict build's own readback has drained the stream by then)
+  if (ctx->dims_owner) {
+    rc = profile_dims(ctx, ctx->dims_owner, err);
+    if (rc) { delete P; return rc; }
+  }
+  if (!ctx->dims_ev) CUDA_TRY(cudaEventCreateWithFlags(&ctx->dims_ev, cudaEventDisableTiming));
+  CUDA_TRY(cudaMemcpyAsync(ctx->h_small + 40, ctx->d_small, 32, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaEventRecord(ctx->dims_ev, st));
+  P->dims_pending = true;
+  P->dims_late_times = late_times;
+  ctx->dims_owner = P;
   P->nnames = t->nvars;
   *out = P;
   return MP_OK;
