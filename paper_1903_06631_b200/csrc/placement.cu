@@ -571,13 +571,23 @@ __global__ void k_rank(int64_t V, const uint32_t *order, int32_t *rank) {
     rank[order[q]] = (int32_t)q;
 }
 
+// counters, the initial ready queue, the placement sentinels (record
+// all-ones, or offset -1 / level 0) and the footprint's starting value
 __global__ void k_ready_init(int64_t V, const int32_t *pcnt, int32_t *remaining, int32_t *queue, int32_t *tail,
-                             unsigned long long *arena_need) {
+                             unsigned long long *arena_need, longlong2 *rec, int64_t *off, int32_t *level,
+                             long long *footprint) {
   PDL_WAIT();
+  if (blockIdx.x == 0 && threadIdx.x == 0) *footprint = LLONG_MIN;
   unsigned long long need = 0;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
     int c = pcnt[v];
     remaining[v] = c;
+    if (rec) {
+      rec[v] = make_longlong2(-1, -1);
+    } else {
+      off[v] = -1;
+      level[v] = 0;
+    }
     if (c > 128) {
       unsigned long long n2 = 64;
       while (n2 < (unsigned long long)c) n2 <<= 1;
@@ -744,13 +754,7 @@ extern "C" int mp_plan_pool(mp_ctx *ctx, mp_dgraph *g, int32_t policy, int64_t *
   // sentinels: -1 offsets, level 0 or -1 (see pred_range)
   DBuf<longlong2> rec;
   const bool use_rec = PLACE_REC && g->size_lo >= 0 && g->size_hi <= (int64_t)0xffffffffll;
-  if (use_rec) {
-    CUDA_TRY(rec.alloc(V, st));
-    CUDA_TRY(cudaMemsetAsync(rec.p, 0xff, V * 16, st));
-  } else {
-    CUDA_TRY(cudaMemsetAsync(off.p, 0xff, V * 8, st));
-    CUDA_TRY(cudaMemsetAsync(level.p, 0, V * 4, st));
-  }
+  if (use_rec) CUDA_TRY(rec.alloc(V, st));  // sentinels written by k_ready_init
   size_t smem = 0;
   // the 32-bit hole scan pays off only when the pool fits 2^31 bytes: the
   // narrow kernel when the traced peak (a lower bound of the footprint) does
@@ -786,10 +790,8 @@ extern "C" int mp_plan_pool(mp_ctx *ctx, mp_dgraph *g, int32_t policy, int64_t *
       StageTimer tm(ctx, MP_ST_PLACE_SPLIT);
       CUDA_TRY(cudaMemsetAsync(queue.p, 0, V * 4, st));
       CUDA_TRY(cudaMemsetAsync(ctr.p, 0, 64, st));
-      const long long lmin = LLONG_MIN;
-      CUDA_TRY(cudaMemcpyAsync(d_fp, &lmin, 8, cudaMemcpyHostToDevice, st));
       LAUNCH(ctx, k_ready_init, grid_for(V, 256, 2048), 256, 0, V, g->pcnt.p, remaining.p, queue.p, ctr.p + 1,
-             d_need);
+             d_need, use_rec ? rec.p : (longlong2 *)nullptr, off.p, level.p, d_fp);
     }
     StageTimer ptm(ctx, MP_ST_PLACE);
     LAUNCH(ctx, kern, (unsigned)nblocks, PLACE_THREADS, smem, a);
