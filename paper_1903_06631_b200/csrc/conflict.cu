@@ -477,8 +477,13 @@ __device__ __forceinline__ int prof_effective(int ns, int4 sg, int32_t &a0, int3
 // than 2^31 intervals)
 __global__ void k_prof_intervals(int64_t nv, const int32_t *nseg, const int32_t *seg, const int64_t *size,
                                  int32_t *ea, int32_t *eb, int64_t *cnt, unsigned long long *hse,
-                                 unsigned long long *kmm) {
+                                 unsigned long long *kmm, int32_t *curs, int64_t ncurs,
+                                 unsigned long long *arena) {
   PDL_WAIT();
+  // scratch the later kernels of the build count into (no memsets)
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ncurs; i += (int64_t)gridDim.x * blockDim.x)
+    curs[i] = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *arena = 0;
   unsigned long long lmn = ~0ull, lmx = 0;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
     const int4 sg = reinterpret_cast<const int4 *>(seg)[v];
@@ -542,13 +547,16 @@ __global__ void k_prof_counts(int64_t n, const uint32_t *perm, const int32_t *ea
 }
 
 // row bounds from the slot scan, and the long-row scratch bound
-__global__ void k_prof_rows(int64_t nv, const int64_t *sub_off, int64_t *row_off, unsigned long long *need) {
+__global__ void k_prof_rows(int64_t nv, const int64_t *sub_off, int64_t *row_off, unsigned long long *need,
+                            int32_t *scur, int32_t *pcnt) {
   PDL_WAIT();
   unsigned long long s = 0;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v <= nv; v += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r0 = sub_off[2 * v];
     row_off[v] = r0;
     if (v < nv) {
+      scur[v] = 0;  // the fill's row cursors
+      pcnt[v] = 0;
       const int64_t d = sub_off[2 * v + 2] - r0;
       if (d > 128) {
         unsigned long long n2 = 64;
@@ -573,14 +581,14 @@ static int build_csr_profile(mp_ctx *ctx, mp_dprofile *P, mp_dgraph *g, mp_err *
   CUDA_TRY(hse.alloc(p + 2, st)); CUDA_TRY(pref.alloc(p + 2, st)); CUDA_TRY(curs.alloc(p + 1, st));
   CUDA_TRY(cnt.alloc(ns + 1, st)); CUDA_TRY(sub_off.alloc(ns + 1, st));
   CUDA_TRY(cudaMemsetAsync(hse.p, 0, (p + 2) * 8, st));
-  CUDA_TRY(cudaMemsetAsync(curs.p, 0, (p + 1) * 4, st));
   // d_small: [0..1] size-key range, [2] interval count, [3] arena need, [4] nnz
   unsigned long long *d_kmm = (unsigned long long *)ctx->d_small;
   int64_t *d_ni = ctx->d_small + 2;
   CUDA_TRY(cudaMemsetAsync(d_kmm, 0xff, 8, st));
   CUDA_TRY(cudaMemsetAsync(d_kmm + 1, 0, 8, st));
+  unsigned long long *d_arena = (unsigned long long *)(ctx->d_small + 3);
   LAUNCH(ctx, k_prof_intervals, grid_for(nv, 256, (int64_t)ctx->num_sms * 8), 256, 0, nv, P->nseg.p, P->seg.p,
-         P->size.p, ea.p, eb.p, cnt.p, (unsigned long long *)hse.p, d_kmm);
+         P->size.p, ea.p, eb.p, cnt.p, (unsigned long long *)hse.p, d_kmm, curs.p, p + 1, d_arena);
   int rc = dev_exclusive_scan<int64_t>(ctx, hse.p, pref.p, p + 2, d_ni, err);
   if (rc) return rc;
   int64_t h[3];
@@ -600,9 +608,8 @@ static int build_csr_profile(mp_ctx *ctx, mp_dprofile *P, mp_dgraph *g, mp_err *
   if (rc) return rc;
   CUDA_TRY(cudaMemcpyAsync(sub_off.p + ns, d_tot, 8, cudaMemcpyDeviceToDevice, st));
   CUDA_TRY(g->row_off.alloc(nv + 1, st));
-  unsigned long long *d_arena = (unsigned long long *)(ctx->d_small + 3);
-  CUDA_TRY(cudaMemsetAsync(d_arena, 0, 8, st));
-  LAUNCH(ctx, k_prof_rows, grid_for(nv + 1, 256, 2048), 256, 0, nv, sub_off.p, g->row_off.p, d_arena);
+  LAUNCH(ctx, k_prof_rows, grid_for(nv + 1, 256, 2048), 256, 0, nv, sub_off.p, g->row_off.p, d_arena, scur.p,
+         g->pcnt.p);
   int64_t h2[2];
   rc = dev_read_n(ctx, ctx->d_small + 3, h2, 16, err);
   if (rc) return rc;
@@ -610,8 +617,7 @@ static int build_csr_profile(mp_ctx *ctx, mp_dprofile *P, mp_dgraph *g, mp_err *
   g->nnz = h2[1];
   g->arena_need = h2[0];
   CUDA_TRY(g->col.alloc(g->nnz, st));
-  CUDA_TRY(cudaMemsetAsync(scur.p, 0, nv * 4, st));
-  CUDA_TRY(cudaMemsetAsync(g->pcnt.p, 0, nv * 4, st));
+
   delete tm;
   StageTimer fill(ctx, MP_ST_CONFLICT_FILL);
   LAUNCH(ctx, k_iv_fill, grid_for(ni * 32, 256, 148 * 64), 256, 0, ni, sv.p, g->row_off.p, g->pcnt.p, scur.p,
