@@ -12,6 +12,7 @@
 #include <string.h>
 
 #include <mutex>
+#include <memory>
 #include <vector>
 
 #include "../../include/memplan_b200.h"
@@ -54,6 +55,7 @@ struct mp_ctx {
   cudaEvent_t dims_ev = nullptr;
   // stage timing (CUDA events on `stream`)
   bool timing = false;
+  struct StageTimer *open_timer = nullptr;  // innermost running stage
   std::vector<mp_stage_rec> pending;
   std::vector<cudaEvent_t> spare;
   cudaEvent_t event() {
@@ -66,23 +68,39 @@ struct mp_ctx {
 
 #define CTX_GUARD(c) std::lock_guard<std::recursive_mutex> _ctx_guard((c)->mu)
 
-// RAII: brackets a stage with events on the context stream when timing is on
+// RAII: brackets a stage with events on the context stream when timing is on.
+// Stages nest exclusively: while an inner stage runs (the size-order sort
+// inside the conflict build) the outer one is paused, so per-stage times add
+// up to the step instead of counting the inner work twice.
 struct StageTimer {
   mp_ctx *c;
   int id;
   cudaEvent_t a = nullptr;
+  StageTimer *outer = nullptr;
   StageTimer(mp_ctx *c_, int id_) : c(c_), id(id_) {
     if (c->timing) {
-      a = c->event();
-      cudaEventRecord(a, c->stream);
+      outer = c->open_timer;
+      if (outer) outer->stop();
+      c->open_timer = this;
+      start();
     }
   }
+  void start() {
+    a = c->event();
+    cudaEventRecord(a, c->stream);
+  }
+  void stop() {
+    if (!a) return;
+    cudaEvent_t b = c->event();
+    cudaEventRecord(b, c->stream);
+    c->pending.push_back({id, a, b});
+    a = nullptr;
+  }
   ~StageTimer() {
-    if (a) {
-      cudaEvent_t b = c->event();
-      cudaEventRecord(b, c->stream);
-      c->pending.push_back({id, a, b});
-    }
+    if (c->open_timer != this) return;
+    stop();
+    c->open_timer = outer;
+    if (outer) outer->start();
   }
 };
 

@@ -319,7 +319,7 @@ static int build_csr(mp_ctx *ctx, int64_t nv, const int64_t *seg_off_d, const in
   // placement order first: the fill writes rows already split by it
   CUDA_TRY(g->rank.alloc(nv, st));
   CUDA_TRY(g->pcnt.alloc(nv, st));
-  StageTimer *tm = new StageTimer(ctx, MP_ST_CONFLICT_PREP);
+  std::unique_ptr<StageTimer> tm(new StageTimer(ctx, MP_ST_CONFLICT_PREP));
   DBuf<int64_t> ecnt, eoff;
   CUDA_TRY(ecnt.alloc(nv + 1, st));
   CUDA_TRY(eoff.alloc(nv + 1, st));
@@ -418,7 +418,7 @@ static int build_csr(mp_ctx *ctx, int64_t nv, const int64_t *seg_off_d, const in
   CUDA_TRY(g->col.alloc(nnz, st));
   CUDA_TRY(cudaMemsetAsync(scur.p, 0, nv * 4, st));
   CUDA_TRY(cudaMemsetAsync(g->pcnt.p, 0, nv * 4, st));
-  delete tm;
+  tm.reset();
   StageTimer fill(ctx, MP_ST_CONFLICT_FILL);
   LAUNCH(ctx, k_iv_fill, grid_for(ni * 32, 256, 148 * 64), 256, 0, ni, sv.p, g->row_off.p, g->pcnt.p, scur.p,
          g->col.p);
@@ -577,7 +577,7 @@ static int build_csr_profile(mp_ctx *ctx, mp_dprofile *P, mp_dgraph *g, mp_err *
   const int64_t nv = P->d.nvars, p = P->d.period, ns = 2 * nv;
   CUDA_TRY(g->rank.alloc(nv, st));
   CUDA_TRY(g->pcnt.alloc(nv, st));
-  StageTimer *tm = new StageTimer(ctx, MP_ST_CONFLICT_PREP);
+  std::unique_ptr<StageTimer> tm(new StageTimer(ctx, MP_ST_CONFLICT_PREP));
   DBuf<int32_t> ea, eb, curs, sv, scur;
   DBuf<int64_t> cnt, sub_off, hse, pref;
   CUDA_TRY(ea.alloc(ns, st)); CUDA_TRY(eb.alloc(ns, st));
@@ -621,7 +621,7 @@ static int build_csr_profile(mp_ctx *ctx, mp_dprofile *P, mp_dgraph *g, mp_err *
   g->arena_need = h2[0];
   CUDA_TRY(g->col.alloc(g->nnz, st));
 
-  delete tm;
+  tm.reset();
   StageTimer fill(ctx, MP_ST_CONFLICT_FILL);
   LAUNCH(ctx, k_iv_fill, grid_for(ni * 32, 256, 148 * 64), 256, 0, ni, sv.p, g->row_off.p, g->pcnt.p, scur.p,
          g->col.p);

@@ -672,7 +672,7 @@ extern "C" int mp_extract(mp_ctx *ctx, mp_dtrace *t, int64_t start, int64_t end,
   if (rc) return rc;
   cudaStream_t st = ctx->stream;
   int64_t p = end - start;
-  StageTimer *tm = new StageTimer(ctx, MP_ST_EXTRACT);
+  std::unique_ptr<StageTimer> tm(new StageTimer(ctx, MP_ST_EXTRACT));
   int32_t nv = t->nvars;
   DBuf<int32_t> owner, w_free, w_nacc, w_mcarry, is_malloc, win_ord, c_free, c_nacc, c_twin, c_surv,
       carry_ord, nmalloc;
@@ -775,7 +775,7 @@ extern "C" int mp_extract(mp_ctx *ctx, mp_dtrace *t, int64_t start, int64_t end,
   } else {
     LAUNCH(ctx, k_ex_times, grid_for(p, 256), 256, 0, t->t_us.p, start, end, P->op_times.p, d_dur);
   }
-  delete tm;
+  tm.reset();
   rc = profile_loads_async(ctx, P, err);
   if (rc) { delete P; return rc; }
   // peak, peak index, access count, period duration: copied to pinned

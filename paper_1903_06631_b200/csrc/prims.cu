@@ -255,6 +255,23 @@ constexpr int RS_BINS = 256;
 // look-back over earlier tiles (32-bit flag|count words), and scatter
 // through shared memory so global writes stay coalesced per digit run.
 
+// lanes of the warp holding the same digit (d < 1 << RB), among `valid` lanes
+template <int RB>
+__device__ __forceinline__ unsigned multisplit_peers(unsigned d, unsigned valid) {
+  unsigned peers = valid;
+#pragma unroll
+  for (int b = 0; b < RB; b++) {
+    const bool bit = (d >> b) & 1u;
+    const unsigned bb = __ballot_sync(FULL_MASK, bit);
+    peers &= bit ? bb : ~bb;
+  }
+  return peers;
+}
+
+#ifndef OS_MATCH
+#define OS_MATCH 0  // 1: rank with match.any
+#endif
+
 constexpr uint32_t OS_AGG = 1u << 30, OS_PFX = 2u << 30, OS_MASK = (1u << 30) - 1;
 constexpr int OS_MAX_PASSES = 8;
 
@@ -326,7 +343,13 @@ __global__ void __launch_bounds__(RS_THREADS) k_os_pass(const K *keys, const uin
   }
 #pragma unroll
   for (int i = 0; i < ITEMS; i++) {
+#if OS_MATCH
     unsigned peers = __match_any_sync(FULL_MASK, dig[i]);
+#else
+    // eight ballots instead of match.any (whose result latency dominated
+    // the pass's stalls)
+    unsigned peers = multisplit_peers<8>((unsigned)dig[i] & 0xffu, __ballot_sync(FULL_MASK, dig[i] < RS_BINS));
+#endif
     int rank = __popc(peers & lanemask_lt());
     int cnt = __popc(peers);
     int leader = __ffs(peers) - 1;
@@ -435,19 +458,6 @@ __global__ void __launch_bounds__(RS_THREADS) k_os_pass(const K *keys, const uin
 #define RS_ONESWEEP 0
 #endif
 
-// lanes of the warp holding the same digit (d < 1 << RB), among `valid` lanes
-template <int RB>
-__device__ __forceinline__ unsigned multisplit_peers(unsigned d, unsigned valid) {
-  unsigned peers = valid;
-#pragma unroll
-  for (int b = 0; b < RB; b++) {
-    const bool bit = (d >> b) & 1u;
-    const unsigned bb = __ballot_sync(FULL_MASK, bit);
-    peers &= bit ? bb : ~bb;
-  }
-  return peers;
-}
-
 template <typename K, int RB, int ITEMS>
 __global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const K *keys, int64_t n, int shift, int32_t ntiles,
                                                         int32_t *mat) {
@@ -501,12 +511,14 @@ __global__ void __launch_bounds__(RS_THREADS, RS_MINB) k_rs_scatter(const K *key
   constexpr int BINS = 1 << RB;
   constexpr int TILE = RS_THREADS * ITEMS;
   constexpr int PER_WARP = 32 * ITEMS;
+  // dynamic: the staged tile, then the per-warp digit counts and the tile's
+  // digit starts / global positions
   extern __shared__ __align__(16) unsigned char smem_raw[];
   K *sk = (K *)smem_raw;
   uint32_t *sv = (uint32_t *)(sk + TILE);
-  __shared__ int32_t whist[RS_WARPS][BINS];
-  __shared__ int32_t dstart[BINS];
-  __shared__ int32_t gpos[BINS];
+  int32_t(*whist)[BINS] = (int32_t(*)[BINS])(sv + TILE);
+  int32_t *dstart = &whist[RS_WARPS][0];
+  int32_t *gpos = dstart + BINS;
   __shared__ int32_t wtot[RS_WARPS];
 
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -633,7 +645,7 @@ static int radix_sort_rts(mp_ctx *ctx, const K *kin, const uint32_t *vin, K *kou
   const int need = passes > 1 ? 2 : (alias ? 1 : 0);
   if (need >= 1) { CUDA_TRY(ka.alloc(n, st)); CUDA_TRY(va.alloc(n, st)); }
   if (need >= 2 && passes > 2) { CUDA_TRY(kb.alloc(n, st)); CUDA_TRY(vb.alloc(n, st)); }
-  const size_t smem = (size_t)TILE * (sizeof(K) + sizeof(uint32_t));
+  const size_t smem = (size_t)TILE * (sizeof(K) + sizeof(uint32_t)) + (size_t)(RS_WARPS + 2) * BINS * sizeof(int32_t);
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(k_rs_scatter<K, RB, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
