@@ -534,9 +534,13 @@ __global__ void k_prof_scatter(int64_t nslots, const int32_t *ea, const int64_t 
 }
 
 // k_iv_counts_dense with the slot's variable implicit (slot >> 1)
-__global__ void k_prof_counts(int64_t n, const uint32_t *perm, const int32_t *ea, const int32_t *eb,
-                              const int64_t *pref, int64_t *cnt, const int32_t *rank, int32_t *sv) {
+// (the interval count is read on the device: the low half of the packed
+// start/end total; the rank column of sv is written by k_prof_sv_rank once
+// the size order exists)
+__global__ void k_prof_counts(const int64_t *d_ni, const uint32_t *perm, const int32_t *ea, const int32_t *eb,
+                              const int64_t *pref, int64_t *cnt, int32_t *sv) {
   PDL_WAIT();
+  const int64_t n = (int64_t)(uint32_t)*d_ni;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t iid = perm[k];
     const int64_t f = (int64_t)(uint32_t)pref[eb[iid]] - k - 1;       // starts before the end
@@ -544,9 +548,14 @@ __global__ void k_prof_counts(int64_t n, const uint32_t *perm, const int32_t *ea
     cnt[iid] = f + bw;
     const int32_t v = (int32_t)(iid >> 1);
     sv[3 * k] = v;
-    sv[3 * k + 1] = rank[v];
     sv[3 * k + 2] = (int32_t)f;
   }
+}
+
+__global__ void k_prof_sv_rank(int64_t n, const int32_t *rank, int32_t *sv) {
+  PDL_WAIT();
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+    sv[3 * k + 1] = rank[sv[3 * k]];
 }
 
 // row bounds from the slot scan, and the long-row scratch bound
@@ -594,18 +603,12 @@ static int build_csr_profile(mp_ctx *ctx, mp_dprofile *P, mp_dgraph *g, mp_err *
          P->size.p, ea.p, eb.p, cnt.p, (unsigned long long *)hse.p, d_kmm, curs.p, p + 1, d_arena);
   int rc = dev_exclusive_scan<int64_t>(ctx, hse.p, pref.p, p + 2, d_ni, err);
   if (rc) return rc;
-  int64_t h[3];
-  rc = dev_read_n(ctx, ctx->d_small, h, 24, err);
-  if (rc) return rc;
-  const int64_t ni = (int64_t)(uint32_t)h[2];  // low half of the packed total: the interval count
-  g->size_hi = (int64_t)(~(uint64_t)h[0] ^ 0x8000000000000000ull);
-  g->size_lo = (int64_t)(~(uint64_t)h[1] ^ 0x8000000000000000ull);
-  rc = placement_rank_sort(ctx, nv, g->size.p, nullptr, g->rank.p, (uint64_t)h[0], (uint64_t)h[1], err);
-  if (rc) return rc;
+  // everything up to the row bounds runs without the host: buffers indexed
+  // by sorted interval are sized for every slot that can hold one (ni <= ns)
   DBuf<uint32_t> perm;
-  CUDA_TRY(perm.alloc(ni, st)); CUDA_TRY(sv.alloc(3 * ni, st)); CUDA_TRY(scur.alloc(nv, st));
+  CUDA_TRY(perm.alloc(ns, st)); CUDA_TRY(sv.alloc(3 * ns, st)); CUDA_TRY(scur.alloc(nv, st));
   LAUNCH(ctx, k_prof_scatter, grid_for(ns, 256), 256, 0, ns, ea.p, pref.p, curs.p, perm.p);
-  LAUNCH(ctx, k_prof_counts, grid_for(ni, 256), 256, 0, ni, perm.p, ea.p, eb.p, pref.p, cnt.p, g->rank.p, sv.p);
+  LAUNCH(ctx, k_prof_counts, grid_for(ns, 256), 256, 0, d_ni, perm.p, ea.p, eb.p, pref.p, cnt.p, sv.p);
   int64_t *d_tot = ctx->d_small + 4;
   rc = dev_exclusive_scan<int64_t>(ctx, cnt.p, sub_off.p, ns, d_tot, err);
   if (rc) return rc;
@@ -613,13 +616,20 @@ static int build_csr_profile(mp_ctx *ctx, mp_dprofile *P, mp_dgraph *g, mp_err *
   CUDA_TRY(g->row_off.alloc(nv + 1, st));
   LAUNCH(ctx, k_prof_rows, grid_for(nv + 1, 256, 2048), 256, 0, nv, sub_off.p, g->row_off.p, d_arena, scur.p,
          g->pcnt.p);
-  int64_t h2[2];
-  rc = dev_read_n(ctx, ctx->d_small + 3, h2, 16, err);
+  // one readback: size-key range, interval count, long-row scratch, nnz
+  int64_t h[5];
+  rc = dev_read_n(ctx, ctx->d_small, h, 40, err);
   if (rc) return rc;
+  const int64_t ni = (int64_t)(uint32_t)h[2];  // low half of the packed total: the interval count
+  g->size_hi = (int64_t)(~(uint64_t)h[0] ^ 0x8000000000000000ull);
+  g->size_lo = (int64_t)(~(uint64_t)h[1] ^ 0x8000000000000000ull);
   g->nvars = nv;
-  g->nnz = h2[1];
-  g->arena_need = h2[0];
+  g->nnz = h[4];
+  g->arena_need = h[3];
   CUDA_TRY(g->col.alloc(g->nnz, st));
+  rc = placement_rank_sort(ctx, nv, g->size.p, nullptr, g->rank.p, (uint64_t)h[0], (uint64_t)h[1], err);
+  if (rc) return rc;
+  LAUNCH(ctx, k_prof_sv_rank, grid_for(ni, 256), 256, 0, ni, g->rank.p, sv.p);
 
   tm.reset();
   StageTimer fill(ctx, MP_ST_CONFLICT_FILL);
