@@ -37,7 +37,6 @@ extern "C" int mp_ctx_destroy(mp_ctx *c) {
   cudaStreamSynchronize(c->stream);
   cudaFreeHost(c->h_small);
   cudaFree(c->d_small);
-  if (c->scan_flags) cudaFree(c->scan_flags);
   if (c->scan_vals) cudaFree(c->scan_vals);
   if (c->scan_ctr) cudaFree(c->scan_ctr);
   if (c->copy) {

@@ -38,12 +38,11 @@ struct mp_ctx {
   // pinned host staging for small scalar readbacks
   int64_t *h_small = nullptr;
   int64_t *d_small = nullptr;
-  // single-pass scan state kept across calls (dev_exclusive_scan): tile
-  // flags tagged with a per-scan epoch, so no scan has to clear them first,
-  // per-tile aggregates / inclusive prefixes, and the tile-id counter (each
-  // scan consumes exactly its tile count from it)
-  int32_t *scan_flags = nullptr;
-  int64_t *scan_vals = nullptr;   // [2 * scan_cap]: aggregates, inclusive prefixes (int64 slots)
+  // single-pass scan state kept across calls (dev_exclusive_scan): per-tile
+  // aggregates / inclusive prefixes as value words tagged with a per-scan
+  // epoch, so no scan has to clear them first, and the tile-id counter
+  // (each scan consumes exactly its tile count from it)
+  int64_t *scan_vals = nullptr;   // [4 * scan_cap] 64-bit words (prims.cu k_scan_onepass)
   int32_t *scan_ctr = nullptr;
   int64_t scan_cap = 0;
   uint32_t scan_epoch = 0;

@@ -73,16 +73,50 @@ __device__ T block_excl_scan(T v, T *total) {
 // from a counter, publish their aggregate, then resolve their exclusive
 // prefix from predecessors (aggregate or inclusive prefix, whichever is
 // posted first) and post their own inclusive prefix.
+//
+// Posting carries no fence: every posted value travels in 64-bit words that
+// hold the scan's epoch in the high half and 32 bits of the value in the low
+// half (an int64 value takes two words), so a reader that sees the epoch in
+// a word has that word's half of the value — the word is its own flag.  A
+// word from an earlier scan carries another epoch and reads as "not
+// posted", so the words never need clearing.  words = [agg lo | agg hi |
+// pfx lo | pfx hi] x cap.
+template <typename T>
+__device__ __forceinline__ void scan_post(uint64_t *w, int64_t cap, int64_t tile, uint64_t tag, T v) {
+  if (sizeof(T) == 8) *(volatile uint64_t *)&w[cap + tile] = tag | (uint32_t)((uint64_t)(int64_t)v >> 32);
+  *(volatile uint64_t *)&w[tile] = tag | (uint32_t)(uint64_t)(int64_t)v;
+}
+
+// 0: nothing posted yet, 1: aggregate, 2: inclusive prefix (value in *v)
+template <typename T>
+__device__ __forceinline__ int scan_peek(const uint64_t *w, int64_t cap, int64_t q, uint64_t tag, T *v) {
+#pragma unroll
+  for (int st = 2; st >= 1; st--) {
+    const uint64_t *b = w + (int64_t)(st == 2 ? 2 : 0) * cap;
+    const uint64_t lo = *(volatile const uint64_t *)&b[q];
+    if ((lo & 0xffffffff00000000ull) != tag) continue;
+    if (sizeof(T) == 8) {
+      uint64_t hi;
+      do hi = *(volatile const uint64_t *)&b[cap + q];
+      while ((hi & 0xffffffff00000000ull) != tag);  // posted right after the low word
+      *v = (T)(int64_t)((hi << 32) | (uint32_t)lo);
+    } else {
+      *v = (T)(int32_t)(uint32_t)lo;
+    }
+    return st;
+  }
+  return 0;
+}
+
 template <typename T, bool INCL>
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan_onepass(const T *in, T *out, int64_t n, int32_t *flags,
-                                                               T *agg, T *incl, int32_t *tile_ctr, T *total,
-                                                               int32_t epoch, uint32_t tile_base) {
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_onepass(const T *in, T *out, int64_t n, uint64_t *words,
+                                                               int64_t cap, int32_t *tile_ctr, T *total,
+                                                               uint32_t epoch, uint32_t tile_base) {
   PDL_WAIT();
   __shared__ int32_t s_tile;
   __shared__ T s_excl, s_tot;
-  // flags hold (epoch << 2) | status: a value from an earlier scan reads as
-  // "not posted", so the flags never need clearing
-  const int32_t F_AGG = (epoch << 2) | 1, F_PFX = (epoch << 2) | 2;
+  const uint64_t tag = (uint64_t)epoch << 32;
+  uint64_t *const wagg = words, *const wpfx = words + 2 * cap;
   if (threadIdx.x == 0) s_tile = (int32_t)((uint32_t)atomicAdd(tile_ctr, 1) - tile_base);
   __syncthreads();
   const int64_t tile = s_tile;
@@ -118,39 +152,21 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_onepass(const T *in, T *o
     const T sum = s_tot;
     T excl = 0;
     if (tile == 0) {
-      if (lane == 0) {
-        incl[0] = sum;
-        __threadfence();
-        atomicExch(&flags[0], F_PFX);
-      }
+      if (lane == 0) scan_post<T>(wpfx, cap, 0, tag, sum);
     } else {
-      if (lane == 0) {
-        agg[tile] = sum;
-        __threadfence();
-        atomicExch(&flags[tile], F_AGG);
-      }
+      if (lane == 0) scan_post<T>(wagg, cap, tile, tag, sum);
       for (int64_t p = tile - 1;; p -= 32) {
-        int64_t q = p - lane;
-        int f = q >= 0 ? *(volatile int32_t *)&flags[q] : F_PFX;
-        if (f != F_AGG && f != F_PFX) f = 0;
-        while (__any_sync(FULL_MASK, f == 0))
-          if (f == 0) {
-            f = *(volatile int32_t *)&flags[q];
-            if (f != F_AGG && f != F_PFX) f = 0;
-          }
-        __threadfence();
-        unsigned pfx = __ballot_sync(FULL_MASK, f == F_PFX);
-        int stop = pfx ? __ffs(pfx) - 1 : 31;
+        const int64_t q = p - lane;
         T val = 0;
-        if (lane <= stop && q >= 0) val = f == F_PFX ? *(volatile T *)&incl[q] : *(volatile T *)&agg[q];
-        excl += warp_sum(val);
+        int st = q >= 0 ? scan_peek<T>(words, cap, q, tag, &val) : 2;
+        while (__any_sync(FULL_MASK, st == 0))
+          if (st == 0) st = scan_peek<T>(words, cap, q, tag, &val);
+        const unsigned pfx = __ballot_sync(FULL_MASK, st == 2);
+        const int stop = pfx ? __ffs(pfx) - 1 : 31;
+        excl += warp_sum(lane <= stop ? val : T(0));
         if (pfx) break;
       }
-      if (lane == 0) {
-        incl[tile] = excl + sum;
-        __threadfence();
-        atomicExch(&flags[tile], F_PFX);
-      }
+      if (lane == 0) scan_post<T>(wpfx, cap, tile, tag, excl + sum);
     }
     if (lane == 0) {
       s_excl = excl;
@@ -193,26 +209,23 @@ static int dev_scan(mp_ctx *ctx, const T *in, T *out, int64_t n, T *total, mp_er
   }
   int64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
   // persistent per-context flags / values / tile counter (see mp_ctx)
-  if (nb > ctx->scan_cap || ctx->scan_epoch >= (1u << 28)) {
+  if (nb > ctx->scan_cap || ctx->scan_epoch >= 0xfffffff0u) {
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    if (ctx->scan_flags) cudaFree(ctx->scan_flags);
     if (ctx->scan_vals) cudaFree(ctx->scan_vals);
     if (!ctx->scan_ctr) CUDA_TRY(cudaMalloc((void **)&ctx->scan_ctr, 16));
     int64_t cap = nb < 4096 ? 4096 : nb;
-    CUDA_TRY(cudaMalloc((void **)&ctx->scan_flags, cap * 4));
-    CUDA_TRY(cudaMalloc((void **)&ctx->scan_vals, 2 * cap * 8));
-    CUDA_TRY(cudaMemsetAsync(ctx->scan_flags, 0, cap * 4, ctx->stream));
+    CUDA_TRY(cudaMalloc((void **)&ctx->scan_vals, 4 * cap * 8));
+    CUDA_TRY(cudaMemsetAsync(ctx->scan_vals, 0, 4 * cap * 8, ctx->stream));
     CUDA_TRY(cudaMemsetAsync(ctx->scan_ctr, 0, 16, ctx->stream));
     ctx->scan_cap = cap;
     ctx->scan_epoch = 0;
     ctx->scan_base = 0;
   }
-  const int32_t epoch = (int32_t)++ctx->scan_epoch;
+  const uint32_t epoch = ++ctx->scan_epoch;
   const uint32_t base = ctx->scan_base;
   ctx->scan_base += (uint32_t)nb;
-  T *agg = (T *)ctx->scan_vals, *incl = (T *)(ctx->scan_vals + ctx->scan_cap);
-  LAUNCH(ctx, (k_scan_onepass<T, INCL>), (unsigned)nb, SCAN_THREADS, 0, in, out, n, ctx->scan_flags, agg, incl,
-         ctx->scan_ctr, total, epoch, base);
+  LAUNCH(ctx, (k_scan_onepass<T, INCL>), (unsigned)nb, SCAN_THREADS, 0, in, out, n, (uint64_t *)ctx->scan_vals,
+         ctx->scan_cap, ctx->scan_ctr, total, epoch, base);
   return MP_OK;
 }
 
