@@ -266,6 +266,8 @@ int dev_radix_sort_u64(mp_ctx *ctx, uint64_t *keys, uint32_t *vals, int64_t n, i
                        mp_err *err);
 // stable sort of kin's bits [0, bits) into kout, the positions 0..n-1 carried
 // into vout (kin may alias kout)
+int64_t dev_radix_rank_min_n();
+int dev_radix_rank_u32(mp_ctx *ctx, const uint32_t *kin, int64_t n, int bits, int32_t *rank, mp_err *err);
 int dev_radix_sort_u32_iota(mp_ctx *ctx, const uint32_t *kin, uint32_t *kout, uint32_t *vout, int64_t n, int bits,
                             mp_err *err);
 

@@ -644,7 +644,7 @@ __global__ void k_size_keys32(int64_t V, const int64_t *size, uint64_t kmin, uin
   PDL_WAIT();
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
     keys[v] = (uint32_t)(desc_size_key(size[v]) - kmin);
-    vals[v] = (uint32_t)v;
+    if (vals) vals[v] = (uint32_t)v;
   }
 }
 
@@ -657,6 +657,11 @@ int placement_rank_sort(mp_ctx *ctx, int64_t V, const int64_t *size, const int64
     // of 32-bit keys (a third less traffic per pass than the 64-bit path)
     DBuf<uint32_t> k32, order;
     CUDA_TRY(k32.alloc(V, st));
+    if (V >= dev_radix_rank_min_n() && bits_for(kmax - kmin) > 0) {
+      // the sort's last pass writes the ranks itself
+      LAUNCH(ctx, k_size_keys32, grid_for(V, 256), 256, 0, V, size, kmin, k32.p, (uint32_t *)nullptr);
+      return dev_radix_rank_u32(ctx, k32.p, V, bits_for(kmax - kmin), rank, err);
+    }
     CUDA_TRY(order.alloc(V, st));
     LAUNCH(ctx, k_size_keys32, grid_for(V, 256), 256, 0, V, size, kmin, k32.p, order.p);
     int rc = dev_radix_sort_u32(ctx, k32.p, order.p, V, bits_for(kmax - kmin), err);

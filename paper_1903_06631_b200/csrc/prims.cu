@@ -522,7 +522,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const K *keys, int64_t n
 template <typename K, int RB, int ITEMS>
 __global__ void __launch_bounds__(RS_THREADS, RS_MINB) k_rs_scatter(const K *keys, const uint32_t *vals, K *okeys,
                                                            uint32_t *ovals, int64_t n, int shift, int32_t ntiles,
-                                                           const int32_t *offs) {
+                                                           const int32_t *offs, int32_t *rank_out) {
   PDL_WAIT();
   constexpr int BINS = 1 << RB;
   constexpr int TILE = RS_THREADS * ITEMS;
@@ -619,8 +619,12 @@ __global__ void __launch_bounds__(RS_THREADS, RS_MINB) k_rs_scatter(const K *key
     const K key = sk[i];
     const unsigned d = (unsigned)(key >> shift) & (BINS - 1);
     const int64_t pos = (int64_t)gpos[d] + (i - dstart[d]);
-    okeys[pos] = key;
-    ovals[pos] = sv[i];
+    if (rank_out) {
+      rank_out[sv[i]] = (int32_t)pos;  // last pass of a ranking: each value's sorted position
+    } else {
+      okeys[pos] = key;
+      ovals[pos] = sv[i];
+    }
   }
 }
 
@@ -634,7 +638,7 @@ __global__ void k_rs_iota(uint32_t *v, int64_t n) {
 // nullptr sorts the positions 0..n-1.  kin/vin may alias kout/vout.
 template <typename K, int ITEMS>
 static int radix_sort_rts(mp_ctx *ctx, const K *kin, const uint32_t *vin, K *kout, uint32_t *vout, int64_t n,
-                          int bits, mp_err *err) {
+                          int bits, mp_err *err, int32_t *rank_out = nullptr) {
   constexpr int RB = 8, BINS = 1 << RB;
   constexpr int TILE = RS_THREADS * ITEMS;
   cudaStream_t st = ctx->stream;
@@ -681,15 +685,24 @@ static int radix_sort_rts(mp_ctx *ctx, const K *kin, const uint32_t *vin, K *kou
     int rc = dev_exclusive_scan<int32_t>(ctx, mat.p, mat.p, (int64_t)BINS * ntiles, nullptr, err);
     if (rc) return rc;
     LAUNCH(ctx, (k_rs_scatter<K, RB, ITEMS>), (unsigned)ntiles, RS_THREADS, smem, sk, sv, dk, dv, n, shift, ntiles,
-           mat.p);
+           mat.p, last ? rank_out : (int32_t *)nullptr);
     sk = dk;
     sv = dv;
   }
-  if (sk != kout) {
+  if (!rank_out && sk != kout) {
     CUDA_TRY(cudaMemcpyAsync(kout, sk, n * sizeof(K), cudaMemcpyDeviceToDevice, st));
     CUDA_TRY(cudaMemcpyAsync(vout, sv, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
   }
   return MP_OK;
+}
+
+// rank[i] = position of key i in the stable order of kin (bits [0, bits)),
+// the last pass scattering positions instead of keys and values; returns 1
+// (nothing done) below dev_radix_rank_min_n() keys
+int64_t dev_radix_rank_min_n() { return RS_RTS_MIN_N32; }
+int dev_radix_rank_u32(mp_ctx *ctx, const uint32_t *kin, int64_t n, int bits, int32_t *rank, mp_err *err) {
+  if (n < RS_RTS_MIN_N32 || bits <= 0) return 1;
+  return radix_sort_rts<uint32_t, RS_RTS_ITEMS32>(ctx, kin, nullptr, nullptr, nullptr, n, bits, err, rank);
 }
 
 int dev_radix_sort_u32_iota(mp_ctx *ctx, const uint32_t *kin, uint32_t *kout, uint32_t *vout, int64_t n, int bits,
