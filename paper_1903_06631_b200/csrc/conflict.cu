@@ -481,7 +481,7 @@ __device__ __forceinline__ int prof_effective(int ns, int4 sg, int32_t &a0, int3
 __global__ void k_prof_intervals(int64_t nv, const int32_t *nseg, const int32_t *seg, const int64_t *size,
                                  int32_t *ea, int32_t *eb, int64_t *cnt, unsigned long long *hse,
                                  unsigned long long *kmm, int32_t *curs, int64_t ncurs,
-                                 unsigned long long *arena) {
+                                 unsigned long long *arena, unsigned long long *cells, unsigned int *finished) {
   PDL_WAIT();
   // scratch the later kernels of the build count into (no memsets)
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ncurs; i += (int64_t)gridDim.x * blockDim.x)
@@ -508,9 +508,10 @@ __global__ void k_prof_intervals(int64_t nv, const int32_t *nseg, const int32_t 
     lmn = x < lmn ? x : lmn;
     lmx = y > lmx ? y : lmx;
   }
-  // one pair of global atomics per block (every warp on the same two
-  // addresses serialises in L2)
+  // per-block pairs, reduced by the last block to finish (the range needs
+  // no initialised cell, so no memset ahead of the kernel)
   __shared__ unsigned long long smn[32], smx[32];
+  __shared__ bool last;
   const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   if ((threadIdx.x & 31) == 0) { smn[w] = lmn; smx[w] = lmx; }
   __syncthreads();
@@ -519,8 +520,39 @@ __global__ void k_prof_intervals(int64_t nv, const int32_t *nseg, const int32_t 
       lmn = smn[i] < lmn ? smn[i] : lmn;
       lmx = smx[i] > lmx ? smx[i] : lmx;
     }
-    atomicMin(&kmm[0], lmn);
-    atomicMax(&kmm[1], lmx);
+    cells[blockIdx.x] = lmn;
+    cells[gridDim.x + blockIdx.x] = lmx;
+    __threadfence();
+    last = atomicAdd(finished, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  lmn = ~0ull;
+  lmx = 0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+    const unsigned long long x = *(volatile unsigned long long *)&cells[b];
+    const unsigned long long y = *(volatile unsigned long long *)&cells[gridDim.x + b];
+    lmn = x < lmn ? x : lmn;
+    lmx = y > lmx ? y : lmx;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long x = __shfl_xor_sync(FULL_MASK, lmn, o), y = __shfl_xor_sync(FULL_MASK, lmx, o);
+    lmn = x < lmn ? x : lmn;
+    lmx = y > lmx ? y : lmx;
+  }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) { smn[w] = lmn; smx[w] = lmx; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < nw; i++) {
+      lmn = smn[i] < lmn ? smn[i] : lmn;
+      lmx = smx[i] > lmx ? smx[i] : lmx;
+    }
+    kmm[0] = lmn;
+    kmm[1] = lmx;
+    *finished = 0;  // ready for the next build
   }
 }
 
@@ -559,17 +591,18 @@ __global__ void k_prof_sv_rank(int64_t n, const int32_t *rank, int32_t *sv) {
 }
 
 // row bounds from the slot scan, and the long-row scratch bound
-__global__ void k_prof_rows(int64_t nv, const int64_t *sub_off, int64_t *row_off, unsigned long long *need,
-                            int32_t *scur, int32_t *pcnt) {
+// (sub_off has 2 nv entries; its total, the slot scan's, is read from *tot)
+__global__ void k_prof_rows(int64_t nv, const int64_t *sub_off, const int64_t *tot, int64_t *row_off,
+                            unsigned long long *need, int32_t *scur, int32_t *pcnt) {
   PDL_WAIT();
   unsigned long long s = 0;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v <= nv; v += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r0 = sub_off[2 * v];
+    const int64_t r0 = v < nv ? sub_off[2 * v] : *tot;
     row_off[v] = r0;
     if (v < nv) {
       scur[v] = 0;  // the fill's row cursors
       pcnt[v] = 0;
-      const int64_t d = sub_off[2 * v + 2] - r0;
+      const int64_t d = (v + 1 < nv ? sub_off[2 * v + 2] : *tot) - r0;
       if (d > 128) {
         unsigned long long n2 = 64;
         while (n2 < (unsigned long long)d) n2 <<= 1;
@@ -596,11 +629,12 @@ static int build_csr_profile(mp_ctx *ctx, mp_dprofile *P, mp_dgraph *g, mp_err *
   // d_small: [0..1] size-key range, [2] interval count, [3] arena need, [4] nnz
   unsigned long long *d_kmm = (unsigned long long *)ctx->d_small;
   int64_t *d_ni = ctx->d_small + 2;
-  CUDA_TRY(cudaMemsetAsync(d_kmm, 0xff, 8, st));
-  CUDA_TRY(cudaMemsetAsync(d_kmm + 1, 0, 8, st));
   unsigned long long *d_arena = (unsigned long long *)(ctx->d_small + 3);
-  LAUNCH(ctx, k_prof_intervals, grid_for(nv, 256, (int64_t)ctx->num_sms * 8), 256, 0, nv, P->nseg.p, P->seg.p,
-         P->size.p, ea.p, eb.p, cnt.p, (unsigned long long *)hse.p, d_kmm, curs.p, p + 1, d_arena);
+  const unsigned ib = grid_for(nv, 256, (int64_t)ctx->num_sms * 8);
+  DBuf<unsigned long long> kcells;
+  CUDA_TRY(kcells.alloc(2 * (int64_t)ib, st));
+  LAUNCH(ctx, k_prof_intervals, ib, 256, 0, nv, P->nseg.p, P->seg.p, P->size.p, ea.p, eb.p, cnt.p,
+         (unsigned long long *)hse.p, d_kmm, curs.p, p + 1, d_arena, kcells.p, (unsigned int *)(ctx->d_small + 62));
   int rc = dev_exclusive_scan<int64_t>(ctx, hse.p, pref.p, p + 2, d_ni, err);
   if (rc) return rc;
   // everything up to the row bounds runs without the host: buffers indexed
@@ -612,10 +646,9 @@ static int build_csr_profile(mp_ctx *ctx, mp_dprofile *P, mp_dgraph *g, mp_err *
   int64_t *d_tot = ctx->d_small + 4;
   rc = dev_exclusive_scan<int64_t>(ctx, cnt.p, sub_off.p, ns, d_tot, err);
   if (rc) return rc;
-  CUDA_TRY(cudaMemcpyAsync(sub_off.p + ns, d_tot, 8, cudaMemcpyDeviceToDevice, st));
   CUDA_TRY(g->row_off.alloc(nv + 1, st));
-  LAUNCH(ctx, k_prof_rows, grid_for(nv + 1, 256, 2048), 256, 0, nv, sub_off.p, g->row_off.p, d_arena, scur.p,
-         g->pcnt.p);
+  LAUNCH(ctx, k_prof_rows, grid_for(nv + 1, 256, 2048), 256, 0, nv, sub_off.p, d_tot, g->row_off.p, d_arena,
+         scur.p, g->pcnt.p);
   // one readback: size-key range, interval count, long-row scratch, nnz
   int64_t h[5];
   rc = dev_read_n(ctx, ctx->d_small, h, 40, err);
