@@ -636,10 +636,33 @@ __global__ void k_rs_iota(uint32_t *v, int64_t n) {
 
 // stable sort of (kin, vin) on key bits [0, bits) into (kout, vout); vin ==
 // nullptr sorts the positions 0..n-1.  kin/vin may alias kout/vout.
+#ifndef RS_RTS_MAXRB
+#define RS_RTS_MAXRB 10  // widest digit of a reduce-then-scan pass: 20-bit ids sort in 2 passes (8: 3 passes, same time; 11: 35 % slower)
+#endif
+
+// one reduce-then-scan pass with RB-bit digits (the digit is masked to w bits)
+template <typename K, int RB, int ITEMS>
+static int rts_pass(mp_ctx *ctx, const K *sk, const uint32_t *sv, K *dk, uint32_t *dv, int64_t n, int shift,
+                    int32_t ntiles, int32_t *mat, int32_t *rank_out, mp_err *err) {
+  constexpr int BINS = 1 << RB;
+  constexpr int TILE = RS_THREADS * ITEMS;
+  const size_t smem = (size_t)TILE * (sizeof(K) + sizeof(uint32_t)) + (size_t)(RS_WARPS + 2) * BINS * sizeof(int32_t);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_rs_scatter<K, RB, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_set = true;
+  }
+  LAUNCH(ctx, (k_rs_hist<K, RB, ITEMS>), (unsigned)ntiles, RS_THREADS, 0, sk, n, shift, ntiles, mat);
+  int rc = dev_exclusive_scan<int32_t>(ctx, mat, mat, (int64_t)BINS * ntiles, nullptr, err);
+  if (rc) return rc;
+  LAUNCH(ctx, (k_rs_scatter<K, RB, ITEMS>), (unsigned)ntiles, RS_THREADS, smem, sk, sv, dk, dv, n, shift, ntiles,
+         (const int32_t *)mat, rank_out);
+  return MP_OK;
+}
+
 template <typename K, int ITEMS>
 static int radix_sort_rts(mp_ctx *ctx, const K *kin, const uint32_t *vin, K *kout, uint32_t *vout, int64_t n,
                           int bits, mp_err *err, int32_t *rank_out = nullptr) {
-  constexpr int RB = 8, BINS = 1 << RB;
   constexpr int TILE = RS_THREADS * ITEMS;
   cudaStream_t st = ctx->stream;
   if (n <= 0) return MP_OK;
@@ -647,7 +670,8 @@ static int radix_sort_rts(mp_ctx *ctx, const K *kin, const uint32_t *vin, K *kou
     mp_set_err(err, MP_E_UNSUPPORTED, 0, n, 0, "radix sort of more than 2^31 keys");
     return MP_E_UNSUPPORTED;
   }
-  const int passes = bits <= 0 ? 0 : (bits + RB - 1) / RB;
+  // as few passes as RS_RTS_MAXRB-bit digits allow, the bits split evenly
+  const int passes = bits <= 0 ? 0 : (bits + RS_RTS_MAXRB - 1) / RS_RTS_MAXRB;
   if (passes == 0) {
     if (kout != kin) CUDA_TRY(cudaMemcpyAsync(kout, kin, n * sizeof(K), cudaMemcpyDeviceToDevice, st));
     if (!vin) LAUNCH(ctx, k_rs_iota, grid_for(n, 256), 256, 0, vout, n);
@@ -657,21 +681,19 @@ static int radix_sort_rts(mp_ctx *ctx, const K *kin, const uint32_t *vin, K *kou
   const int32_t ntiles = (int32_t)((n + TILE - 1) / TILE);
   DBuf<K> ka, kb;
   DBuf<uint32_t> va, vb;
+  const int wbase = bits / passes, wextra = bits % passes;  // the first wextra passes take one bit more
+  const int wmax = wbase + (wextra ? 1 : 0);
+  const int rbmax = wmax <= 8 ? 8 : wmax <= 10 ? 10 : 11;
   DBuf<int32_t> mat;
-  CUDA_TRY(mat.alloc((int64_t)BINS * ntiles, st));
+  CUDA_TRY(mat.alloc((int64_t)ntiles << rbmax, st));
   const bool alias = kout == kin || (vin && vout == vin);
   // pass p reads src and writes dst; the last pass writes the caller's
   // output unless it aliases the input of a single pass
   const int need = passes > 1 ? 2 : (alias ? 1 : 0);
   if (need >= 1) { CUDA_TRY(ka.alloc(n, st)); CUDA_TRY(va.alloc(n, st)); }
   if (need >= 2 && passes > 2) { CUDA_TRY(kb.alloc(n, st)); CUDA_TRY(vb.alloc(n, st)); }
-  const size_t smem = (size_t)TILE * (sizeof(K) + sizeof(uint32_t)) + (size_t)(RS_WARPS + 2) * BINS * sizeof(int32_t);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_rs_scatter<K, RB, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr_set = true;
-  }
   const K *sk = kin;
+  int shift = 0;
   const uint32_t *sv = vin;
   for (int p = 0; p < passes; p++) {
     K *dk;
@@ -680,12 +702,15 @@ static int radix_sort_rts(mp_ctx *ctx, const K *kin, const uint32_t *vin, K *kou
     if (last && !(passes == 1 && alias)) { dk = kout; dv = vout; }
     else if ((p & 1) == 0) { dk = ka.p; dv = va.p; }
     else { dk = kb.p; dv = vb.p; }
-    const int shift = RB * p;
-    LAUNCH(ctx, (k_rs_hist<K, RB, ITEMS>), (unsigned)ntiles, RS_THREADS, 0, sk, n, shift, ntiles, mat.p);
-    int rc = dev_exclusive_scan<int32_t>(ctx, mat.p, mat.p, (int64_t)BINS * ntiles, nullptr, err);
+    // a pass of w bits reads digits (k >> shift) & (2^RB - 1): bits above
+    // shift + w are zero in the key range (or sorted by a later pass)
+    const int w = wbase + (p < wextra ? 1 : 0);
+    int32_t *ro = last ? rank_out : (int32_t *)nullptr;
+    int rc = w <= 8    ? rts_pass<K, 8, ITEMS>(ctx, sk, sv, dk, dv, n, shift, ntiles, mat.p, ro, err)
+             : w <= 10 ? rts_pass<K, 10, ITEMS>(ctx, sk, sv, dk, dv, n, shift, ntiles, mat.p, ro, err)
+                       : rts_pass<K, 11, ITEMS>(ctx, sk, sv, dk, dv, n, shift, ntiles, mat.p, ro, err);
     if (rc) return rc;
-    LAUNCH(ctx, (k_rs_scatter<K, RB, ITEMS>), (unsigned)ntiles, RS_THREADS, smem, sk, sv, dk, dv, n, shift, ntiles,
-           mat.p, last ? rank_out : (int32_t *)nullptr);
+    shift += w;
     sk = dk;
     sv = dv;
   }
