@@ -111,6 +111,7 @@ class PoolPlan:
         self._offsets = offsets
         self._sizes = sizes
         self._cols = None  # (names, offsets array, sizes array)
+        self._fp = None    # the FlatProfile those names came from
 
     def _build(self):
         names, off, size = self._cols
@@ -217,9 +218,8 @@ def build_conflict_graph(profile: IterationProfile) -> ConflictGraph:
 
     def fp():
         if "fp" not in snap:
-            own = profile.__dict__.get("_flat")
-            if own is not None and profile.__dict__.get("_dev") is dp:
-                snap["fp"] = own
+            if profile.__dict__.get("_dev") is dp and (profile._flat is not None or profile._arrays is not None):
+                snap["fp"] = profile._flat_profile()  # shared with the profile (and its lookup table)
             else:
                 snap["fp"] = N.download_profile(dp, arrays.names, arrays.name_blob, arrays.name_off, window)
         return snap["fp"]
@@ -232,6 +232,7 @@ def build_conflict_graph(profile: IterationProfile) -> ConflictGraph:
                 for i, (name, size, alloc) in enumerate(zip(f.var_names(), f.size.tolist(), f.alloc.tolist()))]
     g._vars_fn = make_vars
     g._names_fn = lambda: fp().var_names()
+    g._fp_fn = fp
     g._sizes_fn = lambda: fp().size
     return g
 
@@ -290,6 +291,7 @@ def plan_pool(graph: ConflictGraph, policy: str = "best_fit") -> PoolPlan:
                     peak_load_bytes=graph.peak_load_bytes)
     names, sizes = _graph_names_sizes(graph)
     plan._cols = (names, offs, sizes)
+    plan._fp = graph._fp_fn() if getattr(graph, "_fp_fn", None) is not None and graph._vars is None else None
     plan._levels = _levels
     return plan
 
@@ -368,29 +370,65 @@ def brute_force_optimal_footprint(graph: ConflictGraph, max_vars: int = 10) -> i
 
 
 class LookupTable:
-    """Window-relative malloc op index -> (var, pool offset) (smartpool.py:224-243)."""
+    """Window-relative malloc op index -> (var, pool offset) (smartpool.py:224-243).
 
-    def __init__(self, entries: dict[int, tuple[str, int]]):
-        self._entries = dict(entries)
+    Built either from a dict of entries (as the reference) or, by the column
+    path of make_lookup_table, from the selected variables' op indices, names
+    and offsets (an op -> row index array; the dict is built only if asked
+    for through ``items``-style iteration)."""
+
+    def __init__(self, entries: dict[int, tuple[str, int]] | None = None, _cols=None):
+        self._entries = dict(entries) if entries is not None else None
+        self._cols = _cols  # (ops int64 array, names list, offsets list, op -> row int64 array)
 
     def __len__(self) -> int:
-        return len(self._entries)
+        return len(self._entries) if self._entries is not None else len(self._cols[1])
 
-    def __contains__(self, op_index: int) -> bool:
-        return op_index in self._entries
+    def _row(self, op_index):
+        ops, _names, _offs, row = self._cols
+        try:
+            i = int(op_index)
+        except (TypeError, ValueError):
+            return -1
+        if i != op_index or not 0 <= i < row.shape[0]:
+            return -1
+        return int(row[i])
+
+    def __contains__(self, op_index) -> bool:
+        if self._entries is not None:
+            return op_index in self._entries
+        return self._row(op_index) >= 0
 
     def offset_for(self, op_index: int) -> int:
-        return self._entries[op_index][1]
+        if self._entries is not None:
+            return self._entries[op_index][1]
+        r = self._row(op_index)
+        if r < 0:
+            raise KeyError(op_index)
+        return self._cols[2][r]
 
     def var_for(self, op_index: int) -> str:
-        return self._entries[op_index][0]
+        if self._entries is not None:
+            return self._entries[op_index][0]
+        r = self._row(op_index)
+        if r < 0:
+            raise KeyError(op_index)
+        return self._cols[1][r]
 
     def items(self):
-        return sorted(self._entries.items())
+        if self._entries is not None:
+            return sorted(self._entries.items())
+        ops, names, offs, _row = self._cols
+        order = np.argsort(ops, kind="stable").tolist()
+        opl = ops.tolist()
+        return [(opl[i], (names[i], offs[i])) for i in order]
 
 
 def make_lookup_table(plan: PoolPlan, profile: IterationProfile) -> LookupTable:
     """Malloc op index -> offset for every window allocation (smartpool.py:246-254)."""
+    fast = _lookup_from_columns(plan, profile)
+    if fast is not None:
+        return fast
     offsets = plan.offsets
     entries = {}
     for v in profile.variables:
@@ -400,3 +438,37 @@ def make_lookup_table(plan: PoolPlan, profile: IterationProfile) -> LookupTable:
             raise MissingVariable(v.var)
         entries[v.alloc_index] = (v.var, offsets[v.var])
     return LookupTable(entries)
+
+
+def _lookup_from_columns(plan: PoolPlan, profile: IterationProfile):
+    """The lookup table straight from the columns both sides came from, when
+    neither the profile's variables nor the plan's offsets were ever handed
+    out as Python containers (so neither can have been edited) and the plan
+    names the profile's variables in the profile's order: the same entries
+    the per-variable loop builds, without a million VariableLifetime objects.
+    Returns None otherwise (the loop runs)."""
+    cols = getattr(plan, "_cols", None)
+    if cols is None or plan._offsets is not None or "variables" in profile.__dict__:
+        return None
+    if "variables" not in profile.__dict__.get("_pending", ()) or profile._dev is None:
+        return None
+    names, offs, _sizes = cols
+    fp = profile._flat_profile()
+    if getattr(plan, "_fp", None) is not fp:
+        # a plan of another snapshot: usable only if it names the same variables in order
+        pnames = fp.var_names()
+        if len(pnames) != len(names) or pnames != names:
+            return None
+    alloc = np.asarray(fp.alloc, np.int64)
+    sel = np.nonzero(alloc >= 0)[0]
+    ops = alloc[sel]
+    row = np.full(int(ops.max()) + 1 if ops.size else 0, -1, np.int64)
+    row[ops] = np.arange(ops.size, dtype=np.int64)
+    if ops.size and np.count_nonzero(row >= 0) != ops.size:
+        return None  # repeated op indices: the loop's last-wins dict decides
+    offl = np.asarray(offs)[sel].tolist()
+    if sel.size == len(names):
+        seln = names
+    else:
+        seln = [names[i] for i in sel.tolist()]
+    return LookupTable(_cols=(ops, seln, offl, row))

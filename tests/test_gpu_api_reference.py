@@ -292,6 +292,33 @@ def test_lookup_tables(mp):
         mp.make_lookup_table(empty, prof)
 
 
+def test_lookup_table_columns_match_loop(mp):
+    """make_lookup_table's column path (untouched profile and plan) builds the
+    entries the per-variable loop builds; an edited plan or a materialized
+    profile takes the loop (smartpool.py:246-254)."""
+    from paper_1903_06631_b200 import smartpool
+    for seed in (0, 3):
+        spec = mp.vgg_like(depth=6, scale=0.5, iterations=3, seed=seed)
+        t = mp.generate_synthetic_trace(spec)
+        win = mp.detect_iteration(t).window
+        prof = mp.extract_lifetimes(t, win)
+        plan = mp.plan_pool(mp.build_conflict_graph(prof), "best_fit")
+        fast = smartpool._lookup_from_columns(plan, prof)
+        assert fast is not None
+        prof2 = mp.extract_lifetimes(t, win)
+        plan2 = mp.plan_pool(mp.build_conflict_graph(prof2), "best_fit")
+        _ = prof2.variables  # materialized: the loop runs
+        assert smartpool._lookup_from_columns(plan2, prof2) is None
+        slow = mp.make_lookup_table(plan2, prof2)
+        assert fast.items() == slow.items() and len(fast) == len(slow)
+        # an edited plan is honoured
+        plan3 = mp.plan_pool(mp.build_conflict_graph(prof), "best_fit")
+        name = next(iter(plan3.offsets))
+        plan3.offsets[name] = 12345
+        t3 = mp.make_lookup_table(plan3, prof)
+        assert any(v == (name, 12345) for _, v in t3.items()) or name not in {v[0] for _, v in slow.items()}
+
+
 def test_replay_never_double_books_and_alpha(mp):
     for seed in (0, 4):
         spec = mp.vgg_like(depth=5, scale=0.4, iterations=4, seed=seed)
