@@ -153,14 +153,49 @@ class TraceArrays:
 
 
 def _events_to_arrays(events: Sequence[TraceEvent]) -> TraceArrays:
-    """Columns of a list of event objects.  The per-event work is C-level
-    iteration (attrgetter/map/fromiter); names are interned in first-seen
-    order with a dict, then only the distinct names are sorted."""
-    from operator import attrgetter
+    """Columns of a list of event objects: one C pass (csrc/evconv.c) when the
+    events are in the plain form, else C-level iteration (attrgetter/map/
+    fromiter); names are interned in first-seen order with a dict, then only
+    the distinct names are sorted."""
     n = len(events)
     if n == 0:
         return TraceArrays(np.zeros(0, np.uint8), np.zeros(0, np.int32), np.zeros(0, np.int64),
                            np.zeros(0, np.int64), [])
+    native = _native_columns(events, n)
+    if native is not None:
+        kind, size, t_us, index, first, ids = native
+    else:
+        kind, size, t_us, index, first, ids = _python_columns(events, n)
+    # the distinct positions are ranked by name
+    uniq = list(ids)
+    seen = np.fromiter(ids.values(), np.int64, count=len(uniq))
+    order = sorted(range(len(uniq)), key=uniq.__getitem__)
+    rank = np.empty(int(seen.max()) + 1, np.int32)
+    rank[seen[order]] = np.arange(len(uniq), dtype=np.int32)
+    var = rank[first]
+    contiguous = bool(np.array_equal(index, np.arange(n, dtype=np.int64)))
+    return TraceArrays(kind, var, size, t_us, [uniq[i] for i in order], None if contiguous else index)
+
+
+def _native_columns(events, n: int):
+    """One C pass over a list of events (csrc/evconv.c); None when the
+    extension is absent or any event is outside the plain form."""
+    if type(events) is not list:
+        return None
+    try:
+        from . import _evconv
+    except ImportError:
+        return None
+    kind = np.empty(n, np.uint8)
+    size, t_us, index, first = (np.empty(n, np.int64) for _ in range(4))
+    ids: dict[str, int] = {}
+    if _evconv.columns(events, KIND_CODE, ids, kind, size, t_us, index, first) is None:
+        return None
+    return kind, size, t_us, index, first, ids
+
+
+def _python_columns(events, n: int):
+    from operator import attrgetter
     code = KIND_CODE
     kinds = list(map(attrgetter("kind"), events))
     try:
@@ -171,17 +206,9 @@ def _events_to_arrays(events: Sequence[TraceEvent]) -> TraceArrays:
     t_us = np.fromiter(map(attrgetter("t_us"), events), np.int64, count=n)
     index = np.fromiter(map(attrgetter("index"), events), np.int64, count=n)
     ids: dict[str, int] = {}
+    # setdefault with the event position: a name keeps the position of its first event
     first = np.fromiter(map(ids.setdefault, map(attrgetter("var"), events), itertools.count()), np.int64, count=n)
-    # setdefault with the event position: a name keeps the position of its
-    # first event; the distinct positions are then ranked by name
-    uniq = list(ids)
-    seen = np.fromiter(ids.values(), np.int64, count=len(uniq))
-    order = sorted(range(len(uniq)), key=uniq.__getitem__)
-    rank = np.empty(int(seen.max()) + 1, np.int32)
-    rank[seen[order]] = np.arange(len(uniq), dtype=np.int32)
-    var = rank[first]
-    contiguous = bool(np.array_equal(index, np.arange(n, dtype=np.int64)))
-    return TraceArrays(kind, var, size, t_us, [uniq[i] for i in order], None if contiguous else index)
+    return kind, size, t_us, index, first, ids
 
 
 def _remember(trace: Trace, arrays: TraceArrays) -> None:

@@ -124,3 +124,34 @@ def test_parse_and_load_use_the_reader(tmp_path):
         path = tmp_path / f"t.{fmt}"
         T.save_trace(tr, path)
         same(T.load_trace_arrays(path), T.as_arrays(tr))
+
+
+def test_native_event_columns_match_python():
+    """csrc/evconv.c fills the same columns as the Python conversion, and any
+    event outside the plain form hands the whole list to the Python path
+    (same values, same errors)."""
+    import random
+    from paper_1903_06631_b200 import _evconv  # noqa: F401  (built by build())
+    rng = random.Random(3)
+    kinds = list(T.EventKind)
+    ev = [T.TraceEvent(i, rng.randrange(10 ** 6), kinds[rng.randrange(4)], f"v{rng.randrange(300)}",
+                       rng.randrange(1 << 40)) for i in range(5000)]
+    ev.append(T.TraceEvent(5000, 7, "free", "v1", True))  # plain str kind, bool size
+    native = T._native_columns(ev, len(ev))
+    assert native is not None
+    py = T._python_columns(ev, len(ev))
+    for x, y in zip(native[:5], py[:5]):
+        assert np.array_equal(x, y)
+    assert list(native[5].items()) == list(py[5].items())
+    a = T._events_to_arrays(ev)
+    odd = list(ev)
+    odd[10] = T.TraceEvent(10, odd[10].t_us, odd[10].kind, odd[10].var, np.int64(odd[10].size))
+    assert T._native_columns(odd, len(odd)) is None
+    b = T._events_to_arrays(odd)
+    for f in ("kind", "var", "size", "t_us"):
+        assert np.array_equal(getattr(a, f), getattr(b, f))
+    assert a.names == b.names
+    bad = list(ev)
+    bad[3] = T.TraceEvent(3, 0, "bogus", "v1", 1)
+    with pytest.raises(ValueError):
+        T._events_to_arrays(bad)
