@@ -54,3 +54,32 @@ def test_config4_full_size_matches_oracle_and_reference(workload, oracle_profile
     got = np.asarray(plan.offsets)
     assert got.shape == offs.shape
     assert hashlib.sha256(got.tobytes()).hexdigest() == hashlib.sha256(offs.tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("accesses,max_size", [(True, 64 << 20), (False, 256 << 20)])
+def test_config4_full_size_variants_match_oracle(accesses, max_size):
+    """The same 1 M-variable shape with a write after every malloc and a read
+    before every free (6 M events: the access-extraction path at full size),
+    and with sizes up to 256 MiB (a ~7.5 GB pool: the 64-bit placement
+    kernel), offset for offset against the oracle."""
+    import oracle as orc
+    from paper_1903_06631_b200 import workloads
+    from paper_1903_06631_b200.pipeline import plan_arrays
+    arrays, window = workloads.interval_trace(1_000_000, seed=1, accesses=accesses, max_size=max_size)
+    plan = plan_arrays(arrays, policy="best_fit")
+    assert plan.period == window[1] - window[0]
+    rc, fp = orc.extract(arrays, window[0], window[1])
+    assert rc == 0
+    off, lo, hi = orc.profile_segments(fp)
+    h, row, _col = orc.conflict(off, lo, hi)
+    try:
+        assert plan.nvars == fp.nvars and plan.peak_bytes == fp.peak_bytes
+        assert plan.nnz == int(row[-1])
+        rc, offs, foot = orc.plan(h, fp.size, fp.alloc.astype(np.int64), fp.base, fp.name_ralloc(), fp.name_blob,
+                                  fp.name_off, 1)
+        assert rc == 0 and plan.footprint_bytes == foot
+        if max_size > (64 << 20):
+            assert plan.peak_bytes > (1 << 31)
+        assert np.array_equal(np.asarray(plan.offsets), offs)
+    finally:
+        orc.graph_free(h)
