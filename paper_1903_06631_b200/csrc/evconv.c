@@ -27,6 +27,49 @@ static int get_i64(PyObject *o, int64_t *out) {
   return 0;
 }
 
+/* one event into row i; 1 on success, 0 when it is outside the plain form */
+static int convert_one(PyObject *ev, Py_ssize_t i, PyObject *code, PyObject *ids, uint8_t *kind, int64_t *size,
+                       int64_t *t_us, int64_t *index, int64_t *first, PyObject *a_index, PyObject *a_t,
+                       PyObject *a_kind, PyObject *a_var, PyObject *a_size) {
+  PyObject *o;
+  int64_t v;
+  /* index, t_us, size */
+  o = PyObject_GetAttr(ev, a_index);
+  if (!o || get_i64(o, &v)) { Py_XDECREF(o); return 0; }
+  Py_DECREF(o);
+  index[i] = v;
+  o = PyObject_GetAttr(ev, a_t);
+  if (!o || get_i64(o, &v)) { Py_XDECREF(o); return 0; }
+  Py_DECREF(o);
+  t_us[i] = v;
+  o = PyObject_GetAttr(ev, a_size);
+  if (!o || get_i64(o, &v)) { Py_XDECREF(o); return 0; }
+  Py_DECREF(o);
+  size[i] = v;
+  /* kind through the code table */
+  o = PyObject_GetAttr(ev, a_kind);
+  if (!o) return 0;
+  PyObject *c = PyDict_GetItemWithError(code, o);
+  Py_DECREF(o);
+  if (!c || get_i64(c, &v) || v < 0 || v > 255) return 0;
+  kind[i] = (uint8_t)v;
+  /* name: first position that named it */
+  o = PyObject_GetAttr(ev, a_var);
+  if (!o || !PyUnicode_Check(o)) { Py_XDECREF(o); return 0; }
+  PyObject *pos = PyDict_GetItemWithError(ids, o);
+  if (pos) {
+    if (get_i64(pos, &v)) { Py_DECREF(o); return 0; }
+    first[i] = v;
+  } else {
+    PyObject *pi = PyErr_Occurred() ? NULL : PyLong_FromSsize_t(i);
+    if (!pi || PyDict_SetItem(ids, o, pi) < 0) { Py_XDECREF(pi); Py_DECREF(o); return 0; }
+    Py_DECREF(pi);
+    first[i] = (int64_t)i;
+  }
+  Py_DECREF(o);
+  return 1;
+}
+
 /* columns(events, kind_code, ids, kind_u8, size_i64, t_us_i64, index_i64, first_i64) -> True | None */
 static PyObject *columns(PyObject *self, PyObject *args) {
   (void)self;
@@ -55,43 +98,12 @@ static PyObject *columns(PyObject *self, PyObject *args) {
     PyObject *a_size = PyUnicode_InternFromString("size");
     int ok = a_index && a_t && a_kind && a_var && a_size;
     for (Py_ssize_t i = 0; ok && i < n; i++) {
+      /* an attribute getter may run Python code: re-check the list and hold the event */
+      if (PyList_GET_SIZE(events) != n) { ok = 0; break; }
       PyObject *ev = PyList_GET_ITEM(events, i);
-      PyObject *o;
-      int64_t v;
-      /* index, t_us, size */
-      o = PyObject_GetAttr(ev, a_index);
-      if (!o || get_i64(o, &v)) { Py_XDECREF(o); ok = 0; break; }
-      Py_DECREF(o);
-      index[i] = v;
-      o = PyObject_GetAttr(ev, a_t);
-      if (!o || get_i64(o, &v)) { Py_XDECREF(o); ok = 0; break; }
-      Py_DECREF(o);
-      t_us[i] = v;
-      o = PyObject_GetAttr(ev, a_size);
-      if (!o || get_i64(o, &v)) { Py_XDECREF(o); ok = 0; break; }
-      Py_DECREF(o);
-      size[i] = v;
-      /* kind through the code table */
-      o = PyObject_GetAttr(ev, a_kind);
-      if (!o) { ok = 0; break; }
-      PyObject *c = PyDict_GetItemWithError(code, o);
-      Py_DECREF(o);
-      if (!c || get_i64(c, &v) || v < 0 || v > 255) { ok = 0; break; }
-      kind[i] = (uint8_t)v;
-      /* name: first position that named it */
-      o = PyObject_GetAttr(ev, a_var);
-      if (!o || !PyUnicode_Check(o)) { Py_XDECREF(o); ok = 0; break; }
-      PyObject *pos = PyDict_GetItemWithError(ids, o);
-      if (pos) {
-        if (get_i64(pos, &v)) { Py_DECREF(o); ok = 0; break; }
-        first[i] = v;
-      } else {
-        PyObject *pi = PyErr_Occurred() ? NULL : PyLong_FromSsize_t(i);
-        if (!pi || PyDict_SetItem(ids, o, pi) < 0) { Py_XDECREF(pi); Py_DECREF(o); ok = 0; break; }
-        Py_DECREF(pi);
-        first[i] = (int64_t)i;
-      }
-      Py_DECREF(o);
+      Py_INCREF(ev);
+      ok = convert_one(ev, i, code, ids, kind, size, t_us, index, first, a_index, a_t, a_kind, a_var, a_size);
+      Py_DECREF(ev);
     }
     Py_XDECREF(a_index); Py_XDECREF(a_t); Py_XDECREF(a_kind); Py_XDECREF(a_var); Py_XDECREF(a_size);
     for (int k = 0; k < 5; k++) PyBuffer_Release(&view[k]);
