@@ -374,18 +374,26 @@ class LookupTable:
 
     Built either from a dict of entries (as the reference) or, by the column
     path of make_lookup_table, from the selected variables' op indices, names
-    and offsets (an op -> row index array; the dict is built only if asked
-    for through ``items``-style iteration)."""
+    and offsets (an op -> row index array); the reference's ``_entries`` dict
+    is materialized from the columns only if something asks for it."""
 
     def __init__(self, entries: dict[int, tuple[str, int]] | None = None, _cols=None):
-        self._entries = dict(entries) if entries is not None else None
+        self._dict = dict(entries) if entries is not None else None
         self._cols = _cols  # (ops int64 array, names list, offsets list, op -> row int64 array)
 
+    @property
+    def _entries(self) -> dict[int, tuple[str, int]]:
+        if self._dict is None:
+            ops, names, offs, _row = self._cols
+            self._dict = dict(zip(ops.tolist(), zip(names, offs)))
+            self._cols = None
+        return self._dict
+
     def __len__(self) -> int:
-        return len(self._entries) if self._entries is not None else len(self._cols[1])
+        return len(self._dict) if self._dict is not None else len(self._cols[1])
 
     def _row(self, op_index):
-        ops, _names, _offs, row = self._cols
+        _ops, _names, _offs, row = self._cols
         try:
             i = int(op_index)
         except (TypeError, ValueError):
@@ -395,29 +403,29 @@ class LookupTable:
         return int(row[i])
 
     def __contains__(self, op_index) -> bool:
-        if self._entries is not None:
-            return op_index in self._entries
+        if self._dict is not None:
+            return op_index in self._dict
         return self._row(op_index) >= 0
 
     def offset_for(self, op_index: int) -> int:
-        if self._entries is not None:
-            return self._entries[op_index][1]
+        if self._dict is not None:
+            return self._dict[op_index][1]
         r = self._row(op_index)
         if r < 0:
             raise KeyError(op_index)
         return self._cols[2][r]
 
     def var_for(self, op_index: int) -> str:
-        if self._entries is not None:
-            return self._entries[op_index][0]
+        if self._dict is not None:
+            return self._dict[op_index][0]
         r = self._row(op_index)
         if r < 0:
             raise KeyError(op_index)
         return self._cols[1][r]
 
     def items(self):
-        if self._entries is not None:
-            return sorted(self._entries.items())
+        if self._dict is not None:
+            return sorted(self._dict.items())
         ops, names, offs, _row = self._cols
         order = np.argsort(ops, kind="stable").tolist()
         opl = ops.tolist()

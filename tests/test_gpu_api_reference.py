@@ -311,6 +311,11 @@ def test_lookup_table_columns_match_loop(mp):
         assert smartpool._lookup_from_columns(plan2, prof2) is None
         slow = mp.make_lookup_table(plan2, prof2)
         assert fast.items() == slow.items() and len(fast) == len(slow)
+        some = next(iter(slow._entries))
+        assert some in fast and fast.offset_for(some) == slow.offset_for(some)
+        assert fast.var_for(some) == slow.var_for(some) and -1 not in fast and "x" not in fast
+        assert fast._entries == slow._entries  # the reference's dict, materialized on demand
+        assert fast.items() == slow.items()
         # an edited plan is honoured
         plan3 = mp.plan_pool(mp.build_conflict_graph(prof), "best_fit")
         name = next(iter(plan3.offsets))
