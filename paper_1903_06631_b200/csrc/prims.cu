@@ -637,7 +637,7 @@ __global__ void k_rs_iota(uint32_t *v, int64_t n) {
 // stable sort of (kin, vin) on key bits [0, bits) into (kout, vout); vin ==
 // nullptr sorts the positions 0..n-1.  kin/vin may alias kout/vout.
 #ifndef RS_RTS_MAXRB
-#define RS_RTS_MAXRB 10  // widest digit of a reduce-then-scan pass: 20-bit ids sort in 2 passes (8: 3 passes, same time; 11: 35 % slower)
+#define RS_RTS_MAXRB 10  // widest digit of a reduce-then-scan pass (config 4's 21-bit ids: 3 passes of 7 bits; 11: 2 passes, 35 % slower)
 #endif
 
 // one reduce-then-scan pass with RB-bit digits (the digit is masked to w bits)
