@@ -584,22 +584,25 @@ __global__ void __launch_bounds__(RS_THREADS, RS_MINB) k_rs_scatter(const K *key
     dstart[d] = run;
   }
   __syncthreads();
-  // exclusive scan of the tile's digit counts: each warp scans BINS / RS_WARPS
+  // exclusive scan of the tile's digit counts: SW warps scan BINS / SW each
   {
-    constexpr int PER = BINS / RS_WARPS;  // contiguous digits per warp (>= 32)
+    constexpr int SW = BINS >= 32 * RS_WARPS ? RS_WARPS : BINS / 32;  // scanning warps
+    constexpr int PER = BINS / SW;  // contiguous digits per scanning warp (>= 32)
     int32_t c = 0;
-    for (int ch = 0; ch < PER; ch += 32) {
-      const int d = w * PER + ch + lane;
-      const int32_t x = dstart[d];
-      const int32_t xi = warp_incl_scan_add(x);
-      dstart[d] = c + xi - x;
-      c += __shfl_sync(FULL_MASK, xi, 31);
-    }
+    if (w < SW)
+      for (int ch = 0; ch < PER; ch += 32) {
+        const int d = w * PER + ch + lane;
+        const int32_t x = dstart[d];
+        const int32_t xi = warp_incl_scan_add(x);
+        dstart[d] = c + xi - x;
+        c += __shfl_sync(FULL_MASK, xi, 31);
+      }
     if (lane == 0) wtot[w] = c;
     __syncthreads();
     int32_t add = 0;
     for (int ww = 0; ww < w; ww++) add += wtot[ww];
-    for (int ch = 0; ch < PER; ch += 32) dstart[w * PER + ch + lane] += add;
+    if (w < SW)
+      for (int ch = 0; ch < PER; ch += 32) dstart[w * PER + ch + lane] += add;
   }
   __syncthreads();
 #pragma unroll
@@ -636,6 +639,9 @@ __global__ void k_rs_iota(uint32_t *v, int64_t n) {
 
 // stable sort of (kin, vin) on key bits [0, bits) into (kout, vout); vin ==
 // nullptr sorts the positions 0..n-1.  kin/vin may alias kout/vout.
+#ifndef RS_RTS_EXACT_RB
+#define RS_RTS_EXACT_RB 1  // a 7- or 9-bit pass uses 128 / 512 bins (smaller digit matrix and tile scans)
+#endif
 #ifndef RS_RTS_MAXRB
 #define RS_RTS_MAXRB 10  // widest digit of a reduce-then-scan pass (config 4's 21-bit ids: 3 passes of 7 bits; 11: 2 passes, 35 % slower)
 #endif
@@ -683,7 +689,9 @@ static int radix_sort_rts(mp_ctx *ctx, const K *kin, const uint32_t *vin, K *kou
   DBuf<uint32_t> va, vb;
   const int wbase = bits / passes, wextra = bits % passes;  // the first wextra passes take one bit more
   const int wmax = wbase + (wextra ? 1 : 0);
-  const int rbmax = wmax <= 8 ? 8 : wmax <= 10 ? 10 : 11;
+  // digits as wide as the pass (RS_RTS_EXACT_RB), else rounded up to 8 / 10 / 11
+  auto rb_for = [](int w) { return RS_RTS_EXACT_RB ? (w <= 7 ? 7 : w) : (w <= 8 ? 8 : w <= 10 ? 10 : 11); };
+  const int rbmax = rb_for(wmax);
   DBuf<int32_t> mat;
   CUDA_TRY(mat.alloc((int64_t)ntiles << rbmax, st));
   const bool alias = kout == kin || (vin && vout == vin);
@@ -706,9 +714,14 @@ static int radix_sort_rts(mp_ctx *ctx, const K *kin, const uint32_t *vin, K *kou
     // shift + w are zero in the key range (or sorted by a later pass)
     const int w = wbase + (p < wextra ? 1 : 0);
     int32_t *ro = last ? rank_out : (int32_t *)nullptr;
-    int rc = w <= 8    ? rts_pass<K, 8, ITEMS>(ctx, sk, sv, dk, dv, n, shift, ntiles, mat.p, ro, err)
-             : w <= 10 ? rts_pass<K, 10, ITEMS>(ctx, sk, sv, dk, dv, n, shift, ntiles, mat.p, ro, err)
-                       : rts_pass<K, 11, ITEMS>(ctx, sk, sv, dk, dv, n, shift, ntiles, mat.p, ro, err);
+    int rc;
+    switch (rb_for(w)) {
+      case 7: rc = rts_pass<K, 7, ITEMS>(ctx, sk, sv, dk, dv, n, shift, ntiles, mat.p, ro, err); break;
+      case 8: rc = rts_pass<K, 8, ITEMS>(ctx, sk, sv, dk, dv, n, shift, ntiles, mat.p, ro, err); break;
+      case 9: rc = rts_pass<K, 9, ITEMS>(ctx, sk, sv, dk, dv, n, shift, ntiles, mat.p, ro, err); break;
+      case 10: rc = rts_pass<K, 10, ITEMS>(ctx, sk, sv, dk, dv, n, shift, ntiles, mat.p, ro, err); break;
+      default: rc = rts_pass<K, 11, ITEMS>(ctx, sk, sv, dk, dv, n, shift, ntiles, mat.p, ro, err); break;
+    }
     if (rc) return rc;
     shift += w;
     sk = dk;
